@@ -1,0 +1,178 @@
+// TEST INFRASTRUCTURE ONLY — a C-ABI wrapper around the UNMODIFIED reference
+// `dfamin` headers (compiled from /root/reference/proj/include by
+// oracle/Makefile into oracle/_ref/libdfamin_ref.so).  Used to pin the oracle
+// restatement (tests/golden/make_golden.py) and as bench.py's cpu_baseline /
+// `--impl reference` arm.  No reference source is copied: this file only
+// converts flat C buffers to the reference's types and calls its public API
+// (min_sort.hpp:72, min_partref.hpp:156/:170, min_transpr.hpp:59/:90,
+// min_trans.hpp:81, core.hpp:220, generators.hpp:36-145).
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "dfamin/dfamin.hpp"
+
+using namespace dfamin;
+
+namespace {
+
+struct RefStats {
+  uint64_t iterations;
+  uint64_t closure_steps;
+  double elapsed_ms;
+  uint64_t peak_memory_estimate;
+  int32_t status;
+};
+
+Dfa make(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc, uint32_t initial) {
+  Dfa d;
+  d.num_states = n;
+  d.alphabet_size = k;
+  d.delta.assign(k, std::vector<State>(n));
+  for (uint32_t a = 0; a < k; ++a) std::memcpy(d.delta[a].data(), delta + (size_t)a * n, 4ull * n);
+  d.accepting.assign(acc, acc + n);
+  d.initial = initial;
+  return d;
+}
+
+void out(const MinResult& r, uint32_t* block, uint32_t* nb, RefStats* st) {
+  if (r.stats.status == RunStatus::ok && block != nullptr)
+    std::memcpy(block, r.partition.block.data(), 4ull * r.partition.block.size());
+  if (nb) *nb = r.partition.num_blocks;
+  if (st) {
+    st->iterations = r.stats.iterations;
+    st->closure_steps = r.stats.closure_steps;
+    st->elapsed_ms = r.stats.elapsed_ms;
+    st->peak_memory_estimate = r.stats.peak_memory_estimate;
+    st->status = static_cast<int32_t>(r.stats.status);
+  }
+}
+
+substrate::RacePolicy policy_of(int p) {
+  switch (p) {
+    case 1: return substrate::RacePolicy::deterministic_min;
+    case 2: return substrate::RacePolicy::deterministic_max;
+    default: return substrate::RacePolicy::arbitrary_winner;
+  }
+}
+
+void copy_dfa(const Dfa& d, uint32_t* delta, uint8_t* acc) {
+  for (uint32_t a = 0; a < d.alphabet_size; ++a)
+    std::memcpy(delta + (size_t)a * d.num_states, d.delta[a].data(), 4ull * d.num_states);
+  std::memcpy(acc, d.accepting.data(), d.num_states);
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_set_threads(unsigned n) { substrate::set_worker_count(n); }
+unsigned ref_worker_count() { return substrate::worker_count(); }
+
+int ref_sort_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                int64_t timeout_ms, uint32_t* block, uint32_t* nb, RefStats* st,
+                uint32_t* trace_counts, uint32_t trace_cap) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  SortTrace trace;
+  SortOptions opt;
+  opt.timeout_ms = timeout_ms;
+  if (trace_counts) opt.trace = &trace;
+  out(sort_pr(d, opt), block, nb, st);
+  if (trace_counts)
+    for (size_t i = 0; i < trace.block_counts.size() && i < trace_cap; ++i)
+      trace_counts[i] = trace.block_counts[i];
+  return 0;
+}
+
+int ref_naive_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc, int policy,
+                 int fused_cas, int64_t timeout_ms, uint32_t* block, uint32_t* nb, RefStats* st) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  if (fused_cas) {
+    out(naive_pr_cas(d, timeout_ms), block, nb, st);
+  } else {
+    PrOptions opt;
+    opt.policy = policy_of(policy);
+    opt.timeout_ms = timeout_ms;
+    out(naive_pr(d, opt), block, nb, st);
+  }
+  return 0;
+}
+
+int ref_trans_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc, int policy,
+                 int64_t timeout_ms, uint64_t max_memory, uint32_t* block, uint32_t* nb,
+                 RefStats* st) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  PrOptions opt;
+  opt.policy = policy_of(policy);
+  opt.timeout_ms = timeout_ms;
+  Limits lim;
+  lim.max_memory_bytes = max_memory;
+  lim.timeout_ms = timeout_ms;
+  out(trans_pr(d, opt, lim), block, nb, st);
+  return 0;
+}
+
+int ref_expand_alphabet(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                        uint64_t max_memory, uint32_t* rows, uint32_t* levels, uint64_t* required) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  Limits lim;
+  lim.max_memory_bytes = max_memory;
+  try {
+    const ExpandedDfa e = expand_alphabet(d, lim);
+    *levels = e.levels;
+    *required = expand_required_bytes(n, k);
+    for (size_t r = 0; r < e.delta.size(); ++r)
+      std::memcpy(rows + r * n, e.delta[r].data(), 4ull * n);
+    return 0;
+  } catch (const CapacityError& err) {
+    *required = err.required_bytes();
+    return -2;
+  }
+}
+
+int ref_trans_minimize(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                       int64_t timeout_ms, uint64_t max_memory, uint32_t* block, uint32_t* nb,
+                       RefStats* st, uint8_t* apart, uint64_t* popcounts, uint32_t pop_cap) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  Limits lim;
+  lim.max_memory_bytes = max_memory;
+  lim.timeout_ms = timeout_ms;
+  TransInspect ins;
+  out(trans_minimize(d, lim, &ins), block, nb, st);
+  if (apart && !ins.apart.empty()) std::memcpy(apart, ins.apart.data(), ins.apart.size());
+  if (popcounts)
+    for (size_t i = 0; i < ins.apart_popcounts.size() && i < pop_cap; ++i)
+      popcounts[i] = ins.apart_popcounts[i];
+  return 0;
+}
+
+uint32_t ref_moore(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                   uint32_t* block, uint64_t* rounds) {
+  const Dfa d = make(n, k, delta, acc, 0);
+  RunStats st;
+  const Partition p = moore_oracle(d, &st);
+  std::memcpy(block, p.block.data(), 4ull * n);
+  if (rounds) *rounds = st.iterations;
+  return p.num_blocks;
+}
+
+uint32_t ref_canonicalize(const uint32_t* raw, uint32_t n, uint32_t* outp) {
+  const Partition p = canonicalize(std::vector<uint32_t>(raw, raw + n));
+  std::memcpy(outp, p.block.data(), 4ull * n);
+  return p.num_blocks;
+}
+
+// generators: n/k are known to the caller (fib_len etc. computed by the oracle)
+void ref_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double p, uint32_t* delta,
+                    uint8_t* acc) {
+  copy_dfa(random_dfa(n, k, seed, p), delta, acc);
+}
+void ref_fib_dfa(uint32_t idx, uint32_t* delta, uint8_t* acc) { copy_dfa(fib_dfa(idx), delta, acc); }
+void ref_bit_splitter(uint32_t bits, uint32_t* delta, uint8_t* acc) {
+  copy_dfa(bit_splitter(bits), delta, acc);
+}
+void ref_chain_dfa(uint32_t len, uint32_t* delta, uint8_t* acc) {
+  copy_dfa(chain_dfa(len), delta, acc);
+}
+
+}  // extern "C"
