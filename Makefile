@@ -1,0 +1,29 @@
+# Builds the product library (sm_100a only) and the test-side oracle.
+#   make            -> paper_2410_22764_b200/libdfm.so + oracle/liboracle.so (+ oracle/_ref if the
+#                      reference sources are present)
+NVCC ?= nvcc
+PKG := paper_2410_22764_b200
+CSRC := $(wildcard $(PKG)/csrc/*.cu)
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/dfm.h
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC,-O3 \
+           --expt-relaxed-constexpr -Xptxas -warn-spills
+OBJS := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CSRC))
+
+all: $(PKG)/libdfm.so oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PKG)/libdfm.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcuda
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(PKG)/libdfm.so
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

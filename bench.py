@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 DFA-minimization engine.
+
+Metric (BASELINE.json): transitions refined per second (n*k*passes / wall time)
+and wall time to the minimal DFA.  A "step" is one complete minimization of
+one synthetic DFA to its canonical minimal partition (all refinement passes +
+canonical relabel), DFA resident in HBM before the timed region.
+
+Default workload (N=1): the north-star single-GPU configuration — sortPR on
+random_dfa(n=1e8, k=4, seed=1, p=0.5) (SURVEY.md §8(d) C5 / BASELINE.md §4),
+generated on the device bit-exactly with the reference generator.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
+
+Multi-GPU: each rank minimizes its own replica DFA (seed + rank), no data-path
+collective ("replicas", weak scaling); timing is the max over ranks.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified dfamin headers) on the host cores, on a bounded sample of the same
+workload; rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "transitions refined/s to the minimal DFA (n*k*passes / wall time)"
+UNIT = "transitions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="sort", choices=["sort", "naive", "transpr", "naive_cas"])
+    ap.add_argument("--n", type=int, default=100_000_000)
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--p", type=float, default=0.5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-n", type=int, default=10_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(family: str):
+    """dram bytes per launch for a kernel family from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(family)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(n: int, k: int, seed: int, p: float, threads: int, steps: int = 1):
+    """The unmodified reference sort_pr (oracle/_ref) on host cores; returns
+    (transitions/s per step list, iterations, kind, sample, cores)."""
+    import numpy as np
+    import paper_2410_22764_b200 as dfm
+    from oracle import oracle as O
+    d = dfm.random_dfa(n, k, seed, p)  # bit-exact with generators.hpp:130-145
+    if O.ref_available():
+        R = O.Reference()
+        R.set_threads(threads)
+        runs = []
+        for _ in range(steps):
+            r = R.sort_pr(d.delta, d.accepting)
+            runs.append((n * k * r.iterations) / (r.elapsed_ms / 1e3))
+        return runs, r.iterations, "reference", R.worker_count(), r.elapsed_ms
+    # oracle port (plain C restatement, single-threaded)
+    runs = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = O.sort_pr(d.delta, d.accepting)
+        dt = time.perf_counter() - t0
+        runs.append((n * k * r.iterations) / dt)
+    return runs, r.iterations, "port", 1, dt * 1e3
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = min(args.n, args.cpu_sample_n)
+    t_all = time.perf_counter()
+    for _ in range(args.warmup):
+        cpu_reference_sample(n, args.k, args.seed, args.p, threads)
+    vals = []
+    iters = None
+    kind = cores = None
+    ms = []
+    for _ in range(args.steps):
+        v, iters, kind, cores, el = cpu_reference_sample(n, args.k, args.seed, args.p, threads)
+        vals.append(v[0])
+        ms.append(el)
+    value = statistics.mean(vals)
+    sample = (f"random_dfa(n={n}, k={args.k}, seed={args.seed}, p={args.p}) {args.algo}PR, "
+              f"{iters} passes; time = the reference's own RunStats.elapsed_ms")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.mean(ms), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (host-generated)",
+            "config": config(args, world, iters, None),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+def config(args, world, iters, blocks):
+    return {"workload": f"sortPR on random_dfa(n={args.n:.0e}, k={args.k}, seed={args.seed}, "
+                        f"p={args.p}) — north-star 1-GPU config (SURVEY 8(d) C5)"
+            if args.algo == "sort" else f"{args.algo} on random_dfa(n={args.n}, k={args.k})",
+            "algo": args.algo, "n": args.n, "k": args.k, "passes": iters, "blocks": blocks,
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "inputs larger than L2 (delta = 4nk bytes)" if 4 * args.n * args.k > (126 << 20)
+            else "L2 flushed between timed steps"}
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, rank: int, world: int, local: int):
+    import numpy as np
+    import torch
+    import paper_2410_22764_b200 as dfm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    eng = dfm.Engine(local)
+    stream = torch.cuda.current_stream(dev)
+    eng.set_stream(stream.cuda_stream)
+    algo = {"sort": dfm.Algo.sort, "naive": dfm.Algo.naive, "transpr": dfm.Algo.transpr,
+            "naive_cas": dfm.Algo.naive_cas}[args.algo]
+    cfg = dfm.AlgoRunConfig(policy=dfm.RacePolicy.deterministic_min)
+    seed = args.seed + rank
+    dd = eng.random_dfa_device(args.n, args.k, seed, args.p)
+    flush = None
+    if 4 * args.n * args.k <= (126 << 20):
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        nb, st = eng.run_device(algo, dd, cfg)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- timed region: device-resident input, CUDA events on the launch stream
+    eng.profile_reset()
+    eng.set_profiling(True)
+    launches0 = eng.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    step_ms = []
+    iters = None
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        nb, st = eng.run_device(algo, dd, cfg)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        iters = st.iterations
+        assert st.status == dfm.RunStatus.ok
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    launches = eng.kernel_launches() - launches0
+    eng.set_profiling(False)
+    prof = eng.profile()
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    transitions = float(args.n) * args.k * iters * world
+    value = transitions / (ms_per_step / 1e3)
+
+    # ---- e2e: host DFA in pinned memory -> public API (H2D, run, D2H labels)
+    e2e = None
+    if not args.no_e2e:
+        host = dd.download()
+        pin_delta = torch.empty((args.k, args.n), dtype=torch.int32, pin_memory=True)
+        pin_acc = torch.empty(args.n, dtype=torch.uint8, pin_memory=True)
+        pin_delta.numpy()[:] = host.delta.view(np.int32)
+        pin_acc.numpy()[:] = host.accepting
+        hd = dfm.Dfa(args.n, args.k, pin_delta.numpy().view(np.uint32), pin_acc.numpy(), 0)
+        del host
+        out_pin = torch.empty(args.n, dtype=torch.int32, pin_memory=True)
+        run_host = {"sort": lambda: eng.sort_pr(hd),
+                    "naive": lambda: eng.naive_pr(hd, dfm.PrOptions(
+                        policy=dfm.RacePolicy.deterministic_min)),
+                    "transpr": lambda: eng.trans_pr(hd, dfm.PrOptions(
+                        policy=dfm.RacePolicy.deterministic_min)),
+                    "naive_cas": lambda: eng.naive_pr_cas(hd)}[args.algo]
+        run_host()  # warm the host path
+        barrier()
+        e_ms = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            r = run_host()
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+            assert r.partition.num_blocks == nb
+        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": transitions / (float(et.item()) / 1e3), "unit": UNIT,
+               "ms_per_step": float(et.item()),
+               "h2d_bytes_per_step": 4 * args.n * args.k + args.n,
+               "d2h_bytes_per_step": 4 * args.n,
+               "how": "wall clock around Engine.sort_pr(host Dfa in pinned memory): H2D of "
+                      "delta+accepting, all passes, D2H of the canonical partition"}
+        del out_pin
+
+    if rank != 0:
+        return
+    # ---- roofline of the dominant kernel family (measured live above)
+    peak, peak_src = measured_peaks()
+    fam = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roofline = None
+    if fam is not None:
+        name, (scopes, fms, fbytes) = fam
+        achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
+        traffic = ncu_traffic(name)
+        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "peak_source": peak_src,
+                    "share_of_step": fms / total_ms if total_ms > 0 else None,
+                    "algorithmic_bytes_per_step": fbytes / args.steps,
+                    "families_ms_per_step": {k: v[1] / args.steps for k, v in prof.items()}}
+        # whole-iteration view with SURVEY 8(d)'s per-pass figure 8n(k+1)
+        it_bytes = 8.0 * args.n * (args.k + 1) * iters
+        roofline["iteration_view"] = {
+            "algorithmic_bytes_per_step": it_bytes,
+            "achieved": (it_bytes / 1e9) / (ms_per_step / 1e3),
+            "frac": ((it_bytes / 1e9) / (ms_per_step / 1e3)) / peak}
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            threads = os.cpu_count() or 1
+            ns = min(args.n, args.cpu_sample_n)
+            runs, citers, kind, cores, el = cpu_reference_sample(ns, args.k, args.seed, args.p,
+                                                                 threads)
+            cpu = {"value": runs[0], "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"random_dfa(n={ns}, k={args.k}, seed={args.seed}, p={args.p}) "
+                             f"sortPR, {citers} passes, {el:.0f} ms (reference RunStats)"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": repr(exc)}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "wall_time_to_minimal_dfa_ms": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: random_dfa generated on device, bit-exact with generators.hpp",
+            "config": config(args, world, iters, nb), "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+            "step_ms": step_ms, "lib": dfm.lib_path()}
+    print(json.dumps(line), flush=True)
+    dd.free()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

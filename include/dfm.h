@@ -1,0 +1,183 @@
+/*
+ * dfm.h — C-ABI of the B200-native DFA-minimization engine (libdfm.so).
+ *
+ * The drop-in boundary for the reference's minimize path (arxiv 2410.22764,
+ * `dfamin` headers).  Each entry point replaces one reference interface, cited
+ * below as proj/include/dfamin/<file>:<line>.  Plain pointers and sizes only:
+ * no torch/CUDA types appear in a signature (device pointers are `void*`).
+ *
+ * Conventions
+ *  - Return value: DFM_OK or a dfm_err code for INFRASTRUCTURE faults (bad
+ *    argument, CUDA/NCCL error, out of device memory); the message is in
+ *    dfm_last_error(ctx).  ALGORITHMIC outcomes are reported like the
+ *    reference, as a run status in dfm_stats.status (core.hpp:58):
+ *    timeout / capacity_exceeded leave block_out untouched and set
+ *    *num_blocks_out = 0 (the reference returns an empty partition,
+ *    min_sort.hpp:94-99, min_transpr.hpp:95-101, min_trans.hpp:89-95).
+ *    A CUDA error is never reported as a timeout.
+ *  - dfm_expand_alphabet alone reports over-limit as DFM_ERR_CAPACITY with
+ *    *required_bytes_out set: it mirrors the CapacityError the reference throws
+ *    (min_transpr.hpp:63-67).
+ *  - block_out receives the canonical partition (core.hpp:123-136: label b
+ *    first occurs before label b+1), n entries, caller-owned.
+ *  - Calls are synchronous from the caller's view.  One dfm_ctx per host
+ *    thread (a ctx serialises its own calls with an internal mutex).
+ *  - Host DFA rows are the reference's SoA layout: delta[a] points at the n
+ *    successors on letter a (Dfa::delta[a].data(), core.hpp:24-33) — zero-copy.
+ */
+#ifndef DFM_H
+#define DFM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFM_ABI_VERSION 1
+
+typedef enum {
+  DFM_OK = 0,
+  DFM_ERR_INVALID = 1,  /* malformed argument (the reference would throw invalid_argument) */
+  DFM_ERR_CUDA = 2,     /* CUDA runtime / launch failure */
+  DFM_ERR_CAPACITY = 3, /* dfm_expand_alphabet over max_memory_bytes (CapacityError) */
+  DFM_ERR_NO_MEMORY = 4,/* device allocation failed */
+  DFM_ERR_NO_DEVICE = 5 /* no sm_100 device / extension unusable: never silently falls back */
+} dfm_err;
+
+/* RunStatus, core.hpp:58 */
+typedef enum { DFM_STATUS_OK = 0, DFM_STATUS_TIMEOUT = 1, DFM_STATUS_CAPACITY_EXCEEDED = 2 } dfm_run_status;
+
+/* substrate::RacePolicy, substrate.hpp:24 */
+typedef enum { DFM_POLICY_ARBITRARY = 0, DFM_POLICY_MIN = 1, DFM_POLICY_MAX = 2 } dfm_policy;
+
+/* Algo, bench.hpp:23 (DFM_ALGO_ORACLE is the CPU Moore oracle: not provided by the
+ * GPU engine, dfm_run_algorithm returns DFM_ERR_INVALID for it) */
+typedef enum {
+  DFM_ALGO_TRANS = 0,
+  DFM_ALGO_NAIVE = 1,
+  DFM_ALGO_NAIVE_CAS = 2,
+  DFM_ALGO_SORT = 3,
+  DFM_ALGO_TRANSPR = 4,
+  DFM_ALGO_ORACLE = 5
+} dfm_algo;
+
+typedef struct dfm_ctx dfm_ctx;   /* device, stream, scratch arena */
+typedef struct dfm_ddfa dfm_ddfa; /* a DFA resident in device memory */
+
+/* Dfa, core.hpp:24-33 (host memory, borrowed) */
+typedef struct {
+  uint32_t num_states;
+  uint32_t alphabet_size;
+  const uint32_t* const* delta; /* alphabet_size row pointers, num_states entries each */
+  const uint8_t* accepting;     /* num_states indicators */
+  uint32_t initial;
+} dfm_dfa;
+
+/* RunStats, core.hpp:71-77 */
+typedef struct {
+  uint64_t iterations;     /* passes including the final no-change pass */
+  uint64_t closure_steps;  /* alphabet-doubling rounds (transPR), else 0 */
+  double elapsed_ms;       /* host steady clock around the whole call */
+  uint64_t peak_memory_estimate; /* the reference's estimate formula */
+  int32_t status;          /* dfm_run_status */
+} dfm_stats;
+
+/* Limits, core.hpp:81-84.  timeout_ms <= 0 disables the deadline. */
+typedef struct {
+  uint64_t max_memory_bytes; /* reference default 16 GiB */
+  int64_t timeout_ms;        /* reference default 300000 */
+} dfm_limits;
+
+/* Per-pass trace (SortTrace min_sort.hpp:21-24, PrTrace min_partref.hpp:21-24):
+ * called on the host after every pass with the engine's RAW labels for the
+ * pass (block ids for sortPR, leader ids for naivePR) and the block count. */
+typedef void (*dfm_pass_fn)(void* user, uint64_t pass, const uint32_t* raw_block, uint32_t n,
+                            uint32_t num_blocks);
+typedef struct {
+  dfm_pass_fn on_pass;
+  void* user;
+} dfm_trace;
+
+/* ---------------------------------------------------------------- context */
+const char* dfm_version(void);
+int dfm_ctx_create(int device, dfm_ctx** out);
+void dfm_ctx_destroy(dfm_ctx* ctx);
+const char* dfm_last_error(const dfm_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the ctx's own. */
+int dfm_ctx_set_stream(dfm_ctx* ctx, void* stream);
+/* Record per-kernel CUDA-event timings for subsequent calls (bench/roofline). */
+int dfm_ctx_set_profiling(dfm_ctx* ctx, int enabled);
+/* Read back timing for a kernel family ("sig", "sort", "scan", "relabel", "elect",
+ * "split", "double", "gemm", "propagate", "canon", ...): timed scopes, total ms and
+ * total ALGORITHMIC bytes since the last reset; returns
+ * DFM_ERR_INVALID for an unknown name. */
+int dfm_profile_get(dfm_ctx* ctx, const char* name, uint64_t* scopes, double* total_ms,
+                    uint64_t* algo_bytes);
+/* Comma-separated list of the kernel families recorded so far. */
+const char* dfm_profile_names(dfm_ctx* ctx);
+int dfm_profile_reset(dfm_ctx* ctx);
+/* Process-wide count of libdfm kernel launches so far (all contexts). */
+uint64_t dfm_kernel_launches(void);
+/* Bytes of device memory currently held by the ctx's scratch arena. */
+uint64_t dfm_ctx_device_bytes(const dfm_ctx* ctx);
+
+/* ---------------------------------------------------------------- host-buffer API */
+/* sort_pr, min_sort.hpp:72 / :128 */
+int dfm_sort_pr(dfm_ctx* ctx, const dfm_dfa* d, int64_t timeout_ms, const dfm_trace* trace,
+                uint32_t* block_out, uint32_t* num_blocks_out, dfm_stats* stats);
+/* naive_pr, min_partref.hpp:156 / :160 (policy = dfm_policy) */
+int dfm_naive_pr(dfm_ctx* ctx, const dfm_dfa* d, int32_t policy, int64_t timeout_ms,
+                 const dfm_trace* trace, uint32_t* block_out, uint32_t* num_blocks_out,
+                 dfm_stats* stats);
+/* naive_pr_cas, min_partref.hpp:170 */
+int dfm_naive_pr_cas(dfm_ctx* ctx, const dfm_dfa* d, int64_t timeout_ms, const dfm_trace* trace,
+                     uint32_t* block_out, uint32_t* num_blocks_out, dfm_stats* stats);
+/* power_levels / expand_required_bytes, min_transpr.hpp:21-27 */
+uint32_t dfm_power_levels(uint32_t n);
+uint64_t dfm_expand_required_bytes(uint32_t n, uint32_t k);
+/* expand_alphabet, min_transpr.hpp:59.  rows_out: levels*k*n u32 (row lvl*k+a holds
+ * a^(2^lvl)); may be NULL to query *levels_out / *required_bytes_out only. */
+int dfm_expand_alphabet(dfm_ctx* ctx, const dfm_dfa* d, uint64_t max_memory_bytes,
+                        uint32_t* rows_out, uint32_t* levels_out, uint64_t* required_bytes_out);
+/* trans_pr, min_transpr.hpp:90 / :114 */
+int dfm_trans_pr(dfm_ctx* ctx, const dfm_dfa* d, int32_t policy, const dfm_limits* limits,
+                 uint32_t* block_out, uint32_t* num_blocks_out, dfm_stats* stats);
+/* trans_required_bytes, min_trans.hpp:24-27 (saturates at UINT64_MAX) */
+uint64_t dfm_trans_required_bytes(uint64_t n);
+/* trans_minimize, min_trans.hpp:81.  TransInspect (min_trans.hpp:41-44) when
+ * apart_out (n*n u8) and/or popcounts_out (one u64 per pass, up to cap) are non-NULL. */
+int dfm_trans_minimize(dfm_ctx* ctx, const dfm_dfa* d, const dfm_limits* limits,
+                       uint8_t* apart_out, uint64_t* popcounts_out, uint32_t popcounts_cap,
+                       uint32_t* block_out, uint32_t* num_blocks_out, dfm_stats* stats);
+/* run_algorithm, bench.hpp:83 (AlgoRunConfig = policy + limits) */
+int dfm_run_algorithm(dfm_ctx* ctx, int32_t algo, const dfm_dfa* d, int32_t policy,
+                      const dfm_limits* limits, uint32_t* block_out, uint32_t* num_blocks_out,
+                      dfm_stats* stats);
+
+/* ---------------------------------------------------------------- device-resident API */
+/* Upload a host DFA once (pinned staging, SoA rows of length n). */
+int dfm_ddfa_upload(dfm_ctx* ctx, const dfm_dfa* d, dfm_ddfa** out);
+/* Bit-exact device-side random_dfa (generators.hpp:130-145, counter-based SplitMix64). */
+int dfm_ddfa_random(dfm_ctx* ctx, uint32_t n, uint32_t k, uint64_t seed, double accept_prob,
+                    dfm_ddfa** out);
+/* Copy a device DFA back (rows: k*n u32 flat, acc: n u8); either may be NULL. */
+int dfm_ddfa_download(dfm_ctx* ctx, const dfm_ddfa* dd, uint32_t* delta_flat, uint8_t* accepting);
+int dfm_ddfa_shape(const dfm_ddfa* dd, uint32_t* num_states, uint32_t* alphabet_size);
+void dfm_ddfa_free(dfm_ddfa* dd);
+/* Same algorithms on a resident DFA.  block_out_dev: device pointer (n u32) or NULL
+ * to keep the canonical labels inside the ctx only; *num_blocks_out and stats are host. */
+int dfm_run_algorithm_dev(dfm_ctx* ctx, int32_t algo, const dfm_ddfa* dd, int32_t policy,
+                          const dfm_limits* limits, void* block_out_dev, uint32_t* num_blocks_out,
+                          dfm_stats* stats);
+
+/* ---------------------------------------------------------------- host generators */
+/* Multi-threaded, bit-exact with generators.hpp (SplitMix64 draw j = mix(seed+(j+1)*gamma)). */
+int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double accept_prob,
+                       uint32_t* delta_flat, uint8_t* accepting);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFM_H */

@@ -1,0 +1,418 @@
+// C-ABI entry points of libdfm.so (include/dfm.h).  Converts infrastructure
+// exceptions into dfm_err codes, uploads host DFAs, dispatches algorithms and
+// copies canonical partitions back.
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "dfm_internal.cuh"
+#include "prims.cuh"
+
+struct dfm_ctx {};   // opaque: really dfm::Ctx
+struct dfm_ddfa {};  // opaque: really dfm::DevDfa
+
+namespace dfm {
+namespace {
+
+thread_local std::string g_create_error;
+
+Ctx* as_ctx(dfm_ctx* c) { return reinterpret_cast<Ctx*>(c); }
+const Ctx* as_ctx(const dfm_ctx* c) { return reinterpret_cast<const Ctx*>(c); }
+DevDfa* as_dd(dfm_ddfa* d) { return reinterpret_cast<DevDfa*>(d); }
+const DevDfa* as_dd(const dfm_ddfa* d) { return reinterpret_cast<const DevDfa*>(d); }
+
+template <class F>
+int guarded(dfm_ctx* c, F&& f) {
+  Ctx* ctx = as_ctx(c);
+  if (ctx == nullptr) return DFM_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  try {
+    DFM_CUDA(cudaSetDevice(ctx->device));
+    f(*ctx);
+    ctx->harvest();
+    return DFM_OK;
+  } catch (const Error& e) {
+    ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    ctx->last_error = "host allocation failed";
+    return DFM_ERR_NO_MEMORY;
+  } catch (const std::exception& e) {
+    ctx->last_error = e.what();
+    return DFM_ERR_INVALID;
+  }
+}
+
+__global__ void validate_kernel(const uint32_t* __restrict__ delta, uint64_t total, uint32_t n,
+                                unsigned long long* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool b = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    b |= delta[i] >= n;
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1ull);
+}
+
+void check_host_dfa(const dfm_dfa* d) {
+  if (d == nullptr) throw Error(DFM_ERR_INVALID, "null dfa");
+  if (d->num_states < 1) throw Error(DFM_ERR_INVALID, "automaton needs at least one state");
+  if (d->alphabet_size > 0 && d->delta == nullptr)
+    throw Error(DFM_ERR_INVALID, "transition table has wrong number of letter rows");
+  for (uint32_t a = 0; a < d->alphabet_size; ++a)
+    if (d->delta[a] == nullptr)
+      throw Error(DFM_ERR_INVALID, "transition row " + std::to_string(a) + " is null");
+  if (d->accepting == nullptr) throw Error(DFM_ERR_INVALID, "accepting indicator is null");
+  if (d->initial >= d->num_states) throw Error(DFM_ERR_INVALID, "initial state out of range");
+}
+
+// every target < n (the engine would fault otherwise; core.hpp:104-119)
+void validate_targets(Ctx& ctx, const DevDfa& dd) {
+  const uint64_t total = (uint64_t)dd.n * dd.k;
+  if (total == 0) return;
+  auto* bad = reinterpret_cast<unsigned long long*>(ctx.d_scalars + 40);
+  DFM_CUDA(cudaMemsetAsync(bad, 0, 8, ctx.stream));
+  const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(total, 256), ctx.num_sms * 16ull);
+  validate_kernel<<<grid, 256, 0, ctx.stream>>>(dd.delta, total, dd.n, bad);
+  DFM_LAUNCH_CHECK();
+  DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 40, bad, 8, cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  if (ctx.h_scalars[40]) throw Error(DFM_ERR_INVALID, "transition target out of range");
+}
+
+// stage a host DFA into device memory (slot names under `prefix`)
+DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_alloc) {
+  check_host_dfa(d);
+  DevDfa dd;
+  dd.n = d->num_states;
+  dd.k = d->alphabet_size;
+  dd.initial = d->initial;
+  const uint64_t n = dd.n, k = dd.k;
+  if (own_alloc) {
+    DFM_CUDA(cudaMalloc(&dd.delta, std::max<uint64_t>(n * k, 1) * 4));
+    DFM_CUDA(cudaMalloc(&dd.acc, n));
+    dd.owns = true;
+  } else {
+    dd.delta = ctx.slot_t<uint32_t>(prefix + ".delta", std::max<uint64_t>(n * k, 1));
+    dd.acc = ctx.slot_t<uint8_t>(prefix + ".acc", n);
+    dd.owns = false;
+  }
+  for (uint64_t a = 0; a < k; ++a)
+    DFM_CUDA(cudaMemcpyAsync(dd.delta + a * n, d->delta[a], n * 4, cudaMemcpyHostToDevice,
+                             ctx.stream));
+  DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+  validate_targets(ctx, dd);
+  return dd;
+}
+
+dfm_limits limits_or_default(const dfm_limits* l) {
+  dfm_limits r;
+  r.max_memory_bytes = l ? l->max_memory_bytes : (16ull << 30);
+  r.timeout_ms = l ? l->timeout_ms : 300000;
+  return r;
+}
+
+AlgoOut dispatch(Ctx& ctx, int32_t algo, const DevDfa& dd, int32_t policy, const dfm_limits& lim,
+                 const dfm_trace* trace, uint8_t* apart, uint64_t* pops, uint32_t pop_cap) {
+  if (policy < DFM_POLICY_ARBITRARY || policy > DFM_POLICY_MAX)
+    throw Error(DFM_ERR_INVALID, "unknown race policy");
+  const Deadline dl(lim.timeout_ms);
+  switch (algo) {
+    case DFM_ALGO_TRANS:
+      return run_trans_minimize(ctx, dd, lim, dl, apart, pops, pop_cap);
+    case DFM_ALGO_NAIVE:
+      return run_leader_election(ctx, dd, dd.delta, dd.k, policy, false, dl, trace);
+    case DFM_ALGO_NAIVE_CAS:
+      return run_leader_election(ctx, dd, dd.delta, dd.k, DFM_POLICY_ARBITRARY, true, dl, trace);
+    case DFM_ALGO_SORT:
+      return run_sort_pr(ctx, dd, dl, trace);
+    case DFM_ALGO_TRANSPR:
+      return run_trans_pr(ctx, dd, policy, lim, dl);
+    case DFM_ALGO_ORACLE:
+      throw Error(DFM_ERR_INVALID, "the Moore oracle is a CPU reference, not a GPU algorithm");
+    default:
+      throw Error(DFM_ERR_INVALID, "unknown algorithm");
+  }
+}
+
+void finish(Ctx& ctx, const AlgoOut& o, uint64_t n, const Deadline& dl, uint32_t* block_out,
+            uint32_t* nb_out, dfm_stats* st) {
+  if (o.status == DFM_STATUS_OK && block_out != nullptr)
+    DFM_CUDA(cudaMemcpyAsync(block_out, o.canon_dev, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  if (nb_out) *nb_out = o.status == DFM_STATUS_OK ? o.num_blocks : 0;
+  if (st) {
+    st->iterations = o.iterations;
+    st->closure_steps = o.closure_steps;
+    st->peak_memory_estimate = o.peak_memory_estimate;
+    st->status = o.status;
+    st->elapsed_ms = dl.elapsed();
+  }
+}
+
+int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const dfm_limits* l,
+             const dfm_trace* trace, uint8_t* apart, uint64_t* pops, uint32_t pop_cap,
+             uint32_t* block_out, uint32_t* nb_out, dfm_stats* st) {
+  return guarded(c, [&](Ctx& ctx) {
+    const Deadline whole(0);
+    const dfm_limits lim = limits_or_default(l);
+    const DevDfa dd = upload(ctx, d, "in", false);
+    const AlgoOut o = dispatch(ctx, algo, dd, policy, lim, trace, apart, pops, pop_cap);
+    finish(ctx, o, dd.n, whole, block_out, nb_out, st);
+  });
+}
+
+uint64_t sm_draw(uint64_t seed, uint64_t j) {
+  uint64_t z = seed + (j + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+}  // namespace dfm
+
+using namespace dfm;
+
+extern "C" {
+
+const char* dfm_version(void) { return "libdfm 1 (B200 sm_100a)"; }
+
+int dfm_ctx_create(int device, dfm_ctx** out) {
+  if (out == nullptr) return DFM_ERR_INVALID;
+  try {
+    *out = reinterpret_cast<dfm_ctx*>(new Ctx(device));
+    return DFM_OK;
+  } catch (const Error& e) {
+    g_create_error = e.what();
+    *out = nullptr;
+    return e.code;
+  }
+}
+
+void dfm_ctx_destroy(dfm_ctx* c) { delete as_ctx(c); }
+
+const char* dfm_last_error(const dfm_ctx* c) {
+  if (c == nullptr) return g_create_error.c_str();
+  return as_ctx(c)->last_error.c_str();
+}
+
+int dfm_ctx_set_stream(dfm_ctx* c, void* stream) {
+  return guarded(c, [&](Ctx& ctx) {
+    ctx.sync();
+    ctx.stream = stream ? static_cast<cudaStream_t>(stream) : ctx.own_stream;
+  });
+}
+
+int dfm_ctx_set_profiling(dfm_ctx* c, int enabled) {
+  return guarded(c, [&](Ctx& ctx) { ctx.profiling = enabled != 0; });
+}
+
+int dfm_profile_get(dfm_ctx* c, const char* name, uint64_t* launches, double* total_ms,
+                    uint64_t* algo_bytes) {
+  int found = 0;
+  const int rc = guarded(c, [&](Ctx& ctx) {
+    auto it = ctx.prof.find(name ? name : "");
+    if (it == ctx.prof.end()) return;
+    found = 1;
+    if (launches) *launches = it->second.launches;
+    if (total_ms) *total_ms = it->second.ms;
+    if (algo_bytes) *algo_bytes = it->second.bytes;
+  });
+  if (rc != DFM_OK) return rc;
+  return found ? DFM_OK : DFM_ERR_INVALID;
+}
+
+const char* dfm_profile_names(dfm_ctx* c) {
+  if (c == nullptr) return "";
+  return as_ctx(c)->prof_names.c_str();
+}
+
+int dfm_profile_reset(dfm_ctx* c) {
+  return guarded(c, [&](Ctx& ctx) {
+    ctx.harvest();
+    ctx.prof.clear();
+    ctx.prof_names.clear();
+  });
+}
+
+uint64_t dfm_kernel_launches(void) { return launch_count(); }
+
+uint64_t dfm_ctx_device_bytes(const dfm_ctx* c) { return c ? as_ctx(c)->held_bytes : 0; }
+
+int dfm_sort_pr(dfm_ctx* c, const dfm_dfa* d, int64_t timeout_ms, const dfm_trace* trace,
+                uint32_t* block_out, uint32_t* nb, dfm_stats* st) {
+  const dfm_limits lim{16ull << 30, timeout_ms};
+  return run_host(c, DFM_ALGO_SORT, d, DFM_POLICY_ARBITRARY, &lim, trace, nullptr, nullptr, 0,
+                  block_out, nb, st);
+}
+
+int dfm_naive_pr(dfm_ctx* c, const dfm_dfa* d, int32_t policy, int64_t timeout_ms,
+                 const dfm_trace* trace, uint32_t* block_out, uint32_t* nb, dfm_stats* st) {
+  const dfm_limits lim{16ull << 30, timeout_ms};
+  return run_host(c, DFM_ALGO_NAIVE, d, policy, &lim, trace, nullptr, nullptr, 0, block_out, nb,
+                  st);
+}
+
+int dfm_naive_pr_cas(dfm_ctx* c, const dfm_dfa* d, int64_t timeout_ms, const dfm_trace* trace,
+                     uint32_t* block_out, uint32_t* nb, dfm_stats* st) {
+  const dfm_limits lim{16ull << 30, timeout_ms};
+  return run_host(c, DFM_ALGO_NAIVE_CAS, d, DFM_POLICY_ARBITRARY, &lim, trace, nullptr, nullptr,
+                  0, block_out, nb, st);
+}
+
+uint32_t dfm_power_levels(uint32_t n) { return n == 0 ? 0 : 32 - __builtin_clz(n); }
+
+uint64_t dfm_expand_required_bytes(uint32_t n, uint32_t k) {
+  return (uint64_t)dfm_power_levels(n) * k * n * 4;
+}
+
+int dfm_expand_alphabet(dfm_ctx* c, const dfm_dfa* d, uint64_t max_memory_bytes,
+                        uint32_t* rows_out, uint32_t* levels_out, uint64_t* required_out) {
+  int capacity = 0;
+  const int rc = guarded(c, [&](Ctx& ctx) {
+    check_host_dfa(d);
+    const uint64_t required = dfm_expand_required_bytes(d->num_states, d->alphabet_size);
+    if (required_out) *required_out = required;
+    if (required > max_memory_bytes) {  // CapacityError, min_transpr.hpp:63-67
+      capacity = 1;
+      ctx.last_error = "alphabet expansion needs " + std::to_string(required) +
+                       " bytes, limit is " + std::to_string(max_memory_bytes);
+      return;
+    }
+    const uint32_t levels = dfm_power_levels(d->num_states);
+    if (levels_out) *levels_out = levels;
+    if (rows_out == nullptr) return;
+    const DevDfa dd = upload(ctx, d, "in", false);
+    const uint32_t* rows = expand_alphabet_dev(ctx, dd, levels);
+    DFM_CUDA(cudaMemcpyAsync(rows_out, rows, required, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+  });
+  if (rc != DFM_OK) return rc;
+  return capacity ? DFM_ERR_CAPACITY : DFM_OK;
+}
+
+int dfm_trans_pr(dfm_ctx* c, const dfm_dfa* d, int32_t policy, const dfm_limits* l,
+                 uint32_t* block_out, uint32_t* nb, dfm_stats* st) {
+  return run_host(c, DFM_ALGO_TRANSPR, d, policy, l, nullptr, nullptr, nullptr, 0, block_out, nb,
+                  st);
+}
+
+uint64_t dfm_trans_required_bytes(uint64_t n) {
+  const unsigned __int128 bits = (unsigned __int128)n * n * n * n;
+  const unsigned __int128 bytes = (bits + 7) / 8;
+  return bytes > (unsigned __int128)UINT64_MAX ? UINT64_MAX : (uint64_t)bytes;
+}
+
+int dfm_trans_minimize(dfm_ctx* c, const dfm_dfa* d, const dfm_limits* l, uint8_t* apart_out,
+                       uint64_t* popcounts_out, uint32_t popcounts_cap, uint32_t* block_out,
+                       uint32_t* nb, dfm_stats* st) {
+  return run_host(c, DFM_ALGO_TRANS, d, DFM_POLICY_ARBITRARY, l, nullptr, apart_out,
+                  popcounts_out, popcounts_cap, block_out, nb, st);
+}
+
+int dfm_run_algorithm(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy,
+                      const dfm_limits* l, uint32_t* block_out, uint32_t* nb, dfm_stats* st) {
+  return run_host(c, algo, d, policy, l, nullptr, nullptr, nullptr, 0, block_out, nb, st);
+}
+
+int dfm_ddfa_upload(dfm_ctx* c, const dfm_dfa* d, dfm_ddfa** out) {
+  if (out == nullptr) return DFM_ERR_INVALID;
+  *out = nullptr;
+  return guarded(c, [&](Ctx& ctx) {
+    DevDfa* dd = new DevDfa(upload(ctx, d, "", true));
+    ctx.sync();
+    *out = reinterpret_cast<dfm_ddfa*>(dd);
+  });
+}
+
+int dfm_ddfa_random(dfm_ctx* c, uint32_t n, uint32_t k, uint64_t seed, double p, dfm_ddfa** out) {
+  if (out == nullptr) return DFM_ERR_INVALID;
+  *out = nullptr;
+  return guarded(c, [&](Ctx& ctx) {
+    if (n < 1 || k < 1) throw Error(DFM_ERR_INVALID, "random_dfa needs n >= 1 and k >= 1");
+    DevDfa* dd = new DevDfa();
+    dd->n = n;
+    dd->k = k;
+    dd->owns = true;
+    try {
+      DFM_CUDA(cudaMalloc(&dd->delta, (uint64_t)n * k * 4));
+      DFM_CUDA(cudaMalloc(&dd->acc, n));
+      random_dfa_dev(ctx, *dd, n, k, seed, p);
+      ctx.sync();
+    } catch (...) {
+      cudaFree(dd->delta);
+      cudaFree(dd->acc);
+      delete dd;
+      throw;
+    }
+    *out = reinterpret_cast<dfm_ddfa*>(dd);
+  });
+}
+
+int dfm_ddfa_download(dfm_ctx* c, const dfm_ddfa* d, uint32_t* delta_flat, uint8_t* accepting) {
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa* dd = as_dd(d);
+    if (dd == nullptr) throw Error(DFM_ERR_INVALID, "null device dfa");
+    if (delta_flat)
+      DFM_CUDA(cudaMemcpyAsync(delta_flat, dd->delta, (uint64_t)dd->n * dd->k * 4,
+                               cudaMemcpyDeviceToHost, ctx.stream));
+    if (accepting)
+      DFM_CUDA(cudaMemcpyAsync(accepting, dd->acc, dd->n, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+  });
+}
+
+int dfm_ddfa_shape(const dfm_ddfa* d, uint32_t* n, uint32_t* k) {
+  const DevDfa* dd = as_dd(d);
+  if (dd == nullptr) return DFM_ERR_INVALID;
+  if (n) *n = dd->n;
+  if (k) *k = dd->k;
+  return DFM_OK;
+}
+
+void dfm_ddfa_free(dfm_ddfa* d) {
+  DevDfa* dd = as_dd(d);
+  if (dd == nullptr) return;
+  if (dd->owns) {
+    cudaFree(dd->delta);
+    cudaFree(dd->acc);
+  }
+  delete dd;
+}
+
+int dfm_run_algorithm_dev(dfm_ctx* c, int32_t algo, const dfm_ddfa* d, int32_t policy,
+                          const dfm_limits* l, void* block_out_dev, uint32_t* nb, dfm_stats* st) {
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa* dd = as_dd(d);
+    if (dd == nullptr) throw Error(DFM_ERR_INVALID, "null device dfa");
+    const Deadline whole(0);
+    const dfm_limits lim = limits_or_default(l);
+    const AlgoOut o = dispatch(ctx, algo, *dd, policy, lim, nullptr, nullptr, nullptr, 0);
+    if (o.status == DFM_STATUS_OK && block_out_dev != nullptr)
+      DFM_CUDA(cudaMemcpyAsync(block_out_dev, o.canon_dev, (uint64_t)dd->n * 4,
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+    finish(ctx, o, dd->n, whole, nullptr, nb, st);
+  });
+}
+
+int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double p, uint32_t* delta,
+                       uint8_t* acc) {
+  if (n < 1 || k < 1 || delta == nullptr || acc == nullptr) return DFM_ERR_INVALID;
+  const uint64_t total = (uint64_t)n * k;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned T = (unsigned)std::min<uint64_t>(hw, std::max<uint64_t>(1, (total + n) >> 16));
+  auto work = [&](unsigned t) {
+    const uint64_t lo = total * t / T, hi = total * (t + 1) / T;
+    for (uint64_t j = lo; j < hi; ++j) delta[j] = (uint32_t)(sm_draw(seed, j) % n);
+    const uint64_t alo = (uint64_t)n * t / T, ahi = (uint64_t)n * (t + 1) / T;
+    for (uint64_t q = alo; q < ahi; ++q)
+      acc[q] = ((double)(sm_draw(seed, total + q) >> 11) * 0x1.0p-53) < p ? 1 : 0;
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  return DFM_OK;
+}
+
+}  // extern "C"

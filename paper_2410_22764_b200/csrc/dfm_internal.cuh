@@ -1,0 +1,164 @@
+// Internal runtime of libdfm.so: context, error model, stream-ordered scratch
+// arena and per-kernel-family CUDA-event profiling.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dfm.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libdfm is written for sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace dfm {
+
+constexpr uint32_t kNoLeader = 0xFFFFFFFFu;  // substrate.hpp:95
+
+// Infrastructure faults travel as exceptions inside the library and become
+// dfm_err codes at the C-ABI boundary (capi.cu).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? DFM_ERR_NO_MEMORY : DFM_ERR_CUDA;
+    throw Error(code, std::string(what) + " failed at " + file + ":" + std::to_string(line) +
+                          ": " + cudaGetErrorString(e));
+  }
+}
+#define DFM_CUDA(x) ::dfm::cuda_check((x), #x, __FILE__, __LINE__)
+// every kernel launch site calls DFM_LAUNCH_CHECK(): it also counts launches
+// (dfm_kernel_launches(), the bench's gpu_launches evidence)
+uint64_t note_launch();
+uint64_t launch_count();
+#define DFM_LAUNCH_CHECK() \
+  (::dfm::note_launch(), ::dfm::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__))
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// A growable device buffer from the ctx arena (stream-ordered allocator with
+// an unbounded release threshold, so repeated calls reuse the same HBM).
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+struct Ctx;
+
+// Times one kernel family with events on the launching stream when profiling
+// is enabled.  Usage: { ProfScope p(ctx, "sig"); kernel<<<..., ctx.stream>>>(); }
+// `bytes` is the ALGORITHMIC byte count of the scoped work,
+// accumulated next to the measured time for the roofline.
+struct ProfScope {
+  Ctx& ctx;
+  const char* name;
+  uint64_t bytes;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ProfScope(Ctx& c, const char* n, uint64_t algo_bytes = 0);
+  ~ProfScope();
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::string last_error;
+  // named scratch slots: each algorithm asks for a slot by name and size
+  std::map<std::string, Buf> slots;
+  uint64_t held_bytes = 0;
+  // pinned host staging
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // profiling
+  bool profiling = false;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+    uint64_t bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+  struct Acc {
+    uint64_t launches = 0;
+    double ms = 0;
+    uint64_t bytes = 0;
+  };
+  std::map<std::string, Acc> prof;
+  std::string prof_names;
+  // small device scalars for host read-back (pinned host mirror)
+  uint64_t* d_scalars = nullptr;  // device, 64 slots
+  uint64_t* h_scalars = nullptr;  // pinned host, 64 slots
+
+  explicit Ctx(int dev);
+  ~Ctx();
+
+  void* slot(const std::string& name, size_t bytes);
+  template <class T>
+  T* slot_t(const std::string& name, size_t count) {
+    return static_cast<T*>(slot(name, count * sizeof(T)));
+  }
+  void release_slot(const std::string& name);
+  void* host_pinned(size_t bytes);
+  void sync() { DFM_CUDA(cudaStreamSynchronize(stream)); }
+  // fold completed profiling events into the accumulators
+  void harvest();
+  cudaEvent_t take_event();
+};
+
+inline double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// Deadline bookkeeping shared by all algorithms (core.hpp:190-199).
+struct Deadline {
+  double start;
+  double limit;  // <= 0: none
+  Deadline(int64_t timeout_ms) : start(now_ms()), limit(timeout_ms > 0 ? (double)timeout_ms : 0) {}
+  bool expired() const { return limit > 0 && now_ms() - start > limit; }
+  double elapsed() const { return now_ms() - start; }
+};
+
+// Device-resident DFA: SoA rows packed as one [k][n] allocation.
+struct DevDfa {
+  uint32_t n = 0, k = 0, initial = 0;
+  uint32_t* delta = nullptr;  // k*n
+  uint8_t* acc = nullptr;     // n
+  bool owns = true;
+};
+
+struct AlgoOut {
+  uint32_t num_blocks = 0;
+  uint64_t iterations = 0, closure_steps = 0, peak_memory_estimate = 0;
+  int32_t status = DFM_STATUS_OK;
+  uint32_t* canon_dev = nullptr;  // canonical labels on device (ctx slot "canon")
+};
+
+// ---- algorithm drivers (device-resident input, results on device) ----
+AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace);
+AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uint64_t letters,
+                            int policy, bool fused_cas, const Deadline& dl,
+                            const dfm_trace* trace);
+uint32_t* expand_alphabet_dev(Ctx& ctx, const DevDfa& d, uint32_t levels);
+AlgoOut run_trans_pr(Ctx& ctx, const DevDfa& d, int policy, const dfm_limits& lim,
+                     const Deadline& dl);
+AlgoOut run_trans_minimize(Ctx& ctx, const DevDfa& d, const dfm_limits& lim, const Deadline& dl,
+                           uint8_t* apart_host, uint64_t* popcounts, uint32_t pop_cap);
+// canonical relabel of raw labels (< n) into ctx slot "canon"; returns block count
+uint32_t canonicalize_dev(Ctx& ctx, const uint32_t* raw, uint64_t n, uint32_t* out);
+// device random_dfa
+void random_dfa_dev(Ctx& ctx, DevDfa& d, uint32_t n, uint32_t k, uint64_t seed, double p);
+
+}  // namespace dfm

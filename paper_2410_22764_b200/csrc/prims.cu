@@ -1,0 +1,198 @@
+// Host side of the device-wide primitives (see prims.cuh).
+#include "prims.cuh"
+
+#include <algorithm>
+#include <utility>
+
+namespace dfm {
+namespace prims {
+
+// per-pass digit histograms of all passes in one read of the keys
+__global__ void __launch_bounds__(256) radix_histogram_kernel(const uint64_t* __restrict__ keys,
+                                                              uint64_t count, int passes,
+                                                              uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8 * 256];
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 255)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void radix_bucket_scan_kernel(const uint32_t* __restrict__ hist,
+                                         uint32_t* __restrict__ base) {
+  __shared__ uint32_t s_warp[9];
+  const uint32_t x = hist[blockIdx.x * 256 + threadIdx.x];
+  uint32_t total;
+  const uint32_t e = block_exclusive_sum<256>(x, s_warp, &total);
+  base[blockIdx.x * 256 + threadIdx.x] = e;
+}
+
+template <bool kIdentVals>
+__global__ void __launch_bounds__(kRsThreads) onesweep_kernel(
+    const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t count, int shift,
+    const uint32_t* __restrict__ bucket_base, uint64_t* status, uint32_t* ticket) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kRsTile);
+  uint32_t* s_cnt = s_vals + kRsTile;         // [warp][digit]
+  uint32_t* s_start = s_cnt + kRsWarps * 256;  // tile-local digit start
+  uint32_t* s_glob = s_start + 256;            // global destination base per digit
+  uint32_t* s_misc = s_glob + 256;             // [0] tile id, [1..9] warp sums
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_misc[0] = atomicAdd(ticket, 1u);
+  for (int i = tid; i < kRsWarps * 256; i += kRsThreads) s_cnt[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_misc[0];
+  const uint64_t tile_base = (uint64_t)tile * kRsTile;
+  const uint64_t warp_base = tile_base + (uint64_t)warp * 32 * kRsItems;
+
+  uint64_t k[kRsItems];
+  uint32_t v[kRsItems];
+  uint32_t rank[kRsItems];
+  uint32_t dig[kRsItems];
+#pragma unroll
+  for (int j = 0; j < kRsItems; ++j) {
+    const uint64_t idx = warp_base + (uint64_t)j * 32 + lane;
+    const bool valid = idx < count;
+    k[j] = valid ? keys_in[idx] : 0ull;
+    if (kIdentVals) v[j] = (uint32_t)idx;
+    else v[j] = valid ? vals_in[idx] : 0u;
+    dig[j] = valid ? (uint32_t)((k[j] >> shift) & 255) : 256u;
+  }
+  uint32_t* my_cnt = s_cnt + warp * 256;
+#pragma unroll
+  for (int j = 0; j < kRsItems; ++j) {
+    const uint32_t d = dig[j];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t lt = __popc(peers & lanemask_lt());
+    uint32_t base = 0;
+    if (d < 256) base = my_cnt[d];
+    rank[j] = base + lt;
+    __syncwarp();
+    if (d < 256 && lt == 0) my_cnt[d] = base + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive prefix across warps (stability: warp chunks are in order)
+  uint32_t total = 0;
+  {
+    const int d = tid;  // kRsThreads == 256 digits
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) {
+      const uint32_t c = s_cnt[w * 256 + d];
+      s_cnt[w * 256 + d] = run;
+      run += c;
+    }
+    total = run;
+    uint64_t* my_status = status + (uint64_t)tile * 256 + d;
+    st_volatile(my_status, (tile == 0 ? kFlagInc : kFlagAgg) | total);
+  }
+  uint32_t tile_total;
+  const uint32_t start = block_exclusive_sum<kRsThreads>(total, s_misc + 1, &tile_total);
+  s_start[tid] = start;
+  // decoupled look-back, one digit per thread
+  {
+    const int d = tid;
+    uint64_t prefix = 0;
+    if (tile > 0) {
+      int64_t t = (int64_t)tile - 1;
+      while (t >= 0) {
+        uint64_t s;
+        do {
+          s = ld_volatile(status + (uint64_t)t * 256 + d);
+        } while ((s & ~kValMask) == 0);
+        prefix += s & kValMask;
+        if (s & kFlagInc) break;
+        --t;
+      }
+      st_volatile(status + (uint64_t)tile * 256 + d, kFlagInc | (prefix + total));
+    }
+    s_glob[d] = bucket_base[d] + (uint32_t)prefix;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kRsItems; ++j) {
+    const uint32_t d = dig[j];
+    if (d < 256) {
+      const uint32_t pos = s_start[d] + my_cnt[d] + rank[j];
+      s_keys[pos] = k[j];
+      s_vals[pos] = v[j];
+    }
+  }
+  __syncthreads();
+  const uint64_t left = count - tile_base;
+  const uint32_t valid = left < (uint64_t)kRsTile ? (uint32_t)left : (uint32_t)kRsTile;
+  for (uint32_t p = tid; p < valid; p += kRsThreads) {
+    const uint64_t key = s_keys[p];
+    const uint32_t d = (uint32_t)((key >> shift) & 255);
+    const uint32_t o = s_glob[d] + (p - s_start[d]);
+    keys_out[o] = key;
+    vals_out[o] = s_vals[p];
+  }
+}
+
+
+bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
+                      uint32_t* alt_vals, uint64_t count, int bits, bool ident_vals) {
+  if (count == 0) return false;
+  if (bits <= 0) bits = 1;  // identity values still need one materialising pass
+  if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "radix_sort_pairs: count >= 2^32");
+  static bool attr_done = false;
+  if (!attr_done) {
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
+    attr_done = true;
+  }
+  const int passes = (bits + 7) / 8;
+  const uint64_t tiles = ceil_div(count, kRsTile);
+  uint32_t* hist = ctx.slot_t<uint32_t>("rs.hist", 2 * 8 * 256 + 16);
+  uint32_t* base = hist + 8 * 256;
+  uint32_t* tickets = base + 8 * 256;
+  uint64_t* status = ctx.slot_t<uint64_t>("rs.status", tiles * 256);
+  DFM_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (2 * 8 * 256 + 16), ctx.stream));
+  {
+    ProfScope p(ctx, "sort", count * 8ull);  // one read of the keys for all digit histograms
+    const unsigned grid =
+        (unsigned)std::min<uint64_t>((uint64_t)ctx.num_sms * 8, ceil_div(count, 256));
+    radix_histogram_kernel<<<grid, 256, 0, ctx.stream>>>(keys, count, passes, hist);
+    DFM_LAUNCH_CHECK();
+    radix_bucket_scan_kernel<<<passes, 256, 0, ctx.stream>>>(hist, base);
+    DFM_LAUNCH_CHECK();
+  }
+  uint64_t* kin = keys;
+  uint32_t* vin = vals;
+  uint64_t* kout = alt_keys;
+  uint32_t* vout = alt_vals;
+  for (int p = 0; p < passes; ++p) {
+    DFM_CUDA(cudaMemsetAsync(status, 0, tiles * 256 * 8, ctx.stream));
+    {
+      ProfScope ps(ctx, "sort", count * 24ull);  // (key 8 + value 4) read + written
+      if (p == 0 && ident_vals)
+        onesweep_kernel<true><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+            kin, nullptr, kout, vout, (uint32_t)count, 8 * p, base + p * 256, status,
+            tickets + p);
+      else
+        onesweep_kernel<false><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+            kin, vin, kout, vout, (uint32_t)count, 8 * p, base + p * 256, status, tickets + p);
+      DFM_LAUNCH_CHECK();
+    }
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  const bool in_alt = (passes & 1) != 0;
+  return in_alt;
+}
+
+}  // namespace prims
+}  // namespace dfm

@@ -1,0 +1,175 @@
+// Device-wide primitives used by every minimizer (the B200 replacement of the
+// reference substrate, substrate.hpp:124-197):
+//   * lookback_scan  — single-pass prefix scan with decoupled look-back
+//                      (adjacent_diff + inclusive_scan, substrate.hpp:156-197)
+//   * radix_sort     — onesweep LSD radix sort of (u64 key, u32 value) pairs,
+//                      stable, 8-bit digits (par_sort, substrate.hpp:124-153)
+// Tiles are claimed through an atomic ticket so the look-back never waits on
+// a tile that has not been scheduled (forward progress under any residency).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dfm_internal.cuh"
+
+namespace dfm {
+namespace prims {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
+// look-back status word: [63:62] flag, [61:0] value (value + flag in one
+// single-copy-atomic 64-bit word, so no fences are needed around it)
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagInc = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t x, uint32_t* s_warp,
+                                                        uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < NT / 32 ? s_warp[lane] : 0;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NT / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
+    if (lane == NT / 32 - 1) s_warp[NT / 32] = wi;
+  }
+  __syncthreads();
+  const uint32_t r = s_warp[warp] + incl - x;
+  *total = s_warp[NT / 32];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ scan
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// in(i) -> u32 value; out(i, exclusive_prefix, value).  Sums must fit in 32 bits.
+template <class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(In in, Out out, uint64_t count,
+                                                                     uint64_t* status,
+                                                                     uint32_t* ticket,
+                                                                     uint64_t* total_out) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
+  __shared__ uint64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t base = tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const uint64_t idx = base + i;
+    v[i] = idx < count ? in(idx) : 0u;
+    sum += v[i];
+  }
+  uint32_t agg;
+  const uint32_t excl = block_exclusive_sum<kScanThreads>(sum, s_warp, &agg);
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint64_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile(status, kFlagInc | agg);
+    } else {
+      if (lane == 0) st_volatile(status + tile, kFlagAgg | agg);
+      int64_t pos = (int64_t)tile - 1 - lane;
+      while (true) {
+        uint64_t s = 0;
+        if (pos >= 0) {
+          do {
+            s = ld_volatile(status + pos);
+          } while ((s & ~kValMask) == 0);
+        } else {
+          s = kFlagInc;  // virtual inclusive zero before tile 0
+        }
+        const uint32_t inc_mask = __ballot_sync(0xffffffffu, (s & kFlagInc) != 0);
+        const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;
+        uint64_t val = (lane <= stop) ? (s & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc_mask) break;
+        pos -= 32;
+      }
+      if (lane == 0) st_volatile(status + tile, kFlagInc | (prefix + agg));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)s_prefix + excl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const uint64_t idx = base + i;
+    if (idx < count) out(idx, run, v[i]);
+    run += v[i];
+  }
+  if (total_out != nullptr && threadIdx.x == 0 && (tile + 1) * kScanTile >= count)
+    *total_out = s_prefix + agg;
+}
+
+// Launch: exclusive scan over [0,count); total written to *total_dev (device).
+template <class In, class Out>
+void lookback_scan(Ctx& ctx, const char* slot, uint64_t count, In in, Out out,
+                   uint64_t* total_dev) {
+  if (count == 0) {
+    if (total_dev) DFM_CUDA(cudaMemsetAsync(total_dev, 0, 8, ctx.stream));
+    return;
+  }
+  const uint64_t tiles = ceil_div(count, kScanTile);
+  uint8_t* scratch = ctx.slot_t<uint8_t>(slot, 16 + tiles * 8);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch);
+  uint64_t* status = reinterpret_cast<uint64_t*>(scratch + 16);
+  DFM_CUDA(cudaMemsetAsync(scratch, 0, 16 + tiles * 8, ctx.stream));
+  lookback_scan_kernel<In, Out><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(
+      in, out, count, status, ticket, total_dev);
+  DFM_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ radix sort
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsItems = 16;
+constexpr int kRsTile = kRsThreads * kRsItems;  // 4096
+constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 64;
+
+// Sorts (keys, vals) of length count on the low `bits` bits.  ident_vals: the
+// input values are 0..count-1 and `vals` is not read.  Uses alt_keys/alt_vals
+// as ping-pong buffers; returns which buffer set holds the result (false:
+// keys/vals, true: alt_*).  count < 2^32.
+bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
+                      uint32_t* alt_vals, uint64_t count, int bits, bool ident_vals);
+
+}  // namespace prims
+}  // namespace dfm

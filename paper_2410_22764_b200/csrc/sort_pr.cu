@@ -1,0 +1,353 @@
+// sortPR — sort-based partition refinement (paper Alg. 4; reference
+// min_sort.hpp:72-126), B200 edition.
+//
+// Per pass the reference sorts ALL n states by (block, signature), marks key
+// changes, scans the marks into dense labels and scatters them back.  Here:
+//
+//  * Only ACTIVE states are processed: states whose block has >= 2 members.
+//    A singleton block can never split, so its state keeps its label; the
+//    partition sequence (and so the pass count) is exactly the reference's.
+//  * Block ids are STABLE: when a block b splits, one sub-block keeps b and the
+//    others get fresh ids B, B+1, ... (dense, so ids stay < n).
+//  * The key (block[q], block[delta[a][q]] for a < k) is packed exactly into
+//    64 bits when (k+1)*bits(B-1) <= 64; otherwise it is a 64-bit hash, and
+//    every pair of equal-hash neighbours after the sort is verified on the
+//    full signature.  A collision aborts the pass (no state is written) and
+//    the pass is redone under a new hash seed: the result is always exact.
+//  * Grouping = onesweep radix sort + decoupled-look-back scan of run heads.
+//
+// Kernels: K1 sig_kernel, K3 radix sort (prims.cu), K4 heads scan /
+// keep_kernel / fresh scan / scatter_kernel, active-list compaction scan,
+// K5 canonicalize (canon.cu).
+#include <algorithm>
+#include <vector>
+
+#include "prims.cuh"
+
+namespace dfm {
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct SigParams {
+  const uint32_t* __restrict__ delta;
+  uint64_t n;
+  uint32_t k;
+  const uint32_t* __restrict__ block;
+  const uint32_t* __restrict__ act;  // nullptr: identity (all states)
+  uint64_t m;
+  int w;  // packed field width
+  uint64_t seed;
+  uint64_t* __restrict__ keys;
+  uint32_t* __restrict__ sig;  // (k+1) words per active item, hashed mode only
+};
+
+// K1: signature gather + key build, one thread per active state.  delta rows
+// are read coalesced (active list is ascending in q); block[] is gathered.
+template <bool kHashed>
+__global__ void __launch_bounds__(256) sig_kernel(SigParams p) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+    const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+    const uint32_t b = p.block[q];
+    if (!kHashed) {
+      uint64_t key = b;
+      for (uint32_t a = 0; a < p.k; ++a)
+        key = (key << p.w) | p.block[p.delta[(uint64_t)a * p.n + q]];
+      p.keys[i] = key;
+    } else {
+      uint32_t* row = p.sig + i * (uint64_t)(p.k + 1);
+      row[0] = b;
+      uint64_t h = mix64(p.seed * kGolden + b);
+      for (uint32_t a = 0; a < p.k; ++a) {
+        const uint32_t s = p.block[p.delta[(uint64_t)a * p.n + q]];
+        row[a + 1] = s;
+        h = mix64(h + kGolden + s);
+      }
+      p.keys[i] = h;
+    }
+  }
+}
+
+// run heads over the sorted keys (+ exact verification of equal-hash neighbours)
+struct HeadIn {
+  const uint64_t* keys;
+  const uint32_t* vals;
+  const uint32_t* sig;  // nullptr in packed mode
+  uint32_t words;
+  unsigned long long* collision;
+  __device__ uint32_t operator()(uint64_t j) const {
+    if (j == 0) return 1u;
+    if (keys[j] != keys[j - 1]) return 1u;
+    if (sig != nullptr) {
+      const uint32_t* a = sig + (uint64_t)vals[j] * words;
+      const uint32_t* b = sig + (uint64_t)vals[j - 1] * words;
+      for (uint32_t i = 0; i < words; ++i) {
+        if (a[i] != b[i]) {
+          atomicOr(collision, 1ull);
+          break;
+        }
+      }
+    }
+    return 0u;
+  }
+};
+struct HeadOut {
+  uint32_t* run_of;
+  uint32_t* runstart;
+  uint64_t m;
+  __device__ void operator()(uint64_t j, uint32_t excl, uint32_t v) const {
+    const uint32_t run = excl + v - 1;
+    run_of[j] = run;
+    if (v) runstart[run] = (uint32_t)j;
+    if (j + 1 == m) runstart[run + 1] = (uint32_t)m;
+  }
+};
+
+__device__ __forceinline__ unsigned long long keep_tag(uint32_t epoch, uint32_t j) {
+  return ((unsigned long long)epoch << 32) | (0xFFFFFFFFu - j);
+}
+
+// one thread per run: the run with the smallest head position in each old
+// block keeps the block's id (epoch-tagged atomicMax: no per-pass reset)
+__global__ void __launch_bounds__(256) keep_kernel(const uint32_t* __restrict__ runstart,
+                                                   const uint32_t* __restrict__ vals,
+                                                   const uint32_t* __restrict__ act,
+                                                   const uint32_t* __restrict__ block,
+                                                   uint32_t* __restrict__ runblock,
+                                                   unsigned long long* cells,
+                                                   const uint64_t* scalars, uint32_t epoch) {
+  if (scalars[2] != 0) return;  // collision: pass is void
+  const uint64_t R = scalars[0];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride) {
+    const uint32_t j = runstart[r];
+    const uint32_t pos = vals[j];
+    const uint32_t q = act ? act[pos] : pos;
+    const uint32_t b = block[q];
+    runblock[r] = b;
+    atomicMax(&cells[b], keep_tag(epoch, j));
+  }
+}
+
+struct FreshIn {
+  const uint32_t* runblock;
+  const uint32_t* runstart;
+  const unsigned long long* cells;
+  const uint64_t* scalars;
+  uint32_t epoch;
+  __device__ uint32_t operator()(uint64_t r) const {
+    if (r >= scalars[0] || scalars[2] != 0) return 0u;
+    return cells[runblock[r]] != keep_tag(epoch, runstart[r]) ? 1u : 0u;
+  }
+};
+struct FreshOut {
+  const uint32_t* runblock;
+  uint32_t* newid;
+  const uint64_t* scalars;
+  uint32_t B;
+  __device__ void operator()(uint64_t r, uint32_t excl, uint32_t v) const {
+    if (r < scalars[0]) newid[r] = v ? B + excl : runblock[r];
+  }
+};
+
+__global__ void __launch_bounds__(256) scatter_kernel(uint64_t m, const uint32_t* __restrict__ vals,
+                                                      const uint32_t* __restrict__ act,
+                                                      const uint32_t* __restrict__ run_of,
+                                                      const uint32_t* __restrict__ runstart,
+                                                      const uint32_t* __restrict__ newid,
+                                                      uint32_t* __restrict__ block,
+                                                      uint8_t* __restrict__ flag,
+                                                      const uint64_t* scalars) {
+  if (scalars[2] != 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint32_t r = run_of[j];
+    const uint32_t len = runstart[r + 1] - runstart[r];
+    const uint32_t pos = vals[j];
+    const uint32_t q = act ? act[pos] : pos;
+    block[q] = newid[r];
+    flag[q] = len >= 2 ? 1 : 0;
+  }
+}
+
+struct ActIn {
+  const uint32_t* act;
+  const uint8_t* flag;
+  __device__ uint32_t operator()(uint64_t i) const {
+    const uint32_t q = act ? act[i] : (uint32_t)i;
+    return flag[q];
+  }
+};
+struct ActOut {
+  const uint32_t* act;
+  uint32_t* act_next;
+  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
+    if (v) act_next[excl] = act ? act[i] : (uint32_t)i;
+  }
+};
+
+__global__ void count_accepting_kernel(const uint8_t* __restrict__ acc, uint64_t n,
+                                       unsigned long long* out) {
+  uint32_t c = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    c += acc[q] != 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+__global__ void init_block_kernel(const uint8_t* __restrict__ acc, uint64_t n, bool split,
+                                  uint32_t* __restrict__ block) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    block[q] = (split && acc[q] == 0) ? 1u : 0u;
+}
+
+unsigned grid_for(const Ctx& ctx, uint64_t items, int threads = 256) {
+  const uint64_t want = ceil_div(std::max<uint64_t>(items, 1), threads);
+  return (unsigned)std::min<uint64_t>(want, (uint64_t)ctx.num_sms * 16);
+}
+
+int bit_width_u32(uint32_t x) { return x == 0 ? 0 : 32 - __builtin_clz(x); }
+
+}  // namespace
+
+AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {
+  AlgoOut out;
+  const uint64_t n = d.n;
+  const uint32_t k = d.k;
+  out.peak_memory_estimate = n * (16 + 4ull * k);  // min_sort.hpp:121
+  uint32_t* block = ctx.slot_t<uint32_t>("sp.block", n);
+  uint8_t* flag = ctx.slot_t<uint8_t>("sp.flag", n);
+  uint32_t* act_buf[2] = {ctx.slot_t<uint32_t>("sp.act0", n), ctx.slot_t<uint32_t>("sp.act1", n)};
+  uint64_t* keysA = ctx.slot_t<uint64_t>("sp.keysA", n);
+  uint64_t* keysB = ctx.slot_t<uint64_t>("sp.keysB", n);
+  uint32_t* valsA = ctx.slot_t<uint32_t>("sp.valsA", n);
+  uint32_t* valsB = ctx.slot_t<uint32_t>("sp.valsB", n);
+  uint32_t* run_of = ctx.slot_t<uint32_t>("sp.runof", n);
+  uint32_t* runstart = ctx.slot_t<uint32_t>("sp.runstart", n + 1);
+  uint32_t* runblock = ctx.slot_t<uint32_t>("sp.runblock", n);
+  uint32_t* newid = ctx.slot_t<uint32_t>("sp.newid", n);
+  auto* cells = ctx.slot_t<unsigned long long>("sp.cells", n);
+  uint32_t* sig = nullptr;
+  uint64_t* sc = ctx.d_scalars;  // [0] runs [1] fresh blocks [2] collision [3] next active [4] acc
+  DFM_CUDA(cudaMemsetAsync(cells, 0, n * 8, ctx.stream));
+  DFM_CUDA(cudaMemsetAsync(sc, 0, 64 * 8, ctx.stream));
+
+  // init, min_sort.hpp:80-88: two blocks iff both acceptance classes are non-empty
+  {
+    ProfScope p(ctx, "init");
+    count_accepting_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(
+        d.acc, n, reinterpret_cast<unsigned long long*>(sc + 4));
+    DFM_LAUNCH_CHECK();
+  }
+  DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars, sc, 64 * 8, cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  const uint64_t n_acc = ctx.h_scalars[4];
+  const bool split = n_acc > 0 && n_acc < n;
+  uint32_t B = split ? 2u : 1u;
+  {
+    ProfScope p(ctx, "init");
+    init_block_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, block);
+    DFM_LAUNCH_CHECK();
+  }
+
+  const uint32_t* act = nullptr;  // identity: every state active at pass 1
+  int act_sel = 0;
+  uint64_t m = n;
+  uint32_t epoch = 0;
+  uint64_t seed = 0x5EED0001ull;
+  std::vector<uint32_t> trace_buf;
+
+  while (true) {
+    if (dl.expired()) {
+      out.status = DFM_STATUS_TIMEOUT;
+      return out;
+    }
+    ++epoch;
+    const int w = std::max(1, bit_width_u32(B - 1));
+    const bool packed = (uint64_t)(k + 1) * (uint64_t)w <= 64;
+    const int bits = packed ? (int)((k + 1) * w) : 64;
+    DFM_CUDA(cudaMemsetAsync(sc, 0, 4 * 8, ctx.stream));
+    uint32_t* act_next = act_buf[act_sel ^ 1];
+    if (m > 0) {
+      if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sp.sig", n * (uint64_t)(k + 1));
+      SigParams sp{d.delta, n, k, block, act, m, w, seed, keysA, sig};
+      {
+        // delta stream 4k + successor-block gather 4k + own block 4 + active id 4 + key 8
+        // (+ signature row 4(k+1) when hashed) per active state
+        ProfScope p(ctx, "sig",
+                    m * (8ull * k + 4 + (act ? 4 : 0) + 8 + (packed ? 0 : 4ull * (k + 1))));
+        if (packed) sig_kernel<false><<<grid_for(ctx, m), 256, 0, ctx.stream>>>(sp);
+        else sig_kernel<true><<<grid_for(ctx, m), 256, 0, ctx.stream>>>(sp);
+        DFM_LAUNCH_CHECK();
+      }
+      const bool alt = prims::radix_sort_pairs(ctx, keysA, valsA, keysB, valsB, m, bits, true);
+      const uint64_t* ks = alt ? keysB : keysA;
+      const uint32_t* vs = alt ? valsB : valsA;
+      {
+        ProfScope p(ctx, "scan", m * 16ull);  // key 8 + run_of 4 + runstart 4
+        prims::lookback_scan(ctx, "sc.heads", m,
+                             HeadIn{ks, vs, packed ? nullptr : sig, k + 1,
+                                    reinterpret_cast<unsigned long long*>(sc + 2)},
+                             HeadOut{run_of, runstart, m}, sc + 0);
+      }
+      {
+        ProfScope p(ctx, "relabel");
+        keep_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(runstart, vs, act, block, runblock,
+                                                              cells, sc, epoch);
+        DFM_LAUNCH_CHECK();
+      }
+      {
+        ProfScope p(ctx, "scan");
+        prims::lookback_scan(ctx, "sc.fresh", m, FreshIn{runblock, runstart, cells, sc, epoch},
+                             FreshOut{runblock, newid, sc, B}, sc + 1);
+      }
+      {
+        // run_of 4 + runstart pair 8 + value 4 + active id 4 + new id 4 + block write 4 + flag 1
+        ProfScope p(ctx, "relabel", m * 29ull);
+        scatter_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, vs, act, run_of, runstart,
+                                                                 newid, block, flag, sc);
+        DFM_LAUNCH_CHECK();
+      }
+      {
+        ProfScope p(ctx, "scan", m * 9ull);  // active id 4 + flag 1 + survivor id 4
+        prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+      }
+    }
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars, sc, 4 * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (ctx.h_scalars[2] != 0) {  // hash collision: redo the pass under a new seed
+      seed = seed * kGolden + 0x632BE59BD9B4E019ull;
+      continue;
+    }
+    const uint64_t fresh = ctx.h_scalars[1];
+    ++out.iterations;
+    const uint32_t B_next = B + (uint32_t)fresh;
+    if (trace && trace->on_pass) {
+      trace_buf.resize(n);
+      DFM_CUDA(cudaMemcpyAsync(trace_buf.data(), block, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      trace->on_pass(trace->user, out.iterations, trace_buf.data(), (uint32_t)n, B_next);
+    }
+    if (fresh == 0) break;  // fixpoint, min_sort.hpp:111-117
+    B = B_next;
+    m = ctx.h_scalars[3];
+    act = act_next;
+    act_sel ^= 1;
+  }
+  out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+  out.num_blocks = canonicalize_dev(ctx, block, n, out.canon_dev);
+  out.status = DFM_STATUS_OK;
+  return out;
+}
+
+}  // namespace dfm

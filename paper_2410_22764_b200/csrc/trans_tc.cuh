@@ -1,0 +1,28 @@
+// tcgen05 int8 squaring engine for the Cho–Huynh closure (see trans_tc.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "dfm_internal.cuh"
+
+namespace dfm {
+
+struct TransTcState {
+  uint64_t V = 0;     // pair nodes
+  uint64_t Vp = 0;    // padded to the GEMM tile
+  int8_t* reach = nullptr;   // Vp x Vp, row-major (A operand, K-major)
+  int8_t* reachT = nullptr;  // transpose (B operand, K-major)
+  int8_t* next = nullptr;
+  int8_t* nextT = nullptr;
+};
+
+namespace trans_tc {
+bool usable(uint64_t V);
+TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V);
+// one pass: next = reach | (reach*reach > 0); apart_next |= rows reaching apart;
+// then swaps reach<->next inside the state
+void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* apart,
+                          unsigned long long* apart_next);
+}  // namespace trans_tc
+
+}  // namespace dfm

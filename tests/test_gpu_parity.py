@@ -1,0 +1,272 @@
+"""GPU parity: libdfm (sm_100a kernels, called through the C-ABI) against the
+oracle, the reference's golden vectors and its known-answer tests.  Bar:
+bit-exact canonical partition, block count, pass count and closure steps."""
+import numpy as np
+import pytest
+
+import paper_2410_22764_b200 as dfm
+from oracle import oracle as O
+from tests.helpers import digest, gen, to_dfa
+
+pytestmark = pytest.mark.gpu
+MIN, MAX, ARB = (dfm.RacePolicy.deterministic_min, dfm.RacePolicy.deterministic_max,
+                 dfm.RacePolicy.arbitrary_winner)
+
+
+def check(r, exp, what):
+    assert r.stats.status == dfm.RunStatus.ok, what
+    assert r.partition.num_blocks == exp["num_blocks"], what
+    assert r.stats.iterations == exp["iterations"], what
+    assert r.stats.closure_steps == exp["closure_steps"], what
+    assert r.stats.peak_memory_estimate == exp["peak_memory_estimate"], what
+    assert digest(r.partition.block) == exp["sha256"], what
+
+
+def test_golden_vectors(eng, golden):
+    for rec in golden["vectors"]:
+        d = to_dfa(gen(rec["spec"]))
+        tr = dfm.SortTrace()
+        check(eng.sort_pr(d, dfm.SortOptions(trace=tr)), rec["sort"], (rec["name"], "sort"))
+        assert tr.block_counts == rec["sort"]["trace_counts"], rec["name"]
+        if "naive_min" in rec:
+            check(eng.naive_pr(d, dfm.PrOptions(policy=MIN)), rec["naive_min"], (rec["name"], "min"))
+            check(eng.naive_pr(d, dfm.PrOptions(policy=MAX)), rec["naive_max"], (rec["name"], "max"))
+            check(eng.trans_pr(d, dfm.PrOptions(policy=MIN)), rec["transpr_min"],
+                  (rec["name"], "transpr"))
+            # scheduling-dependent pass counts: only the partition is pinned
+            assert digest(eng.naive_pr(d, dfm.PrOptions(policy=ARB)).partition.block) == \
+                rec["naive_min"]["sha256"]
+            assert digest(eng.naive_pr_cas(d).partition.block) == rec["naive_min"]["sha256"]
+        if "trans" in rec:
+            ins = dfm.TransInspect()
+            r = eng.trans_minimize(d, inspect=ins)
+            assert r.partition.block.tolist() == rec["trans"]["block"], rec["name"]
+            assert r.stats.iterations == rec["trans"]["iterations"], rec["name"]
+            assert ins.apart_popcounts == rec["trans"]["apart_popcounts"], rec["name"]
+
+
+def test_oracle_agreement_500(eng):
+    """acceptance.cpp:40-79 grid, checked against the C oracle."""
+    rng = np.random.default_rng(1001)
+    for rnd in range(500):
+        n = int(rng.integers(1, 513))
+        k = int(rng.integers(1, 5))
+        p = [0.0, 0.1, 0.5, 1.0][rnd % 4]
+        pair = O.random_dfa(n, k, int(rng.integers(1, 2 ** 62)), p)
+        d = to_dfa(pair)
+        ref = O.sort_pr(*pair)
+        r = eng.sort_pr(d)
+        assert r.partition.block.tolist() == ref.block.tolist() and \
+            r.stats.iterations == ref.iterations, (rnd, n, k)
+        ref_min = O.naive_pr(*pair, "min")
+        r = eng.naive_pr(d, dfm.PrOptions(policy=MIN))
+        assert (r.partition.block == ref_min.block).all() and \
+            r.stats.iterations == ref_min.iterations, (rnd, n, k)
+        assert (eng.naive_pr_cas(d).partition.block == ref.block).all()
+        ref_tp = O.trans_pr(*pair, "min")
+        r = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+        assert (r.partition.block == ref_tp.block).all()
+        assert (r.stats.iterations, r.stats.closure_steps) == (ref_tp.iterations, ref_tp.closure_steps)
+        if n <= 64:
+            ref_t = O.trans_minimize(*pair)
+            r = eng.trans_minimize(d)
+            assert (r.partition.block == ref_t.block).all() and \
+                r.stats.iterations == ref_t.iterations, (rnd, n, k)
+
+
+def test_iteration_laws(eng, pins):
+    for idx in pins["fib_law"]["indices"]:
+        d = to_dfa(O.fib_dfa(idx))
+        N = d.num_states
+        for r in (eng.sort_pr(d), eng.naive_pr(d, dfm.PrOptions(policy=MIN))):
+            assert (r.partition.num_blocks, r.stats.iterations) == (N, N - 1)
+    for b in pins["bits_law"]["bits"]:
+        d = to_dfa(O.bit_splitter(b))
+        for r in (eng.sort_pr(d), eng.naive_pr(d, dfm.PrOptions(policy=MIN))):
+            assert (r.partition.num_blocks, r.stats.iterations) == (1 << b, max(b, 1))
+    for f in pins["flat"]:
+        d = to_dfa(O.random_dfa(*f["random"]))
+        r = {"sort": lambda: eng.sort_pr(d),
+             "naive_min": lambda: eng.naive_pr(d, dfm.PrOptions(policy=MIN)),
+             "transpr_min": lambda: eng.trans_pr(d, dfm.PrOptions(policy=MIN)),
+             "trans": lambda: eng.trans_minimize(d)}[f["algo"]]()
+        assert (r.partition.num_blocks, r.stats.iterations) == (f["blocks"], f["iterations"]), f
+    for fp in pins["sort_first_pass_counts"]:
+        pair = O.bit_splitter(fp["arg"]) if fp["family"] == "bits" else \
+            (np.array(fp["delta"], np.uint32), np.array(fp["acc"], np.uint8))
+        tr = dfm.SortTrace()
+        eng.sort_pr(to_dfa(pair), dfm.SortOptions(trace=tr))
+        c = tr.block_counts
+        assert c[0] == fp["first_count"]
+        assert all(x < y for x, y in zip(c[:-2], c[1:-1])) and c[-1] == c[-2]
+
+
+def test_edge_cases(eng):
+    lone = dfm.Dfa.from_rows([[0]], [1])
+    for r in (eng.sort_pr(lone), eng.naive_pr(lone, dfm.PrOptions(policy=MIN)),
+              eng.naive_pr_cas(lone), eng.trans_pr(lone, dfm.PrOptions(policy=MIN)),
+              eng.trans_minimize(lone)):
+        assert (r.partition.num_blocks, r.stats.iterations) == (1, 1)
+    b1 = to_dfa(O.bit_splitter(1))  # empty alphabet: keys reduce to the block label
+    assert b1.alphabet_size == 0
+    r = eng.sort_pr(b1)
+    assert r.partition.num_blocks == 2 and r.stats.iterations == 1
+    bad = dfm.Dfa.from_rows([[0, 5]], [0, 1])
+    with pytest.raises(dfm.EngineError):
+        eng.sort_pr(bad)
+    with pytest.raises(dfm.EngineError):
+        eng.run_algorithm(dfm.Algo.oracle, lone)
+    # the context survives a rejected call
+    assert eng.sort_pr(lone).partition.num_blocks == 1
+
+
+def test_transpr_pins(eng, pins):
+    t = pins["transpr"]
+    d = to_dfa(O.chain_dfa(10))
+    e = eng.expand_alphabet(d)
+    assert e.levels == t["chain10"]["levels"] and e.row(0, 3)[0] == t["chain10"]["row_0_3_at_0"]
+    assert (e.row(0, 0) == d.delta[0]).all()
+    ident = dfm.Dfa(10, 2, np.vstack([d.delta, np.arange(10, dtype=np.uint32)]), d.accepting)
+    e2 = eng.expand_alphabet(ident)
+    assert all((e2.row(1, lv) == np.arange(10)).all() for lv in range(e2.levels))
+    rng = np.random.default_rng(71)
+    for _ in range(15):
+        pair = O.random_dfa(int(rng.integers(1, 65)), int(rng.integers(1, 4)),
+                            int(rng.integers(1, 2 ** 62)), 0.5)
+        rows, levels = O.expand_alphabet(*pair)
+        e = eng.expand_alphabet(to_dfa(pair))
+        assert e.levels == levels and (e.delta == rows).all()
+    tiny = dfm.Limits(max_memory_bytes=t["guard"]["limit"])
+    with pytest.raises(dfm.CapacityError) as ei:
+        eng.expand_alphabet(to_dfa(O.chain_dfa(256)), tiny)
+    assert ei.value.required_bytes() == t["guard"]["required"]
+    r = eng.trans_pr(to_dfa(O.chain_dfa(256)), dfm.PrOptions(policy=MIN), tiny)
+    assert r.stats.status == dfm.RunStatus.capacity_exceeded and r.partition.block.size == 0
+    assert r.stats.peak_memory_estimate == t["guard"]["required"]
+    assert eng.trans_pr(to_dfa(O.chain_dfa(1024)), dfm.PrOptions(policy=MIN)).stats.closure_steps == 10
+    c64 = to_dfa(O.chain_dfa(64))
+    plain = eng.naive_pr(c64, dfm.PrOptions(policy=MIN))
+    closed = eng.trans_pr(c64, dfm.PrOptions(policy=MIN))
+    assert plain.stats.iterations == 63 and closed.stats.iterations <= 14
+    assert closed.partition.num_blocks == 64
+    r = eng.trans_pr(to_dfa(O.fib_dfa(21)), dfm.PrOptions(policy=MIN))
+    f = t["fib21"]
+    assert (r.stats.iterations, r.stats.closure_steps, r.partition.num_blocks) == \
+        (f["iterations"], f["closure_steps"], f["blocks"])
+    assert [eng.trans_pr(to_dfa(O.fib_dfa(i)), dfm.PrOptions(policy=MIN)).stats.iterations
+            for i in range(5, 13)] == t["fib_5_12"]["iterations"]
+    for k in t["chain_pow2"]["k"]:
+        r = eng.trans_pr(to_dfa(O.chain_dfa(1 << k)), dfm.PrOptions(policy=MIN))
+        assert (r.stats.iterations, r.stats.closure_steps) == (k + 1, k)
+
+
+def test_trans_pins(eng, pins):
+    t = pins["trans"]
+    for idx, passes in {**t["fib_passes"]["values"], **t["fib_10_11"]["values"]}.items():
+        d = to_dfa(O.fib_dfa(int(idx)))
+        r = eng.trans_minimize(d)
+        assert (r.stats.iterations, r.partition.num_blocks) == (passes, d.num_states)
+    d = to_dfa(O.random_dfa(*t["guard"]["random"]))
+    r = eng.trans_minimize(d, dfm.Limits(max_memory_bytes=t["guard"]["limit"]))
+    assert r.stats.status == dfm.RunStatus.capacity_exceeded
+    assert r.stats.peak_memory_estimate == t["guard"]["peak"] and r.partition.block.size == 0
+    # apartness invariants (test_min_trans.cpp:65-113)
+    rng = np.random.default_rng(82)
+    for _ in range(20):
+        n = int(rng.integers(2, 13))
+        k = int(rng.integers(1, 4))
+        pair = O.random_dfa(n, k, int(rng.integers(1, 2 ** 62)), 0.4)
+        ins = dfm.TransInspect()
+        eng.trans_minimize(to_dfa(pair), inspect=ins)
+        A = ins.apart.reshape(n, n).astype(bool)
+        assert not A.diagonal().any() and (A == A.T).all()
+        notA = ~A
+        assert not (notA.astype(int) @ notA.astype(int) > 0)[A].any()  # transitivity of not-apart
+        delta = pair[0]
+        for a in range(k):
+            assert not (A[np.ix_(delta[a], delta[a])] & notA).any()  # edge-closed
+        assert all(x <= y for x, y in zip(ins.apart_popcounts, ins.apart_popcounts[1:]))
+
+
+def test_timeouts_report_status(eng):
+    r = eng.sort_pr(to_dfa(O.fib_dfa(18)), 1)
+    assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
+    r = eng.naive_pr(to_dfa(O.fib_dfa(18)), dfm.PrOptions(policy=MIN, timeout_ms=1))
+    assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
+    r = eng.trans_minimize(to_dfa(O.fib_dfa(11)), dfm.Limits(timeout_ms=1))
+    assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
+
+
+def test_c1_and_comb_pins(eng, pins):
+    c = pins["c1"]
+    for seed, exp in c["seeds"].items():
+        d = to_dfa(O.random_dfa(c["n"], c["k"], int(seed), c["p"]))
+        tr = dfm.SortTrace()
+        r = eng.sort_pr(d, dfm.SortOptions(trace=tr) if seed == "1" else None)
+        assert (r.stats.iterations, r.partition.num_blocks) == (exp["sort"], c["blocks"])
+        if seed == "1":
+            assert tr.block_counts == c["seed1_sort_trace"]
+        r = eng.naive_pr(d, dfm.PrOptions(policy=MIN))
+        assert (r.stats.iterations, r.partition.num_blocks) == (exp["naive_min"], c["blocks"])
+    for L, e in pins["comb"]["L"].items():
+        d = to_dfa(O.comb_dfa(int(L), pins["comb"]["t"]))
+        assert eng.sort_pr(d).stats.iterations == e["sort"]
+        assert eng.naive_pr(d, dfm.PrOptions(policy=MIN)).stats.iterations == e["naive"]
+        r = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+        assert (r.stats.iterations, r.stats.closure_steps, r.partition.num_blocks) == \
+            (e["transpr"], e["closure"], e["blocks"])
+
+
+def test_larger_inputs_vs_oracle(eng):
+    for pair in (O.random_dfa(1_000_000, 4, 5, 0.5), O.vlts_dfa(1000, 1_000_000, 10),
+                 O.random_dfa(300_000, 1, 9, 0.5)):
+        ref = O.sort_pr(*pair)
+        d = to_dfa(pair)
+        r = eng.sort_pr(d)
+        assert r.stats.iterations == ref.iterations
+        assert (r.partition.block == ref.block).all()
+        rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+        assert (rt.partition.block == ref.block).all()
+
+
+def test_device_generator_bit_exact(eng):
+    for n, k, seed in ((1, 1, 4), (12345, 3, 99), (1 << 20, 4, 1)):
+        dd = eng.random_dfa_device(n, k, seed, 0.5)
+        got = dd.download()
+        od, oa = O.random_dfa(n, k, seed, 0.5)
+        assert (got.delta == od).all() and (got.accepting == oa).all()
+        dd.free()
+
+
+def test_full_size_properties(eng):
+    """1e8 states, k=4 (north-star size): size-independent checks — the result is
+    a congruence refining acceptance, and its quotient is already minimal."""
+    n, k = 100_000_000, 4
+    dd = eng.random_dfa_device(n, k, 1, 0.5)
+    nb, st = eng.run_device(dfm.Algo.sort, dd)
+    assert st.status == dfm.RunStatus.ok and 1 <= nb <= n
+    import torch
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    nb2, st2 = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
+    assert (nb2, st2.iterations) == (nb, st.iterations)
+    host = dd.download()
+    block = torch.from_numpy(host.delta.view(np.int32)).cuda()
+    acc = torch.from_numpy(host.accepting).cuda()
+    lab = out.long()
+    # canonical: first occurrences of labels appear in increasing order
+    first = torch.full((nb,), n, dtype=torch.long, device="cuda").scatter_reduce(
+        0, lab, torch.arange(n, device="cuda"), reduce="amin")
+    assert bool((first[1:] > first[:-1]).all())
+    # acceptance constant on blocks; successors' blocks a function of the block
+    acc_b = torch.zeros(nb, dtype=torch.uint8, device="cuda").scatter_(0, lab, acc)
+    assert bool((acc_b[lab] == acc).all())
+    rep = first  # representative state of each block
+    q_rows = []
+    for a in range(k):
+        succ = lab[block[a].long()]
+        assert bool((succ == succ[rep][lab]).all())
+        q_rows.append(succ[rep].to(torch.int32).cpu().numpy().astype(np.uint32))
+    quot = dfm.Dfa(nb, k, np.vstack(q_rows), acc[rep].cpu().numpy(), 0)
+    rq = eng.sort_pr(quot)
+    assert rq.partition.num_blocks == nb  # quotient is minimal
+    dd.free()
