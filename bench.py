@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--p", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--sortpr-engine", default="hash", choices=["hash", "radix"])
     ap.add_argument("--cpu-sample-n", type=int, default=10_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -187,6 +188,7 @@ def config(args, world, iters, blocks):
                         f"p={args.p}) — north-star 1-GPU config (SURVEY 8(d) C5)"
             if args.algo == "sort" else f"{args.algo} on random_dfa(n={args.n}, k={args.k})",
             "algo": args.algo, "n": args.n, "k": args.k, "passes": iters, "blocks": blocks,
+            "sortpr_engine": args.sortpr_engine if args.algo == "sort" else None,
             "parallelism": "replicas" if world > 1 else "single",
             "l2": "inputs larger than L2 (delta = 4nk bytes)" if 4 * args.n * args.k > (126 << 20)
             else "L2 flushed between timed steps"}
@@ -201,6 +203,7 @@ def run_ours(args, rank: int, world: int, local: int):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     eng = dfm.Engine(local)
+    eng.set_sortpr_engine(args.sortpr_engine)
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream.cuda_stream)
     algo = {"sort": dfm.Algo.sort, "naive": dfm.Algo.naive, "transpr": dfm.Algo.transpr,

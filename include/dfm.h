@@ -107,6 +107,13 @@ void dfm_ctx_destroy(dfm_ctx* ctx);
 const char* dfm_last_error(const dfm_ctx* ctx);
 /* Use an external CUDA stream (cudaStream_t as void*); NULL restores the ctx's own. */
 int dfm_ctx_set_stream(dfm_ctx* ctx, void* stream);
+/* sortPR grouping engine: both give the reference's partitions and pass
+ * counts.  HASH (default): active states grouped through an open-addressing table;
+ * RADIX: the paper's sort — onesweep LSD radix sort + look-back scans.  The
+ * DFM_SORTPR_ENGINE=radix|hash environment variable sets the default per context. */
+#define DFM_SORTPR_HASH 0
+#define DFM_SORTPR_RADIX 1
+int dfm_ctx_set_sortpr_engine(dfm_ctx* ctx, int engine);
 /* Record per-kernel CUDA-event timings for subsequent calls (bench/roofline). */
 int dfm_ctx_set_profiling(dfm_ctx* ctx, int enabled);
 /* Read back timing for a kernel family ("sig", "sort", "scan", "relabel", "elect",

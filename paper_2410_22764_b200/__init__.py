@@ -244,6 +244,7 @@ def _load():
         "dfm_last_error": (C.c_char_p, [vp]),
         "dfm_ctx_set_stream": (C.c_int, [vp, vp]),
         "dfm_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
+        "dfm_ctx_set_sortpr_engine": (C.c_int, [vp, C.c_int]),
         "dfm_profile_get": (C.c_int, [vp, C.c_char_p, C.POINTER(u64), C.POINTER(C.c_double),
                                       C.POINTER(u64)]),
         "dfm_kernel_launches": (u64, []),
@@ -538,6 +539,11 @@ class Engine:
     # -- profiling
     def set_stream(self, stream_ptr: Optional[int]) -> None:
         self._check(self.lib.dfm_ctx_set_stream(self.handle, stream_ptr))
+
+    def set_sortpr_engine(self, engine: str) -> None:
+        """'hash' (default) or 'radix' (the paper's sort); same results."""
+        self._check(self.lib.dfm_ctx_set_sortpr_engine(
+            self.handle, {"hash": 0, "radix": 1}[engine]))
 
     def set_profiling(self, on: bool) -> None:
         self._check(self.lib.dfm_ctx_set_profiling(self.handle, int(bool(on))))

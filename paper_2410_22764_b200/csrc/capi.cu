@@ -2,6 +2,7 @@
 // exceptions into dfm_err codes, uploads host DFAs, dispatches algorithms and
 // copies canonical partitions back.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -124,7 +125,8 @@ AlgoOut dispatch(Ctx& ctx, int32_t algo, const DevDfa& dd, int32_t policy, const
     case DFM_ALGO_NAIVE_CAS:
       return run_leader_election(ctx, dd, dd.delta, dd.k, DFM_POLICY_ARBITRARY, true, dl, trace);
     case DFM_ALGO_SORT:
-      return run_sort_pr(ctx, dd, dl, trace);
+      return ctx.sortpr_engine == DFM_SORTPR_RADIX ? run_sort_pr(ctx, dd, dl, trace)
+                                                   : run_sort_pr_hash(ctx, dd, dl, trace);
     case DFM_ALGO_TRANSPR:
       return run_trans_pr(ctx, dd, policy, lim, dl);
     case DFM_ALGO_ORACLE:
@@ -180,7 +182,10 @@ const char* dfm_version(void) { return "libdfm 1 (B200 sm_100a)"; }
 int dfm_ctx_create(int device, dfm_ctx** out) {
   if (out == nullptr) return DFM_ERR_INVALID;
   try {
-    *out = reinterpret_cast<dfm_ctx*>(new Ctx(device));
+    Ctx* ctx = new Ctx(device);
+    if (const char* e = std::getenv("DFM_SORTPR_ENGINE"))
+      ctx->sortpr_engine = std::strcmp(e, "radix") == 0 ? DFM_SORTPR_RADIX : DFM_SORTPR_HASH;
+    *out = reinterpret_cast<dfm_ctx*>(ctx);
     return DFM_OK;
   } catch (const Error& e) {
     g_create_error = e.what();
@@ -200,6 +205,14 @@ int dfm_ctx_set_stream(dfm_ctx* c, void* stream) {
   return guarded(c, [&](Ctx& ctx) {
     ctx.sync();
     ctx.stream = stream ? static_cast<cudaStream_t>(stream) : ctx.own_stream;
+  });
+}
+
+int dfm_ctx_set_sortpr_engine(dfm_ctx* c, int engine) {
+  return guarded(c, [&](Ctx& ctx) {
+    if (engine != DFM_SORTPR_HASH && engine != DFM_SORTPR_RADIX)
+      throw Error(DFM_ERR_INVALID, "unknown sortPR engine");
+    ctx.sortpr_engine = engine;
   });
 }
 

@@ -81,6 +81,8 @@ struct Ctx {
   // pinned host staging
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // sortPR grouping engine: DFM_SORTPR_HASH (default) or DFM_SORTPR_RADIX
+  int sortpr_engine = 0;
   // profiling
   bool profiling = false;
   struct Pending {
@@ -148,6 +150,7 @@ struct AlgoOut {
 
 // ---- algorithm drivers (device-resident input, results on device) ----
 AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace);
+AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace);
 AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uint64_t letters,
                             int policy, bool fused_cas, const Deadline& dl,
                             const dfm_trace* trace);

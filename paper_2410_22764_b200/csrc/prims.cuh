@@ -74,7 +74,14 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-// in(i) -> u32 value; out(i, exclusive_prefix, value).  Sums must fit in 32 bits.
+// in(i) -> u32 value, or a payload struct with a u32 member `v` that is carried
+// from in() to out(); out(i, exclusive_prefix, item).  Sums must fit in 32 bits.
+__device__ __forceinline__ uint32_t scan_value(uint32_t x) { return x; }
+template <class T>
+__device__ __forceinline__ uint32_t scan_value(const T& x) {
+  return x.v;
+}
+
 template <class In, class Out>
 __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(In in, Out out, uint64_t count,
                                                                      uint64_t* status,
@@ -87,13 +94,14 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(In in, Out 
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t base = tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-  uint32_t v[kScanItems];
+  using Item = decltype(in(uint64_t{0}));
+  Item v[kScanItems];
   uint32_t sum = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     const uint64_t idx = base + i;
-    v[i] = idx < count ? in(idx) : 0u;
-    sum += v[i];
+    v[i] = idx < count ? in(idx) : Item{};
+    sum += scan_value(v[i]);
   }
   uint32_t agg;
   const uint32_t excl = block_exclusive_sum<kScanThreads>(sum, s_warp, &agg);
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(In in, Out 
   for (int i = 0; i < kScanItems; ++i) {
     const uint64_t idx = base + i;
     if (idx < count) out(idx, run, v[i]);
-    run += v[i];
+    run += scan_value(v[i]);
   }
   if (total_out != nullptr && threadIdx.x == 0 && (tile + 1) * kScanTile >= count)
     *total_out = s_prefix + agg;

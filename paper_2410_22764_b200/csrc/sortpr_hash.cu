@@ -1,0 +1,505 @@
+// sortPR, hash-grouping engine (the default).
+//
+// Same partition sequence, pass count and fixpoint as the reference
+// (min_sort.hpp:72-126) and as the radix engine (sort_pr.cu): only the way
+// states with equal keys are grouped differs.  Per pass, over the ACTIVE
+// states (block size >= 2), kept in ascending-q order so every delta row and
+// own-id read is coalesced:
+//
+//   K1 insert  : key = (block[q], id[delta_a(q)] ...) — packed exactly when it
+//                fits 63 bits, else a 64-bit hash with the full signature row
+//                kept for verification; one atomic slot update per state in an
+//                open-addressing table (direct-indexed when the key space is
+//                small; CTA shared-memory aggregation when it is tiny).  The
+//                slot collects the group size, its minimum member and whether
+//                it holds the old block's leader (minimum state).
+//   K2 resolve : look-back scan over the active states: the minimum member of
+//                every group decides the group's id — the old block id if the
+//                group holds the old leader, else a fresh id B + rank; equal-
+//                hash members are verified against the minimum member's row.
+//   K3 apply   : writes the new ids in place (skipped if a hash collision was
+//                found: the pass is then redone under a new seed — exact).
+//
+// Random accesses per active state: the k successor-id gathers (the floor of
+// the algorithm) + one slot RMW + one slot read (+ one row for verified
+// members).  Ids are gathered from u8/u16 mirrors while B <= 256 / 65536, so
+// early passes gather from L2.
+#include <algorithm>
+#include <vector>
+
+#include "prims.cuh"
+
+namespace dfm {
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr int kSmallTable = 4096;  // direct tables up to this size aggregate in smem
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct Slot {
+  unsigned long long key;  // 0 = empty; after resolve: the group's new id
+  uint32_t rep;            // ~(minimum active position) — atomicMax
+  uint32_t info;           // member count | (holds old leader) << 31
+};
+static_assert(sizeof(Slot) == 16, "slot is 16 bytes");
+
+struct InsertParams {
+  const uint32_t* __restrict__ delta;
+  uint64_t n;
+  uint32_t k;
+  const uint32_t* __restrict__ block;
+  const void* __restrict__ ids;  // gather source: mirror (u8/u16) or block
+  const uint32_t* __restrict__ act;
+  const uint8_t* __restrict__ lead;
+  uint64_t m;
+  int w;
+  uint64_t seed;
+  uint64_t mask;  // capacity - 1 (hash) or unused (direct)
+  Slot* slots;
+  uint32_t* __restrict__ slot_of;
+  uint32_t* __restrict__ sig;
+  uint32_t row;  // signature row stride (words)
+};
+
+template <int kIdBytes>
+__device__ __forceinline__ uint32_t load_id(const void* ids, uint32_t t) {
+  if (kIdBytes == 1) return static_cast<const uint8_t*>(ids)[t];
+  if (kIdBytes == 2) return static_cast<const uint16_t*>(ids)[t];
+  return static_cast<const uint32_t*>(ids)[t];
+}
+
+template <int kIdBytes, bool kHashed>
+__device__ __forceinline__ unsigned long long make_key(const InsertParams& p, uint64_t i, uint32_t q,
+                                                       uint32_t b) {
+  if (!kHashed) {
+    unsigned long long key = b;
+    for (uint32_t a = 0; a < p.k; ++a)
+      key = (key << p.w) | load_id<kIdBytes>(p.ids, p.delta[(uint64_t)a * p.n + q]);
+    return key;
+  }
+  uint32_t* row = p.sig + i * (uint64_t)p.row;
+  row[0] = b;
+  unsigned long long h = mix64(p.seed * kGolden + b);
+  for (uint32_t a = 0; a < p.k; ++a) {
+    const uint32_t s = load_id<kIdBytes>(p.ids, p.delta[(uint64_t)a * p.n + q]);
+    row[a + 1] = s;
+    h = mix64(h + kGolden + s);
+  }
+  return h;
+}
+
+// K1, hash or large direct table; warp-level aggregation of equal slots
+template <int kIdBytes, bool kHashed, bool kDirect>
+__global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t base = start - (threadIdx.x & 31); base < p.m; base += stride) {
+    const uint64_t i = base + (threadIdx.x & 31);
+    const bool valid = i < p.m;
+    uint64_t s = 0;
+    uint32_t lead = 0;
+    if (valid) {
+      const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+      const uint32_t b = p.block[q];
+      lead = p.lead[q];
+      const unsigned long long key = make_key<kIdBytes, kHashed>(p, i, q, b);
+      if (kDirect) {
+        s = key;
+      } else {
+        // stored key: never 0 (0 marks an empty slot)
+        const unsigned long long stored = kHashed ? (key | 1ull) : key + 1ull;
+        s = (kHashed ? key : mix64(key ^ p.seed)) & p.mask;
+        while (true) {
+          const unsigned long long cur = atomicCAS(&p.slots[s].key, 0ull, stored);
+          if (cur == 0ull || cur == stored) break;
+          s = (s + 1) & p.mask;
+        }
+      }
+      p.slot_of[i] = (uint32_t)s;
+    }
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
+    // lanes with the same slot: the lowest lane (smallest i) updates for all
+    const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s);
+    const uint32_t leads = __ballot_sync(vmask, lead != 0) & peers;
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+      atomicMax(&p.slots[s].rep, ~(uint32_t)i);
+      atomicAdd(&p.slots[s].info, (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u));
+    }
+  }
+}
+
+// K1 for tiny direct tables (pass 1: 2^(k+1) keys): CTA aggregation in smem
+template <int kIdBytes>
+__global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint32_t table) {
+  __shared__ uint32_t s_rep[kSmallTable];
+  __shared__ uint32_t s_info[kSmallTable];
+  for (uint32_t t = threadIdx.x; t < table; t += blockDim.x) {
+    s_rep[t] = 0;
+    s_info[t] = 0;
+  }
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+    const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+    const uint32_t b = p.block[q];
+    const uint32_t s = (uint32_t)make_key<kIdBytes, false>(p, i, q, b);
+    p.slot_of[i] = s;
+    atomicMax(&s_rep[s], ~(uint32_t)i);
+    atomicAdd(&s_info[s], 1u | (p.lead[q] ? 0x80000000u : 0u));
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < table; t += blockDim.x) {
+    if (s_info[t] != 0) {
+      atomicMax(&p.slots[t].rep, s_rep[t]);
+      atomicAdd(&p.slots[t].info, s_info[t]);
+    }
+  }
+}
+
+struct ResolveItem {
+  uint32_t v;      // 1 = minimum member of a group that gets a fresh id
+  uint32_t slot;
+  uint32_t flags;  // bit0 rep, bit1 singleton, bit2 keeper
+};
+
+struct ResolveIn {
+  const Slot* slots;
+  const uint32_t* slot_of;
+  const uint32_t* sig;  // nullptr: exact packed keys
+  uint32_t words, row;
+  unsigned long long* collision;
+  __device__ ResolveItem operator()(uint64_t i) const {
+    const uint32_t s = slot_of[i];
+    const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
+    const uint32_t rep_i = ~sl.x;
+    const uint32_t cnt = sl.y & 0x7FFFFFFFu;
+    const bool keeper = (sl.y >> 31) != 0;
+    const bool is_rep = rep_i == (uint32_t)i;
+    if (!is_rep && sig != nullptr) {  // equal hash: verify the full signature
+      const uint32_t* a = sig + i * (uint64_t)row;
+      const uint32_t* b = sig + (uint64_t)rep_i * row;
+      for (uint32_t x = 0; x < words; ++x)
+        if (a[x] != b[x]) {
+          atomicOr(collision, 1ull);
+          break;
+        }
+    }
+    ResolveItem it;
+    it.v = (is_rep && !keeper) ? 1u : 0u;
+    it.slot = s;
+    it.flags = (is_rep ? 1u : 0u) | (cnt == 1 ? 2u : 0u) | (keeper ? 4u : 0u);
+    return it;
+  }
+};
+
+// st[i]: bit0 take the id from the slot, bit1 stays active, bit2 new leader
+struct ResolveOut {
+  Slot* slots;
+  const uint32_t* act;
+  const uint32_t* block;
+  uint32_t* res;
+  uint8_t* st;
+  uint32_t B;
+  __device__ void operator()(uint64_t i, uint32_t excl, const ResolveItem& it) const {
+    if (it.flags & 1u) {
+      const uint32_t q = act ? act[i] : (uint32_t)i;
+      const uint32_t gid = (it.flags & 4u) ? block[q] : B + excl;
+      res[i] = gid;
+      if (it.flags & 2u) {
+        st[i] = (it.flags & 4u) ? 0u : 4u;
+      } else {
+        slots[it.slot].key = gid;  // publish for the other members
+        st[i] = 2u | ((it.flags & 4u) ? 0u : 4u);
+      }
+    } else {
+      st[i] = 3u;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* __restrict__ act,
+                                                    const uint32_t* __restrict__ res,
+                                                    const uint8_t* __restrict__ st,
+                                                    const uint32_t* __restrict__ slot_of,
+                                                    const Slot* __restrict__ slots,
+                                                    uint32_t* __restrict__ block,
+                                                    uint8_t* __restrict__ flag,
+                                                    uint8_t* __restrict__ lead,
+                                                    const uint64_t* scalars) {
+  if (scalars[2] != 0) return;  // collision: the pass is void
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint32_t s = st[i];
+    const uint32_t q = act ? act[i] : (uint32_t)i;
+    const uint32_t gid = (s & 1u) ? (uint32_t)slots[slot_of[i]].key : res[i];
+    block[q] = gid;
+    flag[q] = (s >> 1) & 1u;
+    if (s & 4u) lead[q] = 1;
+  }
+}
+
+struct ActIn {
+  const uint32_t* act;
+  const uint8_t* flag;
+  __device__ uint32_t operator()(uint64_t i) const { return flag[act ? act[i] : (uint32_t)i]; }
+};
+struct ActOut {
+  const uint32_t* act;
+  uint32_t* act_next;
+  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
+    if (v) act_next[excl] = act ? act[i] : (uint32_t)i;
+  }
+};
+
+__global__ void init_kernel(const uint8_t* __restrict__ acc, uint64_t n, bool split,
+                            const uint32_t* __restrict__ first2, uint32_t* __restrict__ block,
+                            uint8_t* __restrict__ lead, uint8_t* __restrict__ m8) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    const uint32_t b = (split && acc[q] == 0) ? 1u : 0u;
+    block[q] = b;
+    m8[q] = (uint8_t)b;
+    // block leaders = minimum state of each initial block (min_partref.hpp:53-63 analogue)
+    lead[q] = ((uint32_t)q == first2[0] || (uint32_t)q == first2[1] ||
+               (!split && (uint32_t)q == 0))
+                  ? 1
+                  : 0;
+  }
+}
+
+__global__ void first_states_kernel(const uint8_t* __restrict__ acc, uint64_t n, uint32_t* out2) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t fa = kNoLeader, fr = kNoLeader;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    if (acc[q]) fa = min(fa, (uint32_t)q);
+    else fr = min(fr, (uint32_t)q);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
+    fr = min(fr, __shfl_xor_sync(0xffffffffu, fr, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (fa != kNoLeader) atomicMin(&out2[0], fa);
+    if (fr != kNoLeader) atomicMin(&out2[1], fr);
+  }
+}
+
+template <class T>
+__global__ void mirror_kernel(const uint32_t* __restrict__ block, uint64_t n, T* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    out[q] = (T)block[q];
+}
+
+// canonical labels from maintained leaders (leader = minimum state of its block):
+// label(block) = rank of its leader among all leaders (core.hpp:123-136)
+struct LeadIn {
+  const uint8_t* lead;
+  __device__ uint32_t operator()(uint64_t q) const { return lead[q]; }
+};
+struct LeadOut {
+  const uint32_t* block;
+  uint32_t* canon_of_block;
+  __device__ void operator()(uint64_t q, uint32_t excl, uint32_t v) const {
+    if (v) canon_of_block[block[q]] = excl;
+  }
+};
+__global__ void canon_gather_kernel(const uint32_t* __restrict__ block, uint64_t n,
+                                    const uint32_t* __restrict__ canon_of_block,
+                                    uint32_t* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    out[q] = canon_of_block[block[q]];
+}
+__global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    out[q] = (uint32_t)q;
+}
+
+unsigned grid_for(const Ctx& ctx, uint64_t items, int per_sm = 16) {
+  return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
+                                      (uint64_t)ctx.num_sms * per_sm);
+}
+
+int bit_width_u32(uint32_t x) { return x == 0 ? 0 : 32 - __builtin_clz(x); }
+
+template <int kIdBytes>
+void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
+  const unsigned grid = grid_for(ctx, p.m);
+  if (direct && table <= kSmallTable)
+    insert_small_kernel<kIdBytes><<<std::min<unsigned>(grid, ctx.num_sms * 4), 256, 0, ctx.stream>>>(
+        p, (uint32_t)table);
+  else if (direct)
+    insert_kernel<kIdBytes, false, true><<<grid, 256, 0, ctx.stream>>>(p);
+  else if (hashed)
+    insert_kernel<kIdBytes, true, false><<<grid, 256, 0, ctx.stream>>>(p);
+  else
+    insert_kernel<kIdBytes, false, false><<<grid, 256, 0, ctx.stream>>>(p);
+  DFM_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {
+  AlgoOut out;
+  const uint64_t n = d.n;
+  const uint32_t k = d.k;
+  out.peak_memory_estimate = n * (16 + 4ull * k);  // min_sort.hpp:121
+  uint32_t* block = ctx.slot_t<uint32_t>("sh.block", n);
+  uint8_t* flag = ctx.slot_t<uint8_t>("sh.flag", n);
+  uint8_t* lead = ctx.slot_t<uint8_t>("sh.lead", n);
+  uint8_t* m8 = ctx.slot_t<uint8_t>("sh.m8", n);
+  uint16_t* m16 = nullptr;
+  uint32_t* act_buf[2] = {ctx.slot_t<uint32_t>("sh.act0", n), ctx.slot_t<uint32_t>("sh.act1", n)};
+  uint32_t* slot_of = ctx.slot_t<uint32_t>("sh.slotof", n);
+  uint32_t* res = ctx.slot_t<uint32_t>("sh.res", n);
+  uint8_t* st = ctx.slot_t<uint8_t>("sh.st", n);
+  uint32_t* sig = nullptr;
+  const uint32_t row = (k + 1 + 7) & ~7u;  // signature rows padded to 32-byte sectors
+  uint64_t* sc = ctx.d_scalars;  // [1] fresh [2] collision [3] next active [4] accepting
+  uint32_t* first2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
+  DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
+  DFM_CUDA(cudaMemsetAsync(first2, 0xFF, 8, ctx.stream));
+  {
+    ProfScope p(ctx, "init", n * 2);
+    first_states_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2);
+    DFM_LAUNCH_CHECK();
+  }
+  DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 16, first2, 8, cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  const uint32_t fa = (uint32_t)(ctx.h_scalars[16] & 0xFFFFFFFFu);
+  const uint32_t fr = (uint32_t)(ctx.h_scalars[16] >> 32);
+  const bool split = fa != kNoLeader && fr != kNoLeader;  // min_sort.hpp:80-88
+  uint32_t B = split ? 2u : 1u;
+  {
+    ProfScope p(ctx, "init", n * 10);
+    init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, first2, block, lead, m8);
+    DFM_LAUNCH_CHECK();
+  }
+  const uint32_t* act = nullptr;  // identity at pass 1
+  int act_sel = 0;
+  uint64_t m = n;
+  uint64_t seed = 0x5EED0001ull;
+  std::vector<uint32_t> trace_buf;
+  int mirror_bytes = 1;  // id width of the current gather mirror (4 = block itself)
+
+  while (true) {
+    if (dl.expired()) {
+      out.status = DFM_STATUS_TIMEOUT;
+      return out;
+    }
+    const int w = std::max(1, bit_width_u32(B - 1));
+    const uint64_t kbits = (uint64_t)(k + 1) * (uint64_t)w;
+    const bool packed = kbits <= 63;
+    const bool direct = packed && kbits <= 24 && (1ull << kbits) <= std::max<uint64_t>(2 * m, 4096);
+    uint64_t table = 0;
+    if (direct) {
+      table = 1ull << kbits;
+    } else {
+      table = 1024;
+      while (table < m + m / 2) table <<= 1;
+    }
+    DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
+    uint32_t* act_next = act_buf[act_sel ^ 1];
+    if (m > 0) {
+      Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", table * sizeof(Slot)));
+      DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
+      if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
+      const void* ids = mirror_bytes == 1 ? (const void*)m8
+                        : mirror_bytes == 2 ? (const void*)m16 : (const void*)block;
+      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table - 1, slots,
+                      slot_of, packed ? nullptr : sig, row};
+      {
+        // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
+        // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
+        ProfScope p(ctx, "sig",
+                    m * (4ull * k + (uint64_t)mirror_bytes * k + 4 + 1 + (act ? 4 : 0) + 16 + 4 +
+                         (packed ? 0 : 4ull * row)));
+        if (mirror_bytes == 1) launch_insert<1>(ctx, ip, !packed, direct, table);
+        else if (mirror_bytes == 2) launch_insert<2>(ctx, ip, !packed, direct, table);
+        else launch_insert<4>(ctx, ip, !packed, direct, table);
+      }
+      {
+        ProfScope p(ctx, "scan", m * (4ull + 16 + 4 + 4 + 1));  // slot_of, slot, own id, res, st
+        prims::lookback_scan(
+            ctx, "sc.resolve", m,
+            ResolveIn{slots, slot_of, packed ? nullptr : sig, k + 1, row,
+                      reinterpret_cast<unsigned long long*>(sc + 2)},
+            ResolveOut{slots, act, block, res, st, B}, sc + 1);
+      }
+      {
+        ProfScope p(ctx, "relabel", m * (1ull + 4 + 4 + 4 + 1 + 1));
+        apply_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, act, res, st, slot_of, slots,
+                                                               block, flag, lead, sc);
+        DFM_LAUNCH_CHECK();
+      }
+      {
+        ProfScope p(ctx, "scan", m * 9ull);
+        prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+      }
+    }
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 24, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (ctx.h_scalars[2] != 0) {  // hash collision: redo the pass under a new seed
+      seed = seed * kGolden + 0x632BE59BD9B4E019ull;
+      continue;
+    }
+    const uint64_t fresh = ctx.h_scalars[1];
+    ++out.iterations;
+    const uint32_t B_next = B + (uint32_t)fresh;
+    if (trace && trace->on_pass) {
+      trace_buf.resize(n);
+      DFM_CUDA(cudaMemcpyAsync(trace_buf.data(), block, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      trace->on_pass(trace->user, out.iterations, trace_buf.data(), (uint32_t)n, B_next);
+    }
+    if (fresh == 0) break;  // fixpoint, min_sort.hpp:111-117
+    B = B_next;
+    m = ctx.h_scalars[3];
+    act = act_next;
+    act_sel ^= 1;
+    // id mirror for the next pass's gathers
+    if (B <= 256) {
+      ProfScope p(ctx, "mirror", n * 5);
+      mirror_kernel<uint8_t><<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, m8);
+      DFM_LAUNCH_CHECK();
+      mirror_bytes = 1;
+    } else if (B <= 65536) {
+      if (m16 == nullptr) m16 = ctx.slot_t<uint16_t>("sh.m16", n);
+      ProfScope p(ctx, "mirror", n * 6);
+      mirror_kernel<uint16_t><<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, m16);
+      DFM_LAUNCH_CHECK();
+      mirror_bytes = 2;
+    } else {
+      mirror_bytes = 4;
+    }
+  }
+  out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+  if (B == n) {  // every block a singleton: first-occurrence labels are the identity
+    ProfScope p(ctx, "canon", n * 4);
+    iota_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(out.canon_dev, n);
+    DFM_LAUNCH_CHECK();
+    out.num_blocks = B;
+  } else {
+    uint32_t* cob = ctx.slot_t<uint32_t>("sh.cob", n);
+    ProfScope p(ctx, "canon", n * 13ull);
+    prims::lookback_scan(ctx, "sc.canon", n, LeadIn{lead}, LeadOut{block, cob}, sc + 5);
+    canon_gather_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, cob, out.canon_dev);
+    DFM_LAUNCH_CHECK();
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 5, sc + 5, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    out.num_blocks = (uint32_t)ctx.h_scalars[5];
+  }
+  out.status = DFM_STATUS_OK;
+  return out;
+}
+
+}  // namespace dfm

@@ -29,3 +29,11 @@ def golden():
 def eng():
     import paper_2410_22764_b200 as dfm
     return dfm.Engine(0)
+
+
+@pytest.fixture(scope="session")
+def eng_radix():
+    import paper_2410_22764_b200 as dfm
+    e = dfm.Engine(0)
+    e.set_sortpr_engine("radix")
+    return e

