@@ -17,7 +17,7 @@ build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(PKG)/libdfm.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcuda
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
 oracle:
 	$(MAKE) -s -C oracle

@@ -114,6 +114,12 @@ int dfm_ctx_set_stream(dfm_ctx* ctx, void* stream);
 #define DFM_SORTPR_HASH 0
 #define DFM_SORTPR_RADIX 1
 int dfm_ctx_set_sortpr_engine(dfm_ctx* ctx, int engine);
+/* Cho–Huynh squaring engine: AUTO (tensor cores for |V| >= 1024), BIT (packed 64-bit
+ * rows on CUDA cores) or TENSOR (tcgen05 kind::i8 GEMM).  Same results. */
+#define DFM_TRANS_AUTO 0
+#define DFM_TRANS_BIT 1
+#define DFM_TRANS_TENSOR 2
+int dfm_ctx_set_trans_engine(dfm_ctx* ctx, int engine);
 /* Record per-kernel CUDA-event timings for subsequent calls (bench/roofline). */
 int dfm_ctx_set_profiling(dfm_ctx* ctx, int enabled);
 /* Read back timing for a kernel family ("sig", "sort", "scan", "relabel", "elect",

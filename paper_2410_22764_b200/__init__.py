@@ -245,6 +245,7 @@ def _load():
         "dfm_ctx_set_stream": (C.c_int, [vp, vp]),
         "dfm_ctx_set_profiling": (C.c_int, [vp, C.c_int]),
         "dfm_ctx_set_sortpr_engine": (C.c_int, [vp, C.c_int]),
+        "dfm_ctx_set_trans_engine": (C.c_int, [vp, C.c_int]),
         "dfm_profile_get": (C.c_int, [vp, C.c_char_p, C.POINTER(u64), C.POINTER(C.c_double),
                                       C.POINTER(u64)]),
         "dfm_kernel_launches": (u64, []),
@@ -544,6 +545,11 @@ class Engine:
         """'hash' (default) or 'radix' (the paper's sort); same results."""
         self._check(self.lib.dfm_ctx_set_sortpr_engine(
             self.handle, {"hash": 0, "radix": 1}[engine]))
+
+    def set_trans_engine(self, engine: str) -> None:
+        """Cho–Huynh squaring: 'auto' (default), 'bit' (CUDA cores) or 'tensor' (tcgen05)."""
+        self._check(self.lib.dfm_ctx_set_trans_engine(
+            self.handle, {"auto": 0, "bit": 1, "tensor": 2}[engine]))
 
     def set_profiling(self, on: bool) -> None:
         self._check(self.lib.dfm_ctx_set_profiling(self.handle, int(bool(on))))

@@ -216,6 +216,14 @@ int dfm_ctx_set_sortpr_engine(dfm_ctx* c, int engine) {
   });
 }
 
+int dfm_ctx_set_trans_engine(dfm_ctx* c, int engine) {
+  return guarded(c, [&](Ctx& ctx) {
+    if (engine < DFM_TRANS_AUTO || engine > DFM_TRANS_TENSOR)
+      throw Error(DFM_ERR_INVALID, "unknown Cho-Huynh engine");
+    ctx.trans_engine = engine;
+  });
+}
+
 int dfm_ctx_set_profiling(dfm_ctx* c, int enabled) {
   return guarded(c, [&](Ctx& ctx) { ctx.profiling = enabled != 0; });
 }

@@ -83,6 +83,8 @@ struct Ctx {
   size_t pinned_bytes = 0;
   // sortPR grouping engine: DFM_SORTPR_HASH (default) or DFM_SORTPR_RADIX
   int sortpr_engine = 0;
+  // Cho–Huynh squaring engine: DFM_TRANS_AUTO (default) / DFM_TRANS_BIT / DFM_TRANS_TENSOR
+  int trans_engine = 0;
   // profiling
   bool profiling = false;
   struct Pending {

@@ -166,7 +166,7 @@ AlgoOut run_trans_minimize(Ctx& ctx, const DevDfa& d, const dfm_limits& lim, con
   auto* apart = ctx.slot_t<unsigned long long>("tr.apart", W);
   auto* apart_next = ctx.slot_t<unsigned long long>("tr.apart2", W);
   auto* stats = reinterpret_cast<unsigned long long*>(ctx.d_scalars + 24);
-  const bool use_tc = trans_tc::usable(V);
+  const bool use_tc = trans_tc::usable(V, ctx.trans_engine);
   TransTcState tc;
   unsigned long long* reach = nullptr;
   unsigned long long* next = nullptr;

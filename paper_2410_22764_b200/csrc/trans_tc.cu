@@ -1,18 +1,335 @@
-// tcgen05 int8 GEMM squaring for the Cho–Huynh closure.  (engine selection
-// lives in usable())
+// tcgen05 int8 squaring engine for the Cho–Huynh closure (reference
+// min_trans.hpp:131-186; paper Alg. 1), sm_100a.
+//
+// The pair-graph reachability matrix R (|V| x |V|, |V| = n^2, padded to Vp) is
+// held as 0/1 bytes.  One pass computes, tile by tile,
+//     acc  = R · R                      (tcgen05.mma kind::i8, u8 x u8 -> s32 in TMEM)
+//     next = (acc > 0) | R              (epilogue, written as bytes)
+//     apart_next[i] |= OR_j next[i][j] & apart[j]     (fused propagation)
+// which is exactly the reference's squaring (next = reach ∨ reach², pass-entry
+// reach) followed by its propagation (pass-entry apart).
+//
+// Kernel anatomy (one CTA per 128x256 output tile, 256 threads):
+//   warp 0      TMA producer: A = R[m0:m0+128, k:k+128] (K-major, 128B swizzle),
+//               B = R[k:k+128, n0:n0+256] (MN-major, two 128-byte swizzle atoms)
+//   warp 1      MMA issuer (one elected lane): 4 x (128x256x32) per stage
+//   warp 2      TMEM allocator (256 columns of 32-bit accumulators)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 per 32 columns, threshold, OR,
+//               store, propagate
+// 4-stage smem ring (48 KB/stage) with full/empty mbarriers; tcgen05.commit
+// frees a stage and finally signals the accumulator.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "prims.cuh"
 #include "trans_tc.cuh"
 
 namespace dfm {
 namespace trans_tc {
+namespace {
 
-bool usable(uint64_t) { return false; }
+constexpr int kBM = 128, kBN = 256, kBK = 128, kStages = 4;
+constexpr int kStageA = kBM * kBK;                 // 16 KB
+constexpr int kStageB = kBK * kBN;                 // 32 KB
+constexpr int kStageBytes = kStageA + kStageB;     // 48 KB
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kThreads = 256;
+constexpr int kGroupM = 16;  // rasterisation: 16 M-tiles share the concurrent wave
 
-TransTcState init(Ctx&, const DevDfa&, uint64_t) {
-  throw Error(DFM_ERR_INVALID, "tcgen05 closure engine not built");
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-void square_and_propagate(Ctx&, TransTcState&, const unsigned long long*, unsigned long long*) {
-  throw Error(DFM_ERR_INVALID, "tcgen05 closure engine not built");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (sm100 "version 1"), 128B swizzle
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::i8, u8 x u8 -> s32, A K-major, B MN-major, M=128, N=256
+constexpr uint32_t kIdesc = (2u << 4)            // D format S32
+                            | (0u << 7)          // A u8
+                            | (0u << 10)         // B u8
+                            | (0u << 15)         // A K-major
+                            | (1u << 16)         // B MN-major
+                            | ((kBN >> 3) << 17) // N
+                            | ((kBM >> 4) << 24);// M
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+      smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    square_kernel(const __grid_constant__ CUtensorMap map, const int8_t* __restrict__ reach,
+                  int8_t* __restrict__ next, const unsigned long long* __restrict__ apart,
+                  unsigned long long* apart_next, uint32_t Vp, uint32_t W) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // rasterised tile order: groups of kGroupM M-tiles sweep all N-tiles together
+  const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN;
+  const uint32_t tid = blockIdx.x;
+  const uint32_t group = tid / (kGroupM * tiles_n);
+  const uint32_t first_m = group * kGroupM;
+  const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
+  const uint32_t in_group = tid - group * kGroupM * tiles_n;
+  const uint32_t m0 = (first_m + in_group % gm) * kBM;
+  const uint32_t n0 = (in_group / gm) * kBN;
+  const uint32_t kblocks = Vp / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t round = kb / kStages;
+        if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], (round - 1) & 1);
+        uint8_t* a = smem + s * kStageBytes;
+        uint8_t* b = a + kStageA;
+        mbar_expect_tx(&full[s], kStageBytes);
+        tma_load_2d(a, &map, &full[s], (int)(kb * kBK), (int)m0);         // A: {k, m}
+        tma_load_2d(b, &map, &full[s], (int)n0, (int)(kb * kBK));         // B: {n, k} lo
+        tma_load_2d(b + kStageB / 2, &map, &full[s], (int)(n0 + 128), (int)(kb * kBK));  // hi
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&full[s], (kb / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a = smem_u32(smem + s * kStageBytes);
+        const uint32_t b = a + kStageA;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 32; ++kk) {
+          // A K-major: +32 bytes along K; B MN-major: +32 rows of 128 bytes
+          const uint64_t da = smem_desc(a + kk * 32, 16, 1024);
+          const uint64_t db = smem_desc(b + kk * 32 * 128, kStageB / 2, 1024);
+          umma_i8(tmem, da, db, (kb | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);  // frees the stage once these MMAs retire
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {  // epilogue: one accumulator row per thread
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t quarter = warp - 4;  // TMEM lanes [32*quarter, 32*quarter+32)
+    const uint32_t row = m0 + quarter * 32 + lane;
+    const int8_t* rrow = reach + (uint64_t)row * Vp;
+    int8_t* nrow = next + (uint64_t)row * Vp;
+    bool hit = false;
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld32(tmem + ((quarter * 32) << 16) + c * 32, v);
+      const uint32_t j0 = n0 + c * 32;
+      const uint4* rp = reinterpret_cast<const uint4*>(rrow + j0);
+      const uint4 r0 = rp[0], r1 = rp[1];
+      const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      uint32_t mask = 0;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t rb = (rw[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
+        mask |= ((v[b] != 0u) | (rb != 0u) ? 1u : 0u) << b;
+      }
+      uint32_t ow[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t nib = (mask >> (w * 4)) & 0xFu;
+        ow[w] = (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 |
+                ((nib >> 3) & 1u) << 24;
+      }
+      uint4* op = reinterpret_cast<uint4*>(nrow + j0);
+      op[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      op[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+      const uint32_t abits = (j0 >> 6) < W ? (uint32_t)(apart[j0 >> 6] >> (j0 & 63)) : 0u;
+      hit |= (mask & abits) != 0u;
+    }
+    if (hit) atomicOr(&apart_next[row >> 6], 1ull << (row & 63));
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+// 0/1 byte matrix init: row s = (q,r) gets 1 at (delta_a(q), delta_a(r)) for every a
+__global__ void init_bytes_kernel(const uint32_t* __restrict__ delta, uint64_t n, uint32_t k,
+                                  uint64_t V, uint64_t Vp, int8_t* __restrict__ R) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < V; s += stride) {
+    const uint64_t q = s / n, r = s % n;
+    for (uint32_t a = 0; a < k; ++a)
+      R[s * Vp + (uint64_t)delta[a * n + q] * n + delta[a * n + r]] = 1;
+  }
+}
+
+// apart_next starts as apart (the reference ORs the pass-entry flag in)
+__global__ void copy_words_kernel(const unsigned long long* a, unsigned long long* b, uint64_t W) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < W) b[i] = a[i];
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    DFM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (p == nullptr || q != cudaDriverEntryPointSuccess)
+      throw Error(DFM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_map(int8_t* base, uint64_t Vp) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {Vp, Vp};
+  const cuuint64_t strides[1] = {Vp};
+  const cuuint32_t box[2] = {128, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(DFM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+}  // namespace
+
+bool usable(uint64_t V, int engine) {
+  if (engine == DFM_TRANS_BIT) return false;
+  if (engine == DFM_TRANS_TENSOR) return true;
+  return V >= 1024;  // below one wave of tiles the bit engine is already latency-bound
+}
+
+TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V) {
+  static bool attr = false;
+  if (!attr) {
+    DFM_CUDA(cudaFuncSetAttribute(square_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBytes));
+    attr = true;
+  }
+  TransTcState st;
+  st.V = V;
+  st.Vp = std::max<uint64_t>(256, ceil_div(V, 256) * 256);
+  const uint64_t bytes = st.Vp * st.Vp;
+  st.reach = ctx.slot_t<int8_t>("tc.R0", bytes);
+  st.next = ctx.slot_t<int8_t>("tc.R1", bytes);
+  DFM_CUDA(cudaMemsetAsync(st.reach, 0, bytes, ctx.stream));
+  const unsigned grid =
+      (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(V, 1), 256), ctx.num_sms * 16ull);
+  init_bytes_kernel<<<grid, 256, 0, ctx.stream>>>(d.delta, d.n, d.k, V, st.Vp, st.reach);
+  DFM_LAUNCH_CHECK();
+  return st;
+}
+
+void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* apart,
+                          unsigned long long* apart_next) {
+  const uint64_t W = ceil_div(st.V, 64);
+  copy_words_kernel<<<(unsigned)ceil_div(W, 256), 256, 0, ctx.stream>>>(apart, apart_next, W);
+  DFM_LAUNCH_CHECK();
+  const CUtensorMap map = make_map(st.reach, st.Vp);
+  const uint64_t tiles = (st.Vp / kBM) * (st.Vp / kBN);
+  {
+    // 2*Vp^3 int8 multiply-adds (as ops) per pass; bytes: algorithmic tensor-bound figure
+    ProfScope p(ctx, "gemm", 2ull * st.Vp * st.Vp * st.Vp);
+    square_kernel<<<(unsigned)tiles, kThreads, kSmemBytes, ctx.stream>>>(
+        map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W);
+    DFM_LAUNCH_CHECK();
+  }
+  std::swap(st.reach, st.next);
 }
 
 }  // namespace trans_tc

@@ -10,14 +10,12 @@ namespace dfm {
 struct TransTcState {
   uint64_t V = 0;     // pair nodes
   uint64_t Vp = 0;    // padded to the GEMM tile
-  int8_t* reach = nullptr;   // Vp x Vp, row-major (A operand, K-major)
-  int8_t* reachT = nullptr;  // transpose (B operand, K-major)
+  int8_t* reach = nullptr;   // Vp x Vp 0/1 bytes, row-major (A K-major, B MN-major)
   int8_t* next = nullptr;
-  int8_t* nextT = nullptr;
 };
 
 namespace trans_tc {
-bool usable(uint64_t V);
+bool usable(uint64_t V, int engine);  // engine: DFM_TRANS_AUTO / _BIT / _TENSOR
 TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V);
 // one pass: next = reach | (reach*reach > 0); apart_next |= rows reaching apart;
 // then swaps reach<->next inside the state
