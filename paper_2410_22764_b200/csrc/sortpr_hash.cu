@@ -66,27 +66,87 @@ struct InsertParams {
   uint32_t row;  // signature row stride (words)
 };
 
-template <int kIdBytes>
-__device__ __forceinline__ uint32_t load_id(const void* ids, uint32_t t) {
-  if (kIdBytes == 1) return static_cast<const uint8_t*>(ids)[t];
-  if (kIdBytes == 2) return static_cast<const uint16_t*>(ids)[t];
-  return static_cast<const uint32_t*>(ids)[t];
+// L2 eviction policies: the delta stream is read once per pass (evict first) so
+// that the gathered id array — the u8/u16 mirror in early passes — stays resident
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(a), "l"(pol));
+  return v;
 }
 
-template <int kIdBytes, bool kHashed>
+template <int kIdBytes>
+__device__ __forceinline__ uint32_t load_id(const void* ids, uint32_t t, uint64_t pol) {
+  uint32_t v;
+  if (kIdBytes == 1)
+    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(static_cast<const uint8_t*>(ids) + t), "l"(pol));
+  else if (kIdBytes == 2)
+    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(static_cast<const uint16_t*>(ids) + t), "l"(pol));
+  else
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(static_cast<const uint32_t*>(ids) + t), "l"(pol));
+  return v;
+}
+
+// kK > 0: compile-time alphabet size, so all delta loads, then all id gathers,
+// are in flight together; kK == 0: runtime k
+template <int kIdBytes, bool kHashed, int kK>
 __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, uint64_t i, uint32_t q,
-                                                       uint32_t b) {
+                                                       uint32_t b, uint64_t pol_stream,
+                                                       uint64_t pol_ids) {
+  const uint32_t k = kK > 0 ? (uint32_t)kK : p.k;
+  if (kK > 0) {
+    uint32_t t[kK > 0 ? kK : 1], s[kK > 0 ? kK : 1];
+#pragma unroll
+    for (int a = 0; a < kK; ++a) t[a] = ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream);
+#pragma unroll
+    for (int a = 0; a < kK; ++a) s[a] = load_id<kIdBytes>(p.ids, t[a], pol_ids);
+    if (!kHashed) {
+      unsigned long long key = b;
+#pragma unroll
+      for (int a = 0; a < kK; ++a) key = (key << p.w) | s[a];
+      return key;
+    }
+    uint32_t* row = p.sig + i * (uint64_t)p.row;
+    row[0] = b;
+    unsigned long long h = mix64(p.seed * kGolden + b);
+#pragma unroll
+    for (int a = 0; a < kK; ++a) {
+      row[a + 1] = s[a];
+      h = mix64(h + kGolden + s[a]);
+    }
+    return h;
+  }
   if (!kHashed) {
     unsigned long long key = b;
-    for (uint32_t a = 0; a < p.k; ++a)
-      key = (key << p.w) | load_id<kIdBytes>(p.ids, p.delta[(uint64_t)a * p.n + q]);
+    for (uint32_t a = 0; a < k; ++a)
+      key = (key << p.w) |
+            load_id<kIdBytes>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream),
+                              pol_ids);
     return key;
   }
   uint32_t* row = p.sig + i * (uint64_t)p.row;
   row[0] = b;
   unsigned long long h = mix64(p.seed * kGolden + b);
-  for (uint32_t a = 0; a < p.k; ++a) {
-    const uint32_t s = load_id<kIdBytes>(p.ids, p.delta[(uint64_t)a * p.n + q]);
+  for (uint32_t a = 0; a < k; ++a) {
+    const uint32_t s =
+        load_id<kIdBytes>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream), pol_ids);
     row[a + 1] = s;
     h = mix64(h + kGolden + s);
   }
@@ -94,8 +154,10 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
 }
 
 // K1, hash or large direct table; warp-level aggregation of equal slots
-template <int kIdBytes, bool kHashed, bool kDirect>
+template <int kIdBytes, bool kHashed, bool kDirect, int kK>
 __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_ids = policy_evict_last();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t base = start - (threadIdx.x & 31); base < p.m; base += stride) {
@@ -107,7 +169,8 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
       const uint32_t b = p.block[q];
       lead = p.lead[q];
-      const unsigned long long key = make_key<kIdBytes, kHashed>(p, i, q, b);
+      const unsigned long long key =
+          make_key<kIdBytes, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
       if (kDirect) {
         s = key;
       } else {
@@ -135,7 +198,7 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
 }
 
 // K1 for tiny direct tables (pass 1: 2^(k+1) keys): CTA aggregation in smem
-template <int kIdBytes>
+template <int kIdBytes, int kK>
 __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint32_t table) {
   __shared__ uint32_t s_rep[kSmallTable];
   __shared__ uint32_t s_info[kSmallTable];
@@ -144,14 +207,26 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
     s_info[t] = 0;
   }
   __syncthreads();
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_ids = policy_evict_last();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t base = start - (threadIdx.x & 31); base < p.m; base += stride) {
+    const uint64_t i = base + (threadIdx.x & 31);
+    const bool valid = i < p.m;
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    if (!valid) continue;
     const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
     const uint32_t b = p.block[q];
-    const uint32_t s = (uint32_t)make_key<kIdBytes, false>(p, i, q, b);
+    const uint32_t s = (uint32_t)make_key<kIdBytes, false, kK>(p, i, q, b, pol_stream, pol_ids);
     p.slot_of[i] = s;
-    atomicMax(&s_rep[s], ~(uint32_t)i);
-    atomicAdd(&s_info[s], 1u | (p.lead[q] ? 0x80000000u : 0u));
+    // lanes are in ascending i: the lowest lane of each key group updates for all
+    const uint32_t peers = __match_any_sync(vmask, s);
+    const uint32_t leads = __ballot_sync(vmask, p.lead[q] != 0) & peers;
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+      atomicMax(&s_rep[s], ~(uint32_t)i);
+      atomicAdd(&s_info[s], (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u));
+    }
   }
   __syncthreads();
   for (uint32_t t = threadIdx.x; t < table; t += blockDim.x) {
@@ -331,19 +406,30 @@ unsigned grid_for(const Ctx& ctx, uint64_t items, int per_sm = 16) {
 
 int bit_width_u32(uint32_t x) { return x == 0 ? 0 : 32 - __builtin_clz(x); }
 
-template <int kIdBytes>
-void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
+template <int kIdBytes, int kK>
+void launch_insert_k(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
   const unsigned grid = grid_for(ctx, p.m);
   if (direct && table <= kSmallTable)
-    insert_small_kernel<kIdBytes><<<std::min<unsigned>(grid, ctx.num_sms * 4), 256, 0, ctx.stream>>>(
-        p, (uint32_t)table);
+    insert_small_kernel<kIdBytes, kK>
+        <<<std::min<unsigned>(grid, ctx.num_sms * 4), 256, 0, ctx.stream>>>(p, (uint32_t)table);
   else if (direct)
-    insert_kernel<kIdBytes, false, true><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBytes, false, true, kK><<<grid, 256, 0, ctx.stream>>>(p);
   else if (hashed)
-    insert_kernel<kIdBytes, true, false><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBytes, true, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
   else
-    insert_kernel<kIdBytes, false, false><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBytes, false, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
   DFM_LAUNCH_CHECK();
+}
+
+template <int kIdBytes>
+void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
+  switch (p.k) {  // compile-time alphabets for the common small k
+    case 1: return launch_insert_k<kIdBytes, 1>(ctx, p, hashed, direct, table);
+    case 2: return launch_insert_k<kIdBytes, 2>(ctx, p, hashed, direct, table);
+    case 3: return launch_insert_k<kIdBytes, 3>(ctx, p, hashed, direct, table);
+    case 4: return launch_insert_k<kIdBytes, 4>(ctx, p, hashed, direct, table);
+    default: return launch_insert_k<kIdBytes, 0>(ctx, p, hashed, direct, table);
+  }
 }
 
 }  // namespace
@@ -399,7 +485,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     const int w = std::max(1, bit_width_u32(B - 1));
     const uint64_t kbits = (uint64_t)(k + 1) * (uint64_t)w;
     const bool packed = kbits <= 63;
-    const bool direct = packed && kbits <= 24 && (1ull << kbits) <= std::max<uint64_t>(2 * m, 4096);
+    // direct-indexed table (slot = key, no probing) when the key space is small
+    const bool direct = packed && kbits <= 30 && (1ull << kbits) <= std::max<uint64_t>(2 * m, 4096);
     uint64_t table = 0;
     if (direct) {
       table = 1ull << kbits;
