@@ -22,8 +22,8 @@
 //
 // Random accesses per active state: the k successor-id gathers (the floor of
 // the algorithm) + one slot RMW + one slot read (+ one row for verified
-// members).  Ids are gathered from u8/u16 mirrors while B <= 256 / 65536, so
-// early passes gather from L2.
+// members).  Ids are gathered from packed 1/4/8/16-bit mirrors while
+// B <= 2/16/256/65536, so early passes gather from L2.
 #include <algorithm>
 #include <vector>
 
@@ -59,7 +59,7 @@ struct InsertParams {
   uint64_t m;
   int w;
   uint64_t seed;
-  uint64_t mask;  // capacity - 1 (hash) or unused (direct)
+  uint64_t cap;  // hash-table capacity (unused for direct tables)
   Slot* slots;
   uint32_t* __restrict__ slot_of;
   uint32_t* __restrict__ sig;
@@ -78,35 +78,49 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// (non-volatile asm: read-only data, so the compiler may batch these loads)
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* a, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-               : "=r"(v)
-               : "l"(a), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
   return v;
 }
 
-template <int kIdBytes>
+// id gather from the mirror of width kIdBits: 1 (bitmap, B <= 2), 4 (nibbles,
+// B <= 16), 8, 16, or 32 (the block array itself).  Narrow mirrors keep the
+// gathered array L2-resident (12.5 / 50 MB at n = 1e8).
+template <int kIdBits>
 __device__ __forceinline__ uint32_t load_id(const void* ids, uint32_t t, uint64_t pol) {
   uint32_t v;
-  if (kIdBytes == 1)
-    asm volatile("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;"
-                 : "=r"(v)
-                 : "l"(static_cast<const uint8_t*>(ids) + t), "l"(pol));
-  else if (kIdBytes == 2)
-    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;"
-                 : "=r"(v)
-                 : "l"(static_cast<const uint16_t*>(ids) + t), "l"(pol));
+  if (kIdBits == 1) {
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"(static_cast<const uint32_t*>(ids) + (t >> 5)), "l"(pol));
+    return (v >> (t & 31)) & 1u;
+  }
+  if (kIdBits == 4) {
+    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"(static_cast<const uint8_t*>(ids) + (t >> 1)), "l"(pol));
+    return (v >> ((t & 1) * 4)) & 0xFu;
+  }
+  if (kIdBits == 8)
+    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"(static_cast<const uint8_t*>(ids) + t), "l"(pol));
+  else if (kIdBits == 16)
+    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"(static_cast<const uint16_t*>(ids) + t), "l"(pol));
   else
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
-                 : "=r"(v)
-                 : "l"(static_cast<const uint32_t*>(ids) + t), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+        : "=r"(v)
+        : "l"(static_cast<const uint32_t*>(ids) + t), "l"(pol));
   return v;
 }
 
 // kK > 0: compile-time alphabet size, so all delta loads, then all id gathers,
 // are in flight together; kK == 0: runtime k
-template <int kIdBytes, bool kHashed, int kK>
+template <int kIdBits, bool kHashed, int kK>
 __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, uint64_t i, uint32_t q,
                                                        uint32_t b, uint64_t pol_stream,
                                                        uint64_t pol_ids) {
@@ -116,7 +130,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
 #pragma unroll
     for (int a = 0; a < kK; ++a) t[a] = ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream);
 #pragma unroll
-    for (int a = 0; a < kK; ++a) s[a] = load_id<kIdBytes>(p.ids, t[a], pol_ids);
+    for (int a = 0; a < kK; ++a) s[a] = load_id<kIdBits>(p.ids, t[a], pol_ids);
     if (!kHashed) {
       unsigned long long key = b;
 #pragma unroll
@@ -137,7 +151,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
     unsigned long long key = b;
     for (uint32_t a = 0; a < k; ++a)
       key = (key << p.w) |
-            load_id<kIdBytes>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream),
+            load_id<kIdBits>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream),
                               pol_ids);
     return key;
   }
@@ -146,7 +160,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
   unsigned long long h = mix64(p.seed * kGolden + b);
   for (uint32_t a = 0; a < k; ++a) {
     const uint32_t s =
-        load_id<kIdBytes>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream), pol_ids);
+        load_id<kIdBits>(p.ids, ld_stream(p.delta + (uint64_t)a * p.n + q, pol_stream), pol_ids);
     row[a + 1] = s;
     h = mix64(h + kGolden + s);
   }
@@ -154,51 +168,68 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
 }
 
 // K1, hash or large direct table; warp-level aggregation of equal slots
-template <int kIdBytes, bool kHashed, bool kDirect, int kK>
+template <int kIdBits, bool kHashed, bool kDirect, int kK>
 __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_ids = policy_evict_last();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint64_t base = start - (threadIdx.x & 31); base < p.m; base += stride) {
-    const uint64_t i = base + (threadIdx.x & 31);
-    const bool valid = i < p.m;
-    uint64_t s = 0;
-    uint32_t lead = 0;
-    if (valid) {
-      const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
-      const uint32_t b = p.block[q];
-      lead = p.lead[q];
-      const unsigned long long key =
-          make_key<kIdBytes, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
-      if (kDirect) {
-        s = key;
-      } else {
-        // stored key: never 0 (0 marks an empty slot)
-        const unsigned long long stored = kHashed ? (key | 1ull) : key + 1ull;
-        s = (kHashed ? key : mix64(key ^ p.seed)) & p.mask;
-        while (true) {
-          const unsigned long long cur = atomicCAS(&p.slots[s].key, 0ull, stored);
-          if (cur == 0ull || cur == stored) break;
-          s = (s + 1) & p.mask;
+  // each warp takes 64 consecutive active states per step (two per lane) so two
+  // independent gather chains are in flight per thread
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 2;
+  const uint64_t warp_first =
+      ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * 2;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t base = warp_first; base < p.m; base += stride) {
+    uint64_t s[2] = {0, 0};
+    uint32_t lead[2] = {0, 0};
+    unsigned long long key[2] = {0, 0};
+    bool valid[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t i = base + u * 32 + lane;
+      valid[u] = i < p.m;
+      if (valid[u]) {
+        const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+        const uint32_t b = p.block[q];
+        lead[u] = p.lead[q];
+        key[u] = make_key<kIdBits, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t i = base + u * 32 + lane;
+      if (valid[u]) {
+        if (kDirect) {
+          s[u] = key[u];
+        } else {
+          // stored key: never 0 (0 marks an empty slot); start slot = mulhi(hash, capacity)
+          const unsigned long long stored = kHashed ? (key[u] | 1ull) : key[u] + 1ull;
+          const unsigned long long h = kHashed ? key[u] : mix64(key[u] ^ p.seed);
+          uint64_t t = __umul64hi(h, p.cap);
+          while (true) {
+            const unsigned long long cur = atomicCAS(&p.slots[t].key, 0ull, stored);
+            if (cur == 0ull || cur == stored) break;
+            if (++t == p.cap) t = 0;
+          }
+          s[u] = t;
+        }
+        p.slot_of[i] = (uint32_t)s[u];
+      }
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u]);
+      if (valid[u]) {
+        // lanes with the same slot: the lowest lane (smallest i) updates for all
+        const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s[u]);
+        const uint32_t leads = __ballot_sync(vmask, lead[u] != 0) & peers;
+        if (lane == (uint32_t)(__ffs(peers) - 1)) {
+          atomicMax(&p.slots[s[u]].rep, ~(uint32_t)i);
+          atomicAdd(&p.slots[s[u]].info, (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u));
         }
       }
-      p.slot_of[i] = (uint32_t)s;
-    }
-    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    if (!valid) continue;
-    // lanes with the same slot: the lowest lane (smallest i) updates for all
-    const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s);
-    const uint32_t leads = __ballot_sync(vmask, lead != 0) & peers;
-    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
-      atomicMax(&p.slots[s].rep, ~(uint32_t)i);
-      atomicAdd(&p.slots[s].info, (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u));
     }
   }
 }
 
 // K1 for tiny direct tables (pass 1: 2^(k+1) keys): CTA aggregation in smem
-template <int kIdBytes, int kK>
+template <int kIdBits, int kK>
 __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint32_t table) {
   __shared__ uint32_t s_rep[kSmallTable];
   __shared__ uint32_t s_info[kSmallTable];
@@ -218,7 +249,7 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
     if (!valid) continue;
     const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
     const uint32_t b = p.block[q];
-    const uint32_t s = (uint32_t)make_key<kIdBytes, false, kK>(p, i, q, b, pol_stream, pol_ids);
+    const uint32_t s = (uint32_t)make_key<kIdBits, false, kK>(p, i, q, b, pol_stream, pol_ids);
     p.slot_of[i] = s;
     // lanes are in ascending i: the lowest lane of each key group updates for all
     const uint32_t peers = __match_any_sync(vmask, s);
@@ -334,12 +365,11 @@ struct ActOut {
 
 __global__ void init_kernel(const uint8_t* __restrict__ acc, uint64_t n, bool split,
                             const uint32_t* __restrict__ first2, uint32_t* __restrict__ block,
-                            uint8_t* __restrict__ lead, uint8_t* __restrict__ m8) {
+                            uint8_t* __restrict__ lead) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
     const uint32_t b = (split && acc[q] == 0) ? 1u : 0u;
     block[q] = b;
-    m8[q] = (uint8_t)b;
     // block leaders = minimum state of each initial block (min_partref.hpp:53-63 analogue)
     lead[q] = ((uint32_t)q == first2[0] || (uint32_t)q == first2[1] ||
                (!split && (uint32_t)q == 0))
@@ -366,11 +396,22 @@ __global__ void first_states_kernel(const uint8_t* __restrict__ acc, uint64_t n,
   }
 }
 
-template <class T>
-__global__ void mirror_kernel(const uint32_t* __restrict__ block, uint64_t n, T* __restrict__ out) {
+// packed id mirror: 32/kBits ids per 32-bit word (ids < 2^kBits by construction)
+template <int kBits>
+__global__ void mirror_kernel(const uint32_t* __restrict__ block, uint64_t n,
+                              uint32_t* __restrict__ out) {
+  constexpr int kPer = 32 / kBits;
+  const uint64_t words = (n + kPer - 1) / kPer;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
-    out[q] = (T)block[q];
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const uint64_t q = w * kPer + e;
+      if (q < n) word |= block[q] << (e * kBits);
+    }
+    out[w] = word;
+  }
 }
 
 // canonical labels from maintained leaders (leader = minimum state of its block):
@@ -406,29 +447,29 @@ unsigned grid_for(const Ctx& ctx, uint64_t items, int per_sm = 16) {
 
 int bit_width_u32(uint32_t x) { return x == 0 ? 0 : 32 - __builtin_clz(x); }
 
-template <int kIdBytes, int kK>
+template <int kIdBits, int kK>
 void launch_insert_k(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
   const unsigned grid = grid_for(ctx, p.m);
   if (direct && table <= kSmallTable)
-    insert_small_kernel<kIdBytes, kK>
+    insert_small_kernel<kIdBits, kK>
         <<<std::min<unsigned>(grid, ctx.num_sms * 4), 256, 0, ctx.stream>>>(p, (uint32_t)table);
   else if (direct)
-    insert_kernel<kIdBytes, false, true, kK><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBits, false, true, kK><<<grid, 256, 0, ctx.stream>>>(p);
   else if (hashed)
-    insert_kernel<kIdBytes, true, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBits, true, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
   else
-    insert_kernel<kIdBytes, false, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
+    insert_kernel<kIdBits, false, false, kK><<<grid, 256, 0, ctx.stream>>>(p);
   DFM_LAUNCH_CHECK();
 }
 
-template <int kIdBytes>
+template <int kIdBits>
 void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
   switch (p.k) {  // compile-time alphabets for the common small k
-    case 1: return launch_insert_k<kIdBytes, 1>(ctx, p, hashed, direct, table);
-    case 2: return launch_insert_k<kIdBytes, 2>(ctx, p, hashed, direct, table);
-    case 3: return launch_insert_k<kIdBytes, 3>(ctx, p, hashed, direct, table);
-    case 4: return launch_insert_k<kIdBytes, 4>(ctx, p, hashed, direct, table);
-    default: return launch_insert_k<kIdBytes, 0>(ctx, p, hashed, direct, table);
+    case 1: return launch_insert_k<kIdBits, 1>(ctx, p, hashed, direct, table);
+    case 2: return launch_insert_k<kIdBits, 2>(ctx, p, hashed, direct, table);
+    case 3: return launch_insert_k<kIdBits, 3>(ctx, p, hashed, direct, table);
+    case 4: return launch_insert_k<kIdBits, 4>(ctx, p, hashed, direct, table);
+    default: return launch_insert_k<kIdBits, 0>(ctx, p, hashed, direct, table);
   }
 }
 
@@ -442,8 +483,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint32_t* block = ctx.slot_t<uint32_t>("sh.block", n);
   uint8_t* flag = ctx.slot_t<uint8_t>("sh.flag", n);
   uint8_t* lead = ctx.slot_t<uint8_t>("sh.lead", n);
-  uint8_t* m8 = ctx.slot_t<uint8_t>("sh.m8", n);
-  uint16_t* m16 = nullptr;
+  // packed id mirror for the gathers (sized for the widest packed case, 16 bits)
+  uint32_t* mirror = ctx.slot_t<uint32_t>("sh.mirror", ceil_div(n, 2) + 1);
   uint32_t* act_buf[2] = {ctx.slot_t<uint32_t>("sh.act0", n), ctx.slot_t<uint32_t>("sh.act1", n)};
   uint32_t* slot_of = ctx.slot_t<uint32_t>("sh.slotof", n);
   uint32_t* res = ctx.slot_t<uint32_t>("sh.res", n);
@@ -467,15 +508,28 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint32_t B = split ? 2u : 1u;
   {
     ProfScope p(ctx, "init", n * 10);
-    init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, first2, block, lead, m8);
+    init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, first2, block, lead);
     DFM_LAUNCH_CHECK();
   }
+  int mirror_bits = 0;  // id width of the current gather source (32 = block itself)
+  auto build_mirror = [&](uint32_t blocks) {
+    const int bits = blocks <= 2 ? 1 : blocks <= 16 ? 4 : blocks <= 256 ? 8 : blocks <= 65536 ? 16 : 32;
+    mirror_bits = bits;
+    if (bits == 32) return;
+    ProfScope p(ctx, "mirror", n * 4 + n * bits / 8);
+    const unsigned g = grid_for(ctx, ceil_div(n, 32 / bits));
+    if (bits == 1) mirror_kernel<1><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+    else if (bits == 4) mirror_kernel<4><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+    else if (bits == 8) mirror_kernel<8><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+    else mirror_kernel<16><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+    DFM_LAUNCH_CHECK();
+  };
+  build_mirror(B);
   const uint32_t* act = nullptr;  // identity at pass 1
   int act_sel = 0;
   uint64_t m = n;
   uint64_t seed = 0x5EED0001ull;
   std::vector<uint32_t> trace_buf;
-  int mirror_bytes = 1;  // id width of the current gather mirror (4 = block itself)
 
   while (true) {
     if (dl.expired()) {
@@ -487,32 +541,30 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     const bool packed = kbits <= 63;
     // direct-indexed table (slot = key, no probing) when the key space is small
     const bool direct = packed && kbits <= 30 && (1ull << kbits) <= std::max<uint64_t>(2 * m, 4096);
-    uint64_t table = 0;
-    if (direct) {
-      table = 1ull << kbits;
-    } else {
-      table = 1024;
-      while (table < m + m / 2) table <<= 1;
-    }
+    // hash tables: load factor <= 2/3 (capacity need not be a power of two)
+    const uint64_t table = direct ? (1ull << kbits) : std::max<uint64_t>(1024, m + m / 2);
     DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
     uint32_t* act_next = act_buf[act_sel ^ 1];
     if (m > 0) {
       Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", table * sizeof(Slot)));
       DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
-      const void* ids = mirror_bytes == 1 ? (const void*)m8
-                        : mirror_bytes == 2 ? (const void*)m16 : (const void*)block;
-      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table - 1, slots,
+      const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
+      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table, slots,
                       slot_of, packed ? nullptr : sig, row};
       {
         // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
         // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
         ProfScope p(ctx, "sig",
-                    m * (4ull * k + (uint64_t)mirror_bytes * k + 4 + 1 + (act ? 4 : 0) + 16 + 4 +
-                         (packed ? 0 : 4ull * row)));
-        if (mirror_bytes == 1) launch_insert<1>(ctx, ip, !packed, direct, table);
-        else if (mirror_bytes == 2) launch_insert<2>(ctx, ip, !packed, direct, table);
-        else launch_insert<4>(ctx, ip, !packed, direct, table);
+                    m * (4ull * k + (uint64_t)std::max(1, mirror_bits / 8) * k + 4 + 1 +
+                         (act ? 4 : 0) + 16 + 4 + (packed ? 0 : 4ull * row)));
+        switch (mirror_bits) {
+          case 1: launch_insert<1>(ctx, ip, !packed, direct, table); break;
+          case 4: launch_insert<4>(ctx, ip, !packed, direct, table); break;
+          case 8: launch_insert<8>(ctx, ip, !packed, direct, table); break;
+          case 16: launch_insert<16>(ctx, ip, !packed, direct, table); break;
+          default: launch_insert<32>(ctx, ip, !packed, direct, table); break;
+        }
       }
       {
         ProfScope p(ctx, "scan", m * (4ull + 16 + 4 + 4 + 1));  // slot_of, slot, own id, res, st
@@ -553,21 +605,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     m = ctx.h_scalars[3];
     act = act_next;
     act_sel ^= 1;
-    // id mirror for the next pass's gathers
-    if (B <= 256) {
-      ProfScope p(ctx, "mirror", n * 5);
-      mirror_kernel<uint8_t><<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, m8);
-      DFM_LAUNCH_CHECK();
-      mirror_bytes = 1;
-    } else if (B <= 65536) {
-      if (m16 == nullptr) m16 = ctx.slot_t<uint16_t>("sh.m16", n);
-      ProfScope p(ctx, "mirror", n * 6);
-      mirror_kernel<uint16_t><<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, m16);
-      DFM_LAUNCH_CHECK();
-      mirror_bytes = 2;
-    } else {
-      mirror_bytes = 4;
-    }
+    build_mirror(B);  // id mirror for the next pass's gathers
   }
   out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
   if (B == n) {  // every block a singleton: first-occurrence labels are the identity
