@@ -270,7 +270,8 @@ def run_ours(args, rank: int, world: int, local: int):
         hd = dfm.Dfa(args.n, args.k, pin_delta.numpy().view(np.uint32), pin_acc.numpy(), 0)
         del host
         out_pin = torch.empty(args.n, dtype=torch.int32, pin_memory=True)
-        run_host = {"sort": lambda: eng.sort_pr(hd),
+        out_np = out_pin.numpy().view(np.uint32)
+        run_host = {"sort": lambda: eng.sort_pr(hd, out=out_np),
                     "naive": lambda: eng.naive_pr(hd, dfm.PrOptions(
                         policy=dfm.RacePolicy.deterministic_min)),
                     "transpr": lambda: eng.trans_pr(hd, dfm.PrOptions(

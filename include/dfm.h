@@ -190,6 +190,35 @@ int dfm_run_algorithm_dev(dfm_ctx* ctx, int32_t algo, const dfm_ddfa* dd, int32_
 int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double accept_prob,
                        uint32_t* delta_flat, uint8_t* accepting);
 
+/* ---------------------------------------------------------------- sharded sortPR primitives */
+/* State-sharded sortPR: one process per GPU; the host driver
+ * (paper_2410_22764_b200/sharded.py) owns the collectives (torch.distributed over
+ * NCCL) and calls these on device pointers (ctx's device and stream).  A rank owns
+ * states [lo, lo+n_local); delta_local is k rows of n_local GLOBAL target ids. */
+/* keys_out (u64[n_local]): 64-bit hash (never 0) of the signature row
+ * (block_full[lo+i], block_full[delta_a(i)] for a < k) under `seed`; sig_out
+ * (u32[n_local*(k+1)]): the rows themselves; dest_out (u32[n_local]): the rank in
+ * [0, ranks) that groups this key. */
+int dfm_shard_signature(dfm_ctx* ctx, const void* delta_local, uint64_t n_local, uint32_t k,
+                        const void* block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
+                        void* keys_out, void* sig_out, void* dest_out);
+/* Exact grouping of `count` received (key, signature-row) pairs: label_out[i] = dense
+ * local group id in [0, *groups_out).  Equal-hash members are verified word by word
+ * against the group's first member; *collision_out = 1 when two different rows share a
+ * key (the driver then redoes the pass under another seed). */
+int dfm_shard_group(dfm_ctx* ctx, const void* keys, const void* sig, uint32_t words,
+                    uint64_t count, void* label_out, uint64_t* groups_out, int* collision_out);
+/* In-place stable LSD radix sort of (u64 key, u32 value) pairs on the low `bits` bits. */
+int dfm_sort_pairs(dfm_ctx* ctx, void* keys, void* values, uint64_t count, uint32_t bits);
+/* Canonical relabel (core.hpp:123-136) of raw labels < n: device in, device out. */
+int dfm_canonicalize_dev(dfm_ctx* ctx, const void* raw_dev, uint64_t n, void* out_dev,
+                         uint32_t* num_blocks_out);
+/* Bit-exact random_dfa (generators.hpp:130-145) rows for states [lo, lo+count) of an
+ * n_total-state automaton: delta_out k rows of `count` u32, accepting_out count u8. */
+int dfm_random_dfa_slice_dev(dfm_ctx* ctx, uint64_t n_total, uint32_t k, uint64_t seed,
+                             double accept_prob, uint64_t lo, uint64_t count, void* delta_out,
+                             void* accepting_out);
+
 #ifdef __cplusplus
 }
 #endif

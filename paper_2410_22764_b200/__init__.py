@@ -386,13 +386,16 @@ class Engine:
         return _CTrace(fn, None), fn
 
     # -- reference API
-    def sort_pr(self, d: Dfa, opt=None) -> MinResult:
+    def sort_pr(self, d: Dfa, opt=None, out: Optional[np.ndarray] = None) -> MinResult:
+        """`out`: optional caller-owned uint32[n] result buffer (pass pinned memory for a
+        full-bandwidth device-to-host copy)."""
         if opt is None:
             opt = SortOptions()
         elif isinstance(opt, int):
             opt = SortOptions(timeout_ms=opt)
         cd, keep = self._cdfa(d)
-        block = np.empty(d.num_states, np.uint32)
+        block = out if out is not None else np.empty(d.num_states, np.uint32)
+        assert block.dtype == np.uint32 and block.size == d.num_states and block.flags.c_contiguous
         nb = C.c_uint32(0)
         st = _CStats()
         tr = None

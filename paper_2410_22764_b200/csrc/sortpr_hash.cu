@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
 // K1 for tiny direct tables (pass 1: 2^(k+1) keys): CTA aggregation in smem
 template <int kIdBits, int kK>
 __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint32_t table) {
-  __shared__ uint32_t s_rep[kSmallTable];
-  __shared__ uint32_t s_info[kSmallTable];
+  extern __shared__ uint32_t s_small[];  // [table] rep, [table] info (dynamic: tiny tables
+  uint32_t* s_rep = s_small;              //  leave room for many CTAs per SM)
+  uint32_t* s_info = s_small + table;
   for (uint32_t t = threadIdx.x; t < table; t += blockDim.x) {
     s_rep[t] = 0;
     s_info[t] = 0;
@@ -451,8 +452,8 @@ template <int kIdBits, int kK>
 void launch_insert_k(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
   const unsigned grid = grid_for(ctx, p.m);
   if (direct && table <= kSmallTable)
-    insert_small_kernel<kIdBits, kK>
-        <<<std::min<unsigned>(grid, ctx.num_sms * 4), 256, 0, ctx.stream>>>(p, (uint32_t)table);
+    insert_small_kernel<kIdBits, kK><<<std::min<unsigned>(grid, ctx.num_sms * 8), 256,
+                                       2 * table * sizeof(uint32_t), ctx.stream>>>(p, (uint32_t)table);
   else if (direct)
     insert_kernel<kIdBits, false, true, kK><<<grid, 256, 0, ctx.stream>>>(p);
   else if (hashed)

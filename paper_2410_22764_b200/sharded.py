@@ -1,0 +1,208 @@
+"""State-sharded sortPR over several GPUs.
+
+One process per GPU.  Rank g owns the contiguous state range [lo_g, hi_g) and
+its δ rows (global target ids).  Each refinement pass (min_sort.hpp:93-118):
+
+  1. all-gather the owned block-id slices   -> full block vector on every rank
+  2. signature rows + 64-bit keys of owned states (libdfm ``dfm_shard_signature``)
+  3. route every (key, row) to the rank ``dest(key)`` that groups it:
+     radix sort by destination (``dfm_sort_pairs``) + one all-to-all
+  4. exact local grouping at the destination (``dfm_shard_group``); a hash
+     collision anywhere voids the pass for all ranks (max all-reduce) and it is
+     redone under a new seed — the partition stays exact
+  5. all-gather of per-rank group counts -> dense global ids (rank offsets)
+  6. reverse all-to-all of the new ids to the owners
+  7. fixpoint when the global block count did not grow (the reference's
+     ``fresh == num_blocks``), so pass counts equal the reference's.
+
+Grouping is by exact key equality, independent of the number of ranks and of
+the hashing, so the partition sequence is the reference's for any world size.
+
+``Comm`` wraps torch.distributed (NCCL on GPU; gloo with host staging for the
+CPU tests); ``ops`` supplies the device primitives (``CudaShardOps`` here, a CPU
+stand-in in tests/) so the protocol itself is testable with gloo on CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+class Comm:
+    """torch.distributed collectives on 1-D tensors of the ops' device."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.stage = dist.is_initialized() and dist.get_backend(group) == "gloo"
+
+    def _to(self, t):
+        return t.cpu() if self.stage else t
+
+    def all_gather(self, t: torch.Tensor, counts) -> torch.Tensor:
+        """Concatenate every rank's `t` (rank r contributes counts[r] elements)."""
+        if self.world == 1:
+            return t
+        width = int(max(counts))  # collectives need equal sizes: pad, gather, trim
+        src = self._to(t)
+        if src.numel() < width:
+            src = torch.cat([src, src.new_zeros(width - src.numel())])
+        out = torch.empty(width * self.world, dtype=t.dtype, device=src.device)
+        dist.all_gather_into_tensor(out, src, group=self.group)
+        parts = [out[r * width:r * width + int(c)] for r, c in enumerate(counts)]
+        return torch.cat(parts).to(t.device)
+
+    def all_to_all(self, t: torch.Tensor, send_counts, recv_counts) -> torch.Tensor:
+        if self.world == 1:
+            return t.clone()
+        src = self._to(t).contiguous()
+        out = torch.empty(int(sum(recv_counts)), *t.shape[1:], dtype=t.dtype, device=src.device)
+        dist.all_to_all_single(out, src, [int(x) for x in recv_counts],
+                               [int(x) for x in send_counts], group=self.group)
+        return out.to(t.device)
+
+    def all_gather_ints(self, values) -> list:
+        """Gather a short list of python ints from every rank -> list per rank."""
+        v = torch.tensor(list(values), dtype=torch.int64)
+        if self.world == 1:
+            return [v.tolist()]
+        dev = "cpu" if self.stage or not torch.cuda.is_available() else torch.device(
+            "cuda", torch.cuda.current_device())
+        v = v.to(dev)
+        outs = [torch.empty_like(v) for _ in range(self.world)]
+        dist.all_gather(outs, v, group=self.group)
+        return [o.cpu().tolist() for o in outs]
+
+
+class CudaShardOps:
+    """libdfm device primitives on torch CUDA tensors (the product path)."""
+
+    def __init__(self, engine):
+        self.eng = engine
+        self.lib = engine.lib
+        lib = self.lib
+        vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+        lib.dfm_shard_signature.argtypes = [vp, vp, u64, u32, vp, u64, u64, u32, vp, vp, vp]
+        lib.dfm_shard_group.argtypes = [vp, vp, vp, u32, u64, vp, C.POINTER(u64),
+                                        C.POINTER(C.c_int)]
+        lib.dfm_sort_pairs.argtypes = [vp, vp, vp, u64, u32]
+        lib.dfm_canonicalize_dev.argtypes = [vp, vp, u64, vp, C.POINTER(u32)]
+        lib.dfm_random_dfa_slice_dev.argtypes = [vp, u64, u32, u64, C.c_double, u64, u64, vp, vp]
+        for f in ("dfm_shard_signature", "dfm_shard_group", "dfm_sort_pairs",
+                  "dfm_canonicalize_dev", "dfm_random_dfa_slice_dev"):
+            getattr(lib, f).restype = C.c_int
+
+    @property
+    def device(self):
+        return torch.device("cuda", self.eng.device)
+
+    def signature(self, delta_local, block_full, lo: int, seed: int, ranks: int):
+        k, n_local = delta_local.shape
+        keys = torch.empty(n_local, dtype=torch.int64, device=self.device)
+        sig = torch.empty((n_local, k + 1), dtype=torch.int32, device=self.device)
+        dest = torch.empty(n_local, dtype=torch.int32, device=self.device)
+        self.eng._check(self.lib.dfm_shard_signature(
+            self.eng.handle, delta_local.data_ptr(), n_local, k, block_full.data_ptr(), lo,
+            seed & (2 ** 64 - 1), ranks, keys.data_ptr(), sig.data_ptr(), dest.data_ptr()))
+        return keys, sig, dest
+
+    def route(self, dest, ranks: int):
+        """Stable order of items by destination rank + per-rank counts."""
+        n = dest.numel()
+        counts = torch.bincount(dest.long(), minlength=ranks).cpu().tolist()
+        if ranks == 1 or n == 0:
+            return torch.arange(n, dtype=torch.int64, device=self.device), counts
+        keys = dest.to(torch.int64).contiguous()
+        order = torch.arange(n, dtype=torch.int32, device=self.device)
+        bits = max(1, (ranks - 1).bit_length())
+        self.eng._check(self.lib.dfm_sort_pairs(self.eng.handle, keys.data_ptr(),
+                                                order.data_ptr(), n, bits))
+        return order.long(), counts
+
+    def group(self, keys, sig):
+        n, words = sig.shape
+        label = torch.empty(n, dtype=torch.int32, device=self.device)
+        groups = C.c_uint64(0)
+        coll = C.c_int(0)
+        self.eng._check(self.lib.dfm_shard_group(self.eng.handle, keys.data_ptr(), sig.data_ptr(),
+                                                 words, n, label.data_ptr(), C.byref(groups),
+                                                 C.byref(coll)))
+        return label, int(groups.value), bool(coll.value)
+
+    def canonicalize(self, raw):
+        out = torch.empty_like(raw)
+        nb = C.c_uint32(0)
+        self.eng._check(self.lib.dfm_canonicalize_dev(self.eng.handle, raw.data_ptr(), raw.numel(),
+                                                      out.data_ptr(), C.byref(nb)))
+        return out, int(nb.value)
+
+    def random_slice(self, n_total: int, k: int, seed: int, p: float, lo: int, count: int):
+        delta = torch.empty((k, count), dtype=torch.int32, device=self.device)
+        acc = torch.empty(count, dtype=torch.uint8, device=self.device)
+        self.eng._check(self.lib.dfm_random_dfa_slice_dev(
+            self.eng.handle, n_total, k, seed & (2 ** 64 - 1), p, lo, count, delta.data_ptr(),
+            acc.data_ptr()))
+        return delta, acc
+
+
+@dataclass
+class ShardedResult:
+    block_local: torch.Tensor  # canonical labels of the owned states
+    num_blocks: int
+    iterations: int
+    retries: int
+
+
+def shard_bounds(n_total: int, world: int, rank: int):
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
+    return lo, hi
+
+
+def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total: int, lo: int,
+                    comm: Comm, ops, max_passes: int | None = None) -> ShardedResult:
+    """sortPR over state shards.  delta_local: (k, n_local) int32 global targets;
+    acc_local: (n_local,) uint8.  Returns this rank's canonical labels."""
+    world, rank = comm.world, comm.rank
+    k, n_local = delta_local.shape
+    sizes = [hi - lo_ for lo_, hi in (shard_bounds(n_total, world, r) for r in range(world))]
+    # init, min_sort.hpp:80-88: two blocks iff both acceptance classes are non-empty
+    n_acc = sum(v[0] for v in comm.all_gather_ints([int(acc_local.sum().item())]))
+    split = 0 < n_acc < n_total
+    block = ((acc_local == 0).to(torch.int32) if split
+             else torch.zeros(n_local, dtype=torch.int32, device=acc_local.device))
+    B = 2 if split else 1
+    seed = 0x5EED0001
+    iterations = retries = 0
+    while True:
+        if max_passes is not None and iterations >= max_passes:
+            break
+        block_full = comm.all_gather(block, sizes)
+        keys, sig, dest = ops.signature(delta_local, block_full, lo, seed, world)
+        order, send_counts = ops.route(dest, world)
+        recv_counts = [c[rank] for c in comm.all_gather_ints(send_counts)]
+        rkeys = comm.all_to_all(keys[order], send_counts, recv_counts)
+        rsig = comm.all_to_all(sig[order], send_counts, recv_counts)
+        label, groups, collision = ops.group(rkeys, rsig)
+        stats = comm.all_gather_ints([groups, int(collision)])
+        if any(s[1] for s in stats):  # a collision on any rank voids the pass everywhere
+            retries += 1
+            seed = (seed * 0x9E3779B97F4A7C15 + 0x632BE59BD9B4E019) & (2 ** 64 - 1)
+            continue
+        offset = sum(s[0] for s in stats[:rank])
+        B_new = sum(s[0] for s in stats)
+        back = comm.all_to_all(label + offset, recv_counts, send_counts)
+        new_block = torch.empty_like(block)
+        new_block[order] = back.to(new_block.dtype)
+        iterations += 1
+        block = new_block
+        if B_new == B:  # fixpoint, min_sort.hpp:111-117
+            break
+        B = B_new
+    block_full = comm.all_gather(block, sizes)
+    canon, nb = ops.canonicalize(block_full)
+    return ShardedResult(canon[lo:lo + n_local].clone(), nb, iterations, retries)
