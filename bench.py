@@ -13,8 +13,10 @@ generated on the device bit-exactly with the reference generator.
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
-Multi-GPU: each rank minimizes its own replica DFA (seed + rank), no data-path
-collective ("replicas", weak scaling); timing is the max over ranks.
+Multi-GPU (N > 1): one random_dfa of N x 1e8 states, state-sharded over the N
+ranks (paper_2410_22764_b200/sharded.py: NCCL all-gather of block ids + key
+all-to-all per pass; weak scaling, 1e8 states per GPU); timing is the max over
+ranks.  --replicas runs N independent single-GPU minimizations instead.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 unmodified dfamin headers) on the host cores, on a bounded sample of the same
@@ -42,7 +44,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="sort", choices=["sort", "naive", "transpr", "naive_cas"])
+    ap.add_argument("--algo", default="sort",
+                    choices=["sort", "naive", "transpr", "naive_cas", "trans"])
+    ap.add_argument("--family", default="random",
+                    choices=["random", "chain", "comb", "fib", "bits", "vlts"],
+                    help="random: random_dfa(n,k,seed,p); chain: chain_dfa(n); comb: comb(n,3); "
+                         "fib: fib_dfa(n) (word index); bits: bit_splitter(n); "
+                         "vlts: inflated VLTS-shaped (m=--vlts-m, n, k)")
+    ap.add_argument("--vlts-m", type=int, default=1000)
     ap.add_argument("--n", type=int, default=100_000_000)
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--seed", type=int, default=1)
@@ -52,6 +61,8 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=10_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas instead of the state-sharded sortPR")
     return ap.parse_args()
 
 
@@ -183,10 +194,34 @@ def run_reference_arm(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def make_family(args):
+    from paper_2410_22764_b200 import generators as G
+    if args.family == "chain":
+        return G.chain_dfa(args.n)
+    if args.family == "comb":
+        return G.comb_dfa(args.n, 3)
+    if args.family == "fib":
+        return G.fib_dfa(args.n)
+    if args.family == "bits":
+        return G.bit_splitter(args.n)
+    if args.family == "vlts":
+        return G.vlts_dfa(args.vlts_m, args.n, args.k)
+    raise ValueError(args.family)
+
+
+def workload_name(args):
+    if args.family == "random" and args.algo == "sort":
+        return (f"sortPR on random_dfa(n={args.n:.0e}, k={args.k}, seed={args.seed}, p={args.p}) "
+                "— north-star 1-GPU config (SURVEY 8(d) C5)")
+    fam = {"random": f"random_dfa(n={args.n}, k={args.k}, seed={args.seed})",
+           "chain": f"chain_dfa({args.n})", "comb": f"comb({args.n},3)",
+           "fib": f"fib_dfa({args.n})", "bits": f"bit_splitter({args.n})",
+           "vlts": f"vlts(m={args.vlts_m}, n={args.n}, k={args.k})"}[args.family]
+    return f"{args.algo} on {fam}"
+
+
 def config(args, world, iters, blocks):
-    return {"workload": f"sortPR on random_dfa(n={args.n:.0e}, k={args.k}, seed={args.seed}, "
-                        f"p={args.p}) — north-star 1-GPU config (SURVEY 8(d) C5)"
-            if args.algo == "sort" else f"{args.algo} on random_dfa(n={args.n}, k={args.k})",
+    return {"workload": workload_name(args), "family": args.family,
             "algo": args.algo, "n": args.n, "k": args.k, "passes": iters, "blocks": blocks,
             "sortpr_engine": args.sortpr_engine if args.algo == "sort" else None,
             "parallelism": "replicas" if world > 1 else "single",
@@ -207,10 +242,15 @@ def run_ours(args, rank: int, world: int, local: int):
     stream = torch.cuda.current_stream(dev)
     eng.set_stream(stream.cuda_stream)
     algo = {"sort": dfm.Algo.sort, "naive": dfm.Algo.naive, "transpr": dfm.Algo.transpr,
-            "naive_cas": dfm.Algo.naive_cas}[args.algo]
+            "naive_cas": dfm.Algo.naive_cas, "trans": dfm.Algo.trans}[args.algo]
     cfg = dfm.AlgoRunConfig(policy=dfm.RacePolicy.deterministic_min)
     seed = args.seed + rank
-    dd = eng.random_dfa_device(args.n, args.k, seed, args.p)
+    if args.family == "random":
+        dd = eng.random_dfa_device(args.n, args.k, seed, args.p)
+    else:
+        hd = make_family(args)
+        args.n, args.k = hd.num_states, hd.alphabet_size
+        dd = eng.upload(hd)
     flush = None
     if 4 * args.n * args.k <= (126 << 20):
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -276,7 +316,8 @@ def run_ours(args, rank: int, world: int, local: int):
                         policy=dfm.RacePolicy.deterministic_min)),
                     "transpr": lambda: eng.trans_pr(hd, dfm.PrOptions(
                         policy=dfm.RacePolicy.deterministic_min)),
-                    "naive_cas": lambda: eng.naive_pr_cas(hd)}[args.algo]
+                    "naive_cas": lambda: eng.naive_pr_cas(hd),
+                    "trans": lambda: eng.trans_minimize(hd)}[args.algo]
         run_host()  # warm the host path
         barrier()
         e_ms = []
@@ -319,7 +360,7 @@ def run_ours(args, rank: int, world: int, local: int):
             "achieved": (it_bytes / 1e9) / (ms_per_step / 1e3),
             "frac": ((it_bytes / 1e9) / (ms_per_step / 1e3)) / peak}
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and args.algo == "sort" and args.family == "random":
         try:
             threads = os.cpu_count() or 1
             ns = min(args.n, args.cpu_sample_n)
@@ -343,6 +384,106 @@ def run_ours(args, rank: int, world: int, local: int):
     dd.free()
 
 
+def run_sharded(args, rank: int, world: int, local: int):
+    """N > 1: one random_dfa of n_total = n * N states, state-sharded over the ranks
+    (paper_2410_22764_b200/sharded.py: NCCL all-gather of block ids + key exchange).
+    Weak scaling: every GPU owns n states."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2410_22764_b200 as dfm
+    from paper_2410_22764_b200.sharded import Comm, CudaShardOps, shard_bounds, sharded_sort_pr
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    eng = dfm.Engine(local)
+    eng.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    ops = CudaShardOps(eng)
+    comm = Comm()
+    n_total = args.n * world
+    lo, hi = shard_bounds(n_total, world, rank)
+    delta, acc = ops.random_slice(n_total, args.k, args.seed, args.p, lo, hi - lo)
+    for _ in range(args.warmup):
+        r = sharded_sort_pr(delta, acc, n_total, lo, comm, ops)
+    eng.profile_reset()
+    eng.set_profiling(True)
+    launches0 = eng.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    step_ms = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = sharded_sort_pr(delta, acc, n_total, lo, comm, ops)
+        e1.record()
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clk = clocks.stop()
+    launches = eng.kernel_launches() - launches0
+    eng.set_profiling(False)
+    prof = eng.profile()
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    transitions = float(n_total) * args.k * r.iterations
+    value = transitions / (ms_per_step / 1e3)
+    e2e = None
+    if not args.no_e2e:
+        # host slice in pinned memory -> H2D, sharded run, D2H of this rank's labels
+        pin_d = torch.empty(delta.shape, dtype=torch.int32, pin_memory=True)
+        pin_a = torch.empty(acc.shape, dtype=torch.uint8, pin_memory=True)
+        pin_d.copy_(delta)
+        pin_a.copy_(acc)
+        out = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        e_ms = []
+        for _ in range(args.e2e_steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            rr = sharded_sort_pr(pin_d.to(dev, non_blocking=True), pin_a.to(dev, non_blocking=True),
+                                 n_total, lo, comm, ops)
+            out.copy_(rr.block_local)
+            torch.cuda.synchronize(dev)
+            e_ms.append((time.perf_counter() - t0) * 1e3)
+        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": transitions / (float(et.item()) / 1e3), "unit": UNIT,
+               "ms_per_step": float(et.item()),
+               "h2d_bytes_per_step": (4 * args.k + 1) * n_total,
+               "d2h_bytes_per_step": 4 * n_total,
+               "how": "per rank: pinned host slice -> H2D, sharded sortPR, D2H of owned labels; "
+                      "max over ranks"}
+    if rank != 0:
+        return
+    peak, peak_src = measured_peaks()
+    fam = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    roofline = None
+    if fam is not None:
+        name, (scopes, fms, fbytes) = fam
+        achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
+        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(name),
+                    "peak_source": peak_src, "rank": 0,
+                    "families_ms_per_step": {k: v[1] / args.steps for k, v in prof.items()}}
+    cfg = config(args, world, r.iterations, r.num_blocks)
+    cfg.update({"parallelism": f"state-sharded x{world} (NCCL all-gather + all-to-all)",
+                "n_total": n_total, "workload": f"sharded sortPR on random_dfa(n={n_total:.2e}, "
+                f"k={args.k}, seed={args.seed}) — {args.n:.0e} states per GPU (SURVEY 8(d) C5)",
+                "hash_retries": r.retries})
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "wall_time_to_minimal_dfa_ms": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: random_dfa slices generated on device, bit-exact with generators.hpp",
+            "config": cfg, "e2e": e2e, "roofline": roofline, "cpu_baseline": None,
+            "clocks": clk, "gpu_launches": launches, "step_ms": step_ms, "lib": dfm.lib_path()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -356,7 +497,10 @@ def main():
         torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        run_ours(args, rank, world, local)
+        if world > 1 and args.algo == "sort" and not args.replicas:
+            run_sharded(args, rank, world, local)
+        else:
+            run_ours(args, rank, world, local)
     finally:
         if world > 1:
             import torch

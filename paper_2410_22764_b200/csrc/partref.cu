@@ -16,7 +16,11 @@
 #include <algorithm>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "prims.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dfm {
 namespace {
@@ -153,12 +157,115 @@ __global__ void __launch_bounds__(256) double_kernel(const uint32_t* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent cooperative variant: all passes of a run in one launch, passes
+// separated by grid-wide barriers instead of kernel boundaries — for inputs
+// whose pass count, not per-pass work, dominates (C1: 16,474 passes on 1e5
+// states; rings and chains: n-1 passes).  Same per-pass semantics as
+// elect/split/cas_kernel above.
+struct PersistentArgs {
+  const uint32_t* rows;
+  uint64_t n, letters;
+  uint32_t* lab0;
+  uint32_t* lab1;
+  unsigned long long* cells;
+  uint8_t* split;
+  uint32_t* changed;  // one flag per pass of this launch (zeroed by the host)
+  uint32_t pass0;     // epoch of the pass before this launch
+  uint32_t max_passes;
+  int start_sel;
+  uint32_t* out;      // [0] passes executed, [1] stable, [2] buffer holding the labels
+};
+
+template <int kPolicy, bool kCas>
+__global__ void __launch_bounds__(256) persistent_kernel(PersistentArgs a) {
+  cg::grid_group g = cg::this_grid();
+  const uint64_t first = g.thread_rank(), nth = g.size();
+  int sel = a.start_sel;
+  uint32_t p = 0;
+  bool stable = false;
+  while (p < a.max_passes) {
+    const uint32_t pass = a.pass0 + p + 1;
+    const uint32_t* cur = sel ? a.lab1 : a.lab0;
+    uint32_t* nxt = sel ? a.lab0 : a.lab1;
+    bool any = false;
+    if (kCas) {
+      for (uint64_t qi = first; qi < a.n; qi += nth) {
+        const uint32_t q = (uint32_t)qi;
+        const uint32_t leader = cur[q];
+        if (!splits(a.rows, a.n, a.letters, cur, q, leader)) {
+          nxt[q] = leader;
+          continue;
+        }
+        any = true;
+        const unsigned long long mine = ((unsigned long long)pass << 32) | q;
+        unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(&a.cells[leader]);
+        uint32_t winner;
+        while (true) {
+          if ((uint32_t)(old >> 32) == pass) {
+            winner = (uint32_t)old;
+            break;
+          }
+          const unsigned long long prev = atomicCAS(&a.cells[leader], old, mine);
+          if (prev == old) {
+            winner = q;
+            break;
+          }
+          old = prev;
+        }
+        nxt[q] = winner;
+      }
+    } else {
+      for (uint64_t qi = first; qi < a.n; qi += nth) {
+        const uint32_t q = (uint32_t)qi;
+        const uint32_t leader = cur[q];
+        const bool sp = splits(a.rows, a.n, a.letters, cur, q, leader);
+        a.split[q] = sp;
+        if (sp) {
+          if (kPolicy == DFM_POLICY_MIN)
+            atomicMin(&a.cells[leader], ((unsigned long long)(~pass) << 32) | q);
+          else if (kPolicy == DFM_POLICY_MAX)
+            atomicMax(&a.cells[leader], ((unsigned long long)pass << 32) | q);
+          else
+            *reinterpret_cast<volatile unsigned long long*>(&a.cells[leader]) =
+                ((unsigned long long)pass << 32) | q;
+        }
+      }
+      g.sync();
+      for (uint64_t qi = first; qi < a.n; qi += nth) {
+        const uint32_t c = cur[qi];
+        if (a.split[qi]) {
+          nxt[qi] = (uint32_t)a.cells[c];
+          any = true;
+        } else {
+          nxt[qi] = c;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) a.changed[p] = 1u;
+    g.sync();
+    sel ^= 1;
+    ++p;
+    if (*reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u) {
+      stable = true;
+      break;
+    }
+  }
+  if (first == 0) {
+    a.out[0] = p;
+    a.out[1] = stable ? 1u : 0u;
+    a.out[2] = (uint32_t)sel;
+  }
+}
+
 unsigned grid_for(const Ctx& ctx, uint64_t items) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
                                       (uint64_t)ctx.num_sms * 16);
 }
 
 }  // namespace
+
+constexpr uint64_t kPersistentMaxStates = 1ull << 22;
 
 AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uint64_t letters,
                             int policy, bool fused_cas, const Deadline& dl,
@@ -186,6 +293,48 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
   }
   int sel = 0;
   uint32_t pass = 0;
+  const bool tracing_ = trace && trace->on_pass;
+  if (!tracing_ && n <= kPersistentMaxStates) {
+    // one cooperative launch per chunk of passes; the deadline is checked between chunks
+    const uint32_t kChunk = 8192;
+    uint32_t* chg = ctx.slot_t<uint32_t>("pr.pchanged", kChunk);
+    uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
+    void (*kern)(PersistentArgs) =
+        fused_cas ? persistent_kernel<DFM_POLICY_ARBITRARY, true>
+        : policy == DFM_POLICY_MIN ? persistent_kernel<DFM_POLICY_MIN, false>
+        : policy == DFM_POLICY_MAX ? persistent_kernel<DFM_POLICY_MAX, false>
+                                   : persistent_kernel<DFM_POLICY_ARBITRARY, false>;
+    int per_sm = 0;
+    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    const unsigned pgrid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, 256)));
+    while (true) {
+      if (dl.expired()) {
+        out.status = DFM_STATUS_TIMEOUT;
+        return out;
+      }
+      DFM_CUDA(cudaMemsetAsync(chg, 0, kChunk * 4, ctx.stream));
+      PersistentArgs pa{rows, n, letters, lab[0], lab[1], cells, split_flag, chg, pass, kChunk,
+                        sel, pout};
+      void* args[] = {&pa};
+      {
+        ProfScope p(ctx, "elect", 0);
+        DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, 256, args, 0, ctx.stream));
+        DFM_LAUNCH_CHECK();
+      }
+      DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, pout, 12, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(ctx.h_scalars + 20);
+      pass += h[0];
+      sel = (int)h[2];
+      if (h[1]) break;
+    }
+    out.iterations = pass;
+    out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+    out.num_blocks = canonicalize_dev(ctx, lab[sel], n, out.canon_dev);
+    out.status = DFM_STATUS_OK;
+    return out;
+  }
   uint32_t batch = 1;
   std::vector<uint32_t> h_changed(kBatchMax);
   std::vector<uint32_t> trace_buf;

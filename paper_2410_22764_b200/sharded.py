@@ -84,6 +84,8 @@ class CudaShardOps:
     def __init__(self, engine):
         self.eng = engine
         self.lib = engine.lib
+        # kernels must be ordered with the torch ops and NCCL collectives around them
+        engine.set_stream(torch.cuda.current_stream(torch.device("cuda", engine.device)).cuda_stream)
         lib = self.lib
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         lib.dfm_shard_signature.argtypes = [vp, vp, u64, u32, vp, u64, u64, u32, vp, vp, vp]
