@@ -105,7 +105,8 @@ const char* dfm_version(void);
 int dfm_ctx_create(int device, dfm_ctx** out);
 void dfm_ctx_destroy(dfm_ctx* ctx);
 const char* dfm_last_error(const dfm_ctx* ctx);
-/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the ctx's own. */
+/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the ctx's own.
+ * The legacy default stream is passed as cudaStreamLegacy ((void*)0x1). */
 int dfm_ctx_set_stream(dfm_ctx* ctx, void* stream);
 /* sortPR grouping engine: both give the reference's partitions and pass
  * counts.  HASH (default): active states grouped through an open-addressing table;

@@ -542,7 +542,14 @@ class Engine:
 
     # -- profiling
     def set_stream(self, stream_ptr: Optional[int]) -> None:
-        self._check(self.lib.dfm_ctx_set_stream(self.handle, stream_ptr))
+        """Run on a caller stream (e.g. torch.cuda.current_stream().cuda_stream).  torch's
+        default stream has handle 0, which is passed as cudaStreamLegacy (0x1); None
+        restores the engine's own stream."""
+        if stream_ptr is None:
+            ptr = None
+        else:
+            ptr = int(stream_ptr) or 1  # 0 = legacy default stream -> cudaStreamLegacy
+        self._check(self.lib.dfm_ctx_set_stream(self.handle, ptr))
 
     def set_sortpr_engine(self, engine: str) -> None:
         """'hash' (default) or 'radix' (the paper's sort); same results."""

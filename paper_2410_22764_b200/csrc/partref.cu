@@ -295,9 +295,13 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
   uint32_t pass = 0;
   const bool tracing_ = trace && trace->on_pass;
   if (!tracing_ && n <= kPersistentMaxStates) {
-    // one cooperative launch per chunk of passes; the deadline is checked between chunks
-    const uint32_t kChunk = 8192;
-    uint32_t* chg = ctx.slot_t<uint32_t>("pr.pchanged", kChunk);
+    // one cooperative launch per chunk of passes; the deadline is checked between
+    // chunks (the reference checks it before every pass, min_partref.hpp:78-83), so
+    // chunks start small and double: a run that overruns its deadline is reported as
+    // a timeout within ~2x of it
+    const uint32_t kChunkMax = 8192;
+    uint32_t chunk = 16;
+    uint32_t* chg = ctx.slot_t<uint32_t>("pr.pchanged", kChunkMax);
     uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
     void (*kern)(PersistentArgs) =
         fused_cas ? persistent_kernel<DFM_POLICY_ARBITRARY, true>
@@ -313,9 +317,10 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
         out.status = DFM_STATUS_TIMEOUT;
         return out;
       }
-      DFM_CUDA(cudaMemsetAsync(chg, 0, kChunk * 4, ctx.stream));
-      PersistentArgs pa{rows, n, letters, lab[0], lab[1], cells, split_flag, chg, pass, kChunk,
+      DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
+      PersistentArgs pa{rows, n, letters, lab[0], lab[1], cells, split_flag, chg, pass, chunk,
                         sel, pout};
+      chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&pa};
       {
         ProfScope p(ctx, "elect", 0);
