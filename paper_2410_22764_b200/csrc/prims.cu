@@ -34,7 +34,7 @@ __global__ void radix_bucket_scan_kernel(const uint32_t* __restrict__ hist,
 }
 
 template <bool kIdentVals>
-__global__ void __launch_bounds__(kRsThreads) onesweep_kernel(
+__global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t count, int shift,
     const uint32_t* __restrict__ bucket_base, uint64_t* status, uint32_t* ticket) {

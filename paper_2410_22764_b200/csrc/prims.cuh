@@ -168,7 +168,7 @@ void lookback_scan(Ctx& ctx, const char* slot, uint64_t count, In in, Out out,
 // ------------------------------------------------------------------ radix sort
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsItems = 16;
+constexpr int kRsItems = 8;
 constexpr int kRsTile = kRsThreads * kRsItems;  // 4096
 constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 64;
 

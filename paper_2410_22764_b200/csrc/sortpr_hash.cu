@@ -64,6 +64,7 @@ struct InsertParams {
   uint32_t* __restrict__ slot_of;
   uint32_t* __restrict__ sig;
   uint32_t row;  // signature row stride (words)
+  unsigned long long* keys;  // precomputed exact keys (swept passes), else unused
 };
 
 // L2 eviction policies: the delta stream is read once per pass (evict first) so
@@ -168,7 +169,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
 }
 
 // K1, hash or large direct table; warp-level aggregation of equal slots
-template <int kIdBits, bool kHashed, bool kDirect, int kK>
+template <int kIdBits, bool kHashed, bool kDirect, int kK, bool kFromKeys = false>
 __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_ids = policy_evict_last();
@@ -191,7 +192,8 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
         const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
         const uint32_t b = p.block[q];
         lead[u] = p.lead[q];
-        key[u] = make_key<kIdBits, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
+        key[u] = kFromKeys ? p.keys[i]
+                           : make_key<kIdBits, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
       }
     }
 #pragma unroll
@@ -225,6 +227,33 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
         }
       }
     }
+  }
+}
+
+// Target-range sweep for exact packed keys whose id mirror exceeds the L2 share
+// a pass can keep resident (8/16-bit mirrors of 100/200 MB at n = 1e8): sweep s
+// only gathers ids of targets in [lo, hi) — a <= 50 MB slice of the mirror that
+// stays in L2 — and ORs them into the partial key (fields are disjoint bit
+// ranges, so the sweeps commute).  delta is re-streamed per sweep (evict-first).
+template <int kIdBits, int kK>
+__global__ void __launch_bounds__(256) sweep_kernel(InsertParams p, uint32_t lo, uint32_t hi,
+                                                    bool first) {
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_ids = policy_evict_last();
+  const uint32_t k = kK > 0 ? (uint32_t)kK : p.k;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
+    const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+    unsigned long long key = first ? (unsigned long long)p.block[q] << (k * p.w) : p.keys[i];
+#pragma unroll
+    for (int a = 0; a < (kK > 0 ? kK : 1); ++a) {
+      for (uint32_t aa = (kK > 0 ? (uint32_t)a : 0u); aa < (kK > 0 ? (uint32_t)a + 1 : k); ++aa) {
+        const uint32_t t = ld_stream(p.delta + (uint64_t)aa * p.n + q, pol_stream);
+        if (t >= lo && t < hi)
+          key |= (unsigned long long)load_id<kIdBits>(p.ids, t, pol_ids) << ((k - 1 - aa) * p.w);
+      }
+    }
+    p.keys[i] = key;
   }
 }
 
@@ -451,6 +480,25 @@ int bit_width_u32(uint32_t x) { return x == 0 ? 0 : 32 - __builtin_clz(x); }
 template <int kIdBits, int kK>
 void launch_insert_k(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
   const unsigned grid = grid_for(ctx, p.m);
+  constexpr uint64_t kSweepSlice = 48ull << 20;  // mirror bytes per sweep (L2-resident)
+  const uint64_t mirror_bytes = p.n * (uint64_t)kIdBits / 8;
+  if ((kIdBits == 8 || kIdBits == 16) && !hashed && !(direct && table <= kSmallTable) &&
+      mirror_bytes > kSweepSlice && p.keys != nullptr) {
+    const uint64_t sweeps = ceil_div(mirror_bytes, kSweepSlice);
+    const uint64_t width = ceil_div(p.n, sweeps);
+    for (uint64_t s = 0; s < sweeps; ++s) {
+      const uint64_t lo = s * width, hi = std::min<uint64_t>(p.n, lo + width);
+      sweep_kernel<kIdBits, kK><<<grid, 256, 0, ctx.stream>>>(p, (uint32_t)lo, (uint32_t)hi,
+                                                              s == 0);
+      DFM_LAUNCH_CHECK();
+    }
+    if (direct)
+      insert_kernel<kIdBits, false, true, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
+    else
+      insert_kernel<kIdBits, false, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
+    DFM_LAUNCH_CHECK();
+    return;
+  }
   if (direct && table <= kSmallTable)
     insert_small_kernel<kIdBits, kK><<<std::min<unsigned>(grid, ctx.num_sms * 8), 256,
                                        2 * table * sizeof(uint32_t), ctx.stream>>>(p, (uint32_t)table);
@@ -551,8 +599,11 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
       const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
+      unsigned long long* keys = nullptr;
+      if (packed && (mirror_bits == 8 || mirror_bits == 16))
+        keys = ctx.slot_t<unsigned long long>("sh.keys", m);
       InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table, slots,
-                      slot_of, packed ? nullptr : sig, row};
+                      slot_of, packed ? nullptr : sig, row, keys};
       {
         // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
         // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
