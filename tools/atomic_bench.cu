@@ -58,8 +58,11 @@ __global__ void k(Slot* t, uint64_t slots, uint64_t m, unsigned* sink) {
           : "memory");
       acc += (unsigned)lo;
     } else {
-      const uint4 v = *reinterpret_cast<const volatile uint4*>(p);
-      acc += v.x + v.z;
+      unsigned x, y, z, w;
+      asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x), "=r"(y), "=r"(z), "=r"(w)
+                   : "l"(p));
+      acc += x + z;
     }
   }
   if (acc == 0xFFFFFFFF) *sink = acc;
