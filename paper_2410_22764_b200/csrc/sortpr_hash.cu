@@ -79,6 +79,21 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 16-byte compare-and-swap (sm_90+): old = *p; if old == cmp then *p = val
+__device__ __forceinline__ void cas128(void* p, unsigned long long cmp_lo, unsigned long long cmp_hi,
+                                       unsigned long long val_lo, unsigned long long val_hi,
+                                       unsigned long long& old_lo, unsigned long long& old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 d, c, v;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 d, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(val_lo), "l"(val_hi), "l"(p)
+      : "memory");
+}
+
 // (non-volatile asm: read-only data, so the compiler may batch these loads)
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* a, uint64_t pol) {
   uint32_t v;
@@ -207,17 +222,43 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
           const unsigned long long stored = kHashed ? (key[u] | 1ull) : key[u] + 1ull;
           const unsigned long long h = kHashed ? key[u] : mix64(key[u] ^ p.seed);
           uint64_t t = __umul64hi(h, p.cap);
-          while (true) {
-            const unsigned long long cur = atomicCAS(&p.slots[t].key, 0ull, stored);
-            if (cur == 0ull || cur == stored) break;
-            if (++t == p.cap) t = 0;
+          if (kHashed) {
+            // hashed keys are nearly all distinct: claim/update the whole 16-byte slot
+            // {key, rep, info} with one blind 128-bit CAS (one random RMW per state)
+            const unsigned long long mine =
+                (unsigned long long)(~(uint32_t)i) |
+                ((unsigned long long)(1u | (lead[u] ? 0x80000000u : 0u)) << 32);
+            unsigned long long exp_lo = 0, exp_hi = 0, new_hi = mine;
+            while (true) {
+              unsigned long long old_lo, old_hi;
+              cas128(&p.slots[t], exp_lo, exp_hi, stored, new_hi, old_lo, old_hi);
+              if (old_lo == exp_lo && old_hi == exp_hi) break;
+              if (old_lo != stored) {  // another key owns this slot: probe on
+                if (++t == p.cap) t = 0;
+                exp_lo = exp_hi = 0;
+                new_hi = mine;
+                continue;
+              }
+              // same key: merge (min member, count + 1, keeper bit)
+              const uint32_t rep = max((uint32_t)old_hi, ~(uint32_t)i);
+              const uint32_t info = (uint32_t)(old_hi >> 32) + 1u + (lead[u] ? 0x80000000u : 0u);
+              exp_lo = old_lo;
+              exp_hi = old_hi;
+              new_hi = (unsigned long long)rep | ((unsigned long long)info << 32);
+            }
+          } else {
+            while (true) {
+              const unsigned long long cur = atomicCAS(&p.slots[t].key, 0ull, stored);
+              if (cur == 0ull || cur == stored) break;
+              if (++t == p.cap) t = 0;
+            }
           }
           s[u] = t;
         }
         p.slot_of[i] = (uint32_t)s[u];
       }
       const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u]);
-      if (valid[u]) {
+      if (valid[u] && !kHashed) {
         // lanes with the same slot: the lowest lane (smallest i) updates for all
         const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s[u]);
         const uint32_t leads = __ballot_sync(vmask, lead[u] != 0) & peers;
