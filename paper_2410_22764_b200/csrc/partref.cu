@@ -310,12 +310,8 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
                                    : persistent_kernel<DFM_POLICY_ARBITRARY, false>;
     int per_sm = 0;
     DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
-    // small inputs are barrier-bound: one CTA per SM keeps grid.sync() cheap; large
-    // ones are memory-bound and get every resident CTA
-    const uint64_t resident = n <= (1ull << 20) ? (uint64_t)ctx.num_sms
-                                                : (uint64_t)per_sm * ctx.num_sms;
-    const unsigned pgrid =
-        (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(resident, ceil_div(n, 256)));
+    const unsigned pgrid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, 256)));
     while (true) {
       if (dl.expired()) {
         out.status = DFM_STATUS_TIMEOUT;

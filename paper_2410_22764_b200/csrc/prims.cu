@@ -10,13 +10,14 @@ namespace prims {
 // per-pass digit histograms of all passes in one read of the keys
 __global__ void __launch_bounds__(256) radix_histogram_kernel(const uint64_t* __restrict__ keys,
                                                               uint64_t count, int passes,
-                                                              uint32_t* __restrict__ hist) {
+                                                              uint32_t* __restrict__ hist,
+                                                              int lo_bit) {
   __shared__ uint32_t sh[8 * 256];
   for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const uint64_t k = keys[i];
+    const uint64_t k = keys[i] >> lo_bit;
     for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 255)], 1u);
   }
   __syncthreads();
@@ -143,6 +144,12 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
 
 bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
                       uint32_t* alt_vals, uint64_t count, int bits, bool ident_vals) {
+  return radix_sort_pairs_bits(ctx, keys, vals, alt_keys, alt_vals, count, 0, bits, ident_vals);
+}
+
+bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
+                           uint32_t* alt_vals, uint64_t count, int lo_bit, int bits,
+                           bool ident_vals) {
   if (count == 0) return false;
   if (bits <= 0) bits = 1;  // identity values still need one materialising pass
   if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "radix_sort_pairs: count >= 2^32");
@@ -165,7 +172,7 @@ bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_ke
     ProfScope p(ctx, "sort", count * 8ull);  // one read of the keys for all digit histograms
     const unsigned grid =
         (unsigned)std::min<uint64_t>((uint64_t)ctx.num_sms * 8, ceil_div(count, 256));
-    radix_histogram_kernel<<<grid, 256, 0, ctx.stream>>>(keys, count, passes, hist);
+    radix_histogram_kernel<<<grid, 256, 0, ctx.stream>>>(keys, count, passes, hist, lo_bit);
     DFM_LAUNCH_CHECK();
     radix_bucket_scan_kernel<<<passes, 256, 0, ctx.stream>>>(hist, base);
     DFM_LAUNCH_CHECK();
@@ -180,11 +187,12 @@ bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_ke
       ProfScope ps(ctx, "sort", count * 24ull);  // (key 8 + value 4) read + written
       if (p == 0 && ident_vals)
         onesweep_kernel<true><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
-            kin, nullptr, kout, vout, (uint32_t)count, 8 * p, base + p * 256, status,
+            kin, nullptr, kout, vout, (uint32_t)count, lo_bit + 8 * p, base + p * 256, status,
             tickets + p);
       else
         onesweep_kernel<false><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
-            kin, vin, kout, vout, (uint32_t)count, 8 * p, base + p * 256, status, tickets + p);
+            kin, vin, kout, vout, (uint32_t)count, lo_bit + 8 * p, base + p * 256, status,
+            tickets + p);
       DFM_LAUNCH_CHECK();
     }
     std::swap(kin, kout);

@@ -178,6 +178,11 @@ constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4
 // keys/vals, true: alt_*).  count < 2^32.
 bool radix_sort_pairs(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
                       uint32_t* alt_vals, uint64_t count, int bits, bool ident_vals);
+// Same on bits [lo_bit, lo_bit + bits) of the keys (digit passes from lo_bit up):
+// a stable partition by that bit field.
+bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* alt_keys,
+                           uint32_t* alt_vals, uint64_t count, int lo_bit, int bits,
+                           bool ident_vals);
 
 }  // namespace prims
 }  // namespace dfm

@@ -1,0 +1,362 @@
+// Blocked signature builder for sortPR (included by sortpr_hash.cu inside its
+// anonymous namespace: uses ld_stream, load_id, mix64, the L2 policies).
+//
+// Problem: a pass needs, for every active state q, the ids of its k successors
+// — n*k random 4-byte gathers.  Measured on B200 (tools/l2_bench.cu): random
+// gathers are capped at ~285 G/s even when L2-resident (one L1 tag lookup per
+// request per SM clock) and fall to ~40-50 G/s once the id array exceeds L2;
+// shared-memory gathers run at ~700 G/s.
+//
+// Design (propagation blocking; delta is iteration-invariant, so the layout is
+// built once per minimization and reused by every pass):
+//   * target RANGES of kRs = 49152 states: a range's id slice (<= 192 KB even
+//     at 32 bits) fits in shared memory; a transition's target is stored as a
+//     16-bit offset inside its range (tgt, bucket order: range-major, then
+//     source window);
+//   * source WINDOWS of W states (W*k = 32768 transitions, one CTA tile);
+//   * per pass, G (one CTA per group of ranges) loads the id slice into shared
+//     memory and resolves every transition into that range with a shared-
+//     memory gather, writing the id straight to the transition's position in
+//     WINDOW-FLATTENED order (v, runs of ~16 consecutive positions);
+//   * P (one CTA per window) streams the window's ids and tile slots (lsf) —
+//     pure coalesced reads — into a shared-memory k x W tile and emits the
+//     exact packed key (or hash + signature row) of every active state.
+// HBM traffic per transition per pass: 2 (tgt) + 2 (lsf) + 2 x id width bytes;
+// no random HBM access.  Layout: tgt/lsf u16 [T], off u32 [R*nW+1] (bucket
+// start of sub-run (range j, window w), range-major), pre u16 [nW*R] (start of
+// sub-run (j, w) inside window w's flattened order, window-major).
+#pragma once
+
+constexpr uint32_t kRs = 49152;          // states per target range (16-bit offsets)
+constexpr uint32_t kMaxRanges = 4096;    // n <= 2.01e8 on the blocked path
+constexpr uint32_t kWinElems = 32768;    // transitions per source window (u16 tile slots)
+constexpr uint32_t kSliceBytes = 192u << 10;
+
+struct Layout {
+  uint32_t R = 0, W = 0, nW = 0, E = 0;  // E = W*k
+  uint64_t n = 0, T = 0;
+  uint32_t k = 0;
+  uint16_t* tgt = nullptr;
+  uint16_t* lsf = nullptr;
+  uint32_t* eidx = nullptr;    // [T] bucket position of each window-flattened transition
+  uint32_t* off = nullptr;
+  uint16_t* pre = nullptr;
+  uint32_t* wstart = nullptr;  // [nW + 1] first active index of each window
+  void* v = nullptr;           // [T] ids in window-flattened order (id bytes)
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt_() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- layout build: per-window range histogram (w-major) + in-window prefix
+__global__ void __launch_bounds__(512) lay_count_kernel(const uint32_t* __restrict__ delta, Layout L,
+                                                        uint32_t* __restrict__ cnt_w) {
+  extern __shared__ uint32_t s_h[];  // [R]
+  __shared__ uint32_t s_warp[512 / 32 + 1];
+  const uint64_t pol = policy_evict_first();
+  for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
+    for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) s_h[j] = 0;
+    __syncthreads();
+    const uint64_t q0 = (uint64_t)w * L.W;
+    const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
+    // 8 independent delta loads in flight per thread
+    for (uint32_t a = 0; a < L.k; ++a)
+      for (uint32_t x0 = 0; x0 < wn; x0 += 8 * blockDim.x) {
+        uint32_t t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
+          t[u] = x < wn ? ld_stream(delta + a * L.n + q0 + x, pol) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
+          if (x < wn) atomicAdd(&s_h[t[u] / kRs], 1u);
+        }
+      }
+    __syncthreads();
+    // counts (w-major, transposed later for the bucket scan) + in-window prefix
+    constexpr uint32_t kPer = kMaxRanges / 512;
+    const uint32_t j0 = threadIdx.x * kPer;
+    uint32_t c[kPer], sum = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) {
+      c[u] = j0 + u < L.R ? s_h[j0 + u] : 0u;
+      sum += c[u];
+    }
+    uint32_t tot;
+    uint32_t run = prims::block_exclusive_sum<512>(sum, s_warp, &tot);
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u)
+      if (j0 + u < L.R) {
+        cnt_w[(uint64_t)w * L.R + j0 + u] = c[u];
+        L.pre[(uint64_t)w * L.R + j0 + u] = (uint16_t)run;
+        run += c[u];
+      }
+    __syncthreads();
+  }
+}
+
+// [rows][cols] -> [cols][rows], 32x32 tiles
+__global__ void lay_transpose_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                     uint32_t rows, uint32_t cols) {
+  __shared__ uint32_t t[32][33];
+  const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
+    const uint32_t r = r0 + y, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) t[y][threadIdx.x] = in[(uint64_t)r * cols + c];
+  }
+  __syncthreads();
+  for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
+    const uint32_t c = c0 + y, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[(uint64_t)c * rows + r] = t[threadIdx.x][y];
+  }
+}
+
+struct LayOffIn {
+  const uint32_t* cnt;
+  __device__ uint32_t operator()(uint64_t i) const { return cnt[i]; }
+};
+struct LayOffOut {
+  uint32_t* off;
+  uint64_t count;
+  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
+    off[i] = excl;
+    if (i + 1 == count) off[count] = excl + v;
+  }
+};
+
+// ---- layout build: bucket every transition (tgt) and its tile slot (lsf).
+// Both are staged in shared memory in the window's flattened order (sub-run j
+// at pre(w, j)) with the sub-run index; lsf leaves as one coalesced chunk, tgt
+// and dst (the flattened position) as contiguous runs at off(j, w).
+__global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __restrict__ delta,
+                                                          Layout L) {
+  // s_cur[R], s_off[R], s_pre[R+1], then u16 s_lsf[E], s_tgt[E], s_j[E]
+  extern __shared__ uint32_t s_lay[];
+  uint32_t* s_cur = s_lay;
+  uint32_t* s_off = s_lay + L.R;
+  uint32_t* s_pre = s_lay + 2 * L.R;
+  uint16_t* s_lsf = reinterpret_cast<uint16_t*>(s_lay + 3 * L.R + 1);
+  uint16_t* s_tgt = s_lsf + L.E;
+  uint16_t* s_j = s_tgt + L.E;
+  const uint64_t pol = policy_evict_first();
+  for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
+    const uint64_t q0 = (uint64_t)w * L.W;
+    const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
+    const uint32_t ew = wn * L.k;
+    for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) {
+      s_cur[j] = 0;
+      s_off[j] = L.off[(uint64_t)j * L.nW + w];
+      s_pre[j] = L.pre[(uint64_t)w * L.R + j];
+    }
+    if (threadIdx.x == 0) s_pre[L.R] = ew;
+    __syncthreads();
+    for (uint32_t a = 0; a < L.k; ++a)
+      for (uint32_t x0 = 0; x0 < wn; x0 += 8 * blockDim.x) {
+        uint32_t t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
+          t[u] = x < wn ? ld_stream(delta + a * L.n + q0 + x, pol) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
+          if (x < wn) {
+            const uint32_t j = t[u] / kRs;
+            const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
+            s_tgt[f] = (uint16_t)(t[u] - j * kRs);
+            s_lsf[f] = (uint16_t)(a * L.W + x);
+            s_j[f] = (uint16_t)j;
+          }
+        }
+      }
+    __syncthreads();
+    const uint64_t fb = (uint64_t)w * L.E;
+    for (uint32_t f = threadIdx.x; f < ew; f += blockDim.x) {
+      L.lsf[fb + f] = s_lsf[f];
+      const uint32_t j = s_j[f];
+      const uint32_t e = s_off[j] + (f - s_pre[j]);
+      L.tgt[e] = s_tgt[f];
+      L.eidx[fb + f] = e;
+    }
+    __syncthreads();
+  }
+}
+
+// first active index of every window (act ascending); wstart[nW] = m
+__global__ void lay_wstart_kernel(const uint32_t* __restrict__ act, uint64_t m, uint32_t W,
+                                  uint32_t nW, uint32_t* __restrict__ wstart) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += stride) {
+    const int64_t w = i < m ? (int64_t)(act[i] / W) : (int64_t)nW;
+    const int64_t wp = i > 0 ? (int64_t)(act[i - 1] / W) : -1;
+    for (int64_t x = wp + 1; x <= w; ++x) wstart[x] = (uint32_t)i;
+  }
+}
+
+// id bytes in the flattened buffer: 1 for mirrors of <= 8 bits
+template <int kIdBits>
+struct IdT {
+  using type = uint8_t;
+};
+template <>
+struct IdT<16> {
+  using type = uint16_t;
+};
+template <>
+struct IdT<32> {
+  using type = uint32_t;
+};
+
+template <int kIdBits>
+__device__ __forceinline__ uint32_t slice_id(const uint32_t* s, uint32_t x) {
+  if (kIdBits == 1) return (s[x >> 5] >> (x & 31)) & 1u;
+  if (kIdBits == 4) return (s[x >> 3] >> ((x & 7) * 4)) & 0xFu;
+  if (kIdBits == 8) return reinterpret_cast<const uint8_t*>(s)[x];
+  if (kIdBits == 16) return reinterpret_cast<const uint16_t*>(s)[x];
+  return s[x];
+}
+
+// ---- per pass G: shared-memory gathers, one CTA per group of c ranges; ids
+// are written in bucket order (coalesced)
+template <int kIdBits>
+__global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32_t* __restrict__ ids,
+                                                          uint32_t c) {
+  using V = typename IdT<kIdBits>::type;
+  extern __shared__ uint4 s_slice4[];
+  __shared__ uint32_t s_bound[33];
+  uint32_t* s_slice = reinterpret_cast<uint32_t*>(s_slice4);
+  V* __restrict__ vout = static_cast<V*>(L.v);
+  const uint64_t pol = policy_evict_first();
+  const uint32_t groups = (L.R + c - 1) / c;
+  for (uint32_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    const uint32_t j0 = g * c, j1 = min(L.R, j0 + c);
+    // id slice of states [j0*kRs, min(n, j1*kRs)): words of the packed mirror
+    const uint64_t st0 = (uint64_t)j0 * kRs;
+    const uint64_t st1 = min(L.n, (uint64_t)j1 * kRs);
+    const uint64_t w0 = st0 * kIdBits / 32, w1 = (st1 * kIdBits + 31) / 32;
+    const uint32_t nwords = (uint32_t)(w1 - w0);
+    const uint4* src4 = reinterpret_cast<const uint4*>(ids + w0);  // 16-byte aligned: kRs*bits/8
+    for (uint32_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) s_slice4[i] = __ldg(src4 + i);
+    for (uint32_t i = (nwords / 4) * 4 + threadIdx.x; i < nwords; i += blockDim.x)
+      s_slice[i] = __ldg(ids + w0 + i);
+    if (threadIdx.x <= j1 - j0) s_bound[threadIdx.x] = L.off[(uint64_t)(j0 + threadIdx.x) * L.nW];
+    __syncthreads();
+    // range by range (no per-element range search); 8 targets per thread-step
+    for (uint32_t r = 0; r < j1 - j0; ++r) {
+      const uint32_t start = s_bound[r], end = s_bound[r + 1];
+      const uint32_t* sl = s_slice;
+      const uint32_t sb = r * kRs;
+      for (uint32_t e0 = start + threadIdx.x; e0 < end; e0 += 8 * blockDim.x) {
+        uint32_t t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x;
+          uint32_t x = 0;
+          if (e < end)
+            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                : "=r"(x) : "l"(L.tgt + e), "l"(pol));
+          t[u] = x;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x;
+          if (e < end) vout[e] = (V)slice_id<kIdBits>(sl, sb + t[u]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct SigParams {
+  Layout L;
+  const uint32_t* wstart;  // nullptr: every state active (act == identity)
+  const uint32_t* act;
+  const uint32_t* block;
+  int w;
+  uint64_t seed;
+  unsigned long long* keys;
+  uint32_t* sig;  // hashed: signature rows (stride row), else nullptr
+  uint32_t row;
+  // partitioned grouping (sortpr_group.cuh): packed keys leave as a bijective mix,
+  // and vals[i] = i | lead << 31
+  uint32_t* vals;
+  const uint8_t* lead;
+};
+
+// ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
+template <int kIdBits, int kK, bool kHashed>
+__global__ void __launch_bounds__(1024) lay_sig_kernel(SigParams p) {
+  using V = typename IdT<kIdBits>::type;
+  extern __shared__ uint4 s_tile4[];
+  V* s_tile = reinterpret_cast<V*>(s_tile4);  // [k][W]
+  const Layout& L = p.L;
+  const uint32_t k = kK > 0 ? (uint32_t)kK : L.k;
+  const V* __restrict__ vin = static_cast<const V*>(L.v);
+  const uint64_t pol = policy_evict_first();
+  for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
+    const uint64_t q0 = (uint64_t)w * L.W;
+    const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
+    const uint32_t ew = wn * k;
+    const uint64_t fb = (uint64_t)w * L.E;
+    // lane-consecutive transitions (coalesced slot / position loads; the ids come
+    // in runs of ~16 per sub-run), 8 in flight per thread
+    for (uint32_t f0 = threadIdx.x; f0 < ew; f0 += 8 * blockDim.x) {
+      uint32_t sl[8], ee[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t f = f0 + u * blockDim.x;
+        sl[u] = 0;
+        ee[u] = 0;
+        if (f < ew) {
+          asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+              : "=r"(sl[u]) : "l"(L.lsf + fb + f), "l"(pol));
+          asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+              : "=r"(ee[u]) : "l"(L.eidx + fb + f), "l"(pol));
+        }
+      }
+      V x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = (f0 + u * blockDim.x < ew) ? vin[ee[u]] : (V)0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (f0 + u * blockDim.x < ew) s_tile[sl[u]] = x[u];
+    }
+    __syncthreads();
+    const uint64_t i0 = p.wstart ? p.wstart[w] : q0;
+    const uint64_t i1 = p.wstart ? p.wstart[w + 1] : q0 + wn;
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
+      const uint32_t x = (uint32_t)(q - q0);
+      const uint32_t b = p.block[q];
+      if (!kHashed) {
+        unsigned long long key = b;
+#pragma unroll
+        for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
+          key = (key << p.w) | (uint32_t)s_tile[a * L.W + x];
+        p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
+      } else {
+        uint32_t* row = p.sig + i * (uint64_t)p.row;
+        row[0] = b;
+        unsigned long long h = mix64(p.seed * kGolden + b);
+#pragma unroll
+        for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a) {
+          const uint32_t s = s_tile[a * L.W + x];
+          row[a + 1] = s;
+          h = mix64(h + kGolden + s);
+        }
+        p.keys[i] = h;
+      }
+      if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
+      {
+      }
+    }
+    __syncthreads();
+  }
+}

@@ -25,6 +25,7 @@
 // members).  Ids are gathered from packed 1/4/8/16-bit mirrors while
 // B <= 2/16/256/65536, so early passes gather from L2.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "prims.cuh"
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
     uint32_t lead[2] = {0, 0};
     unsigned long long key[2] = {0, 0};
     bool valid[2];
+    bool merge[2] = {!kHashed, !kHashed};  // slot needs the aggregated rep/info update
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const uint64_t i = base + u * 32 + lane;
@@ -228,23 +230,17 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
             const unsigned long long mine =
                 (unsigned long long)(~(uint32_t)i) |
                 ((unsigned long long)(1u | (lead[u] ? 0x80000000u : 0u)) << 32);
-            unsigned long long exp_lo = 0, exp_hi = 0, new_hi = mine;
+            // a state finding its key already present joins the warp-aggregated
+            // atomic update below (a CAS merge loop serialises large groups)
             while (true) {
               unsigned long long old_lo, old_hi;
-              cas128(&p.slots[t], exp_lo, exp_hi, stored, new_hi, old_lo, old_hi);
-              if (old_lo == exp_lo && old_hi == exp_hi) break;
-              if (old_lo != stored) {  // another key owns this slot: probe on
-                if (++t == p.cap) t = 0;
-                exp_lo = exp_hi = 0;
-                new_hi = mine;
-                continue;
+              cas128(&p.slots[t], 0ull, 0ull, stored, mine, old_lo, old_hi);
+              if (old_lo == 0ull && old_hi == 0ull) break;
+              if (old_lo == stored) {
+                merge[u] = true;
+                break;
               }
-              // same key: merge (min member, count + 1, keeper bit)
-              const uint32_t rep = max((uint32_t)old_hi, ~(uint32_t)i);
-              const uint32_t info = (uint32_t)(old_hi >> 32) + 1u + (lead[u] ? 0x80000000u : 0u);
-              exp_lo = old_lo;
-              exp_hi = old_hi;
-              new_hi = (unsigned long long)rep | ((unsigned long long)info << 32);
+              if (++t == p.cap) t = 0;  // another key owns this slot: probe on
             }
           } else {
             while (true) {
@@ -257,8 +253,8 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
         }
         p.slot_of[i] = (uint32_t)s[u];
       }
-      const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u]);
-      if (valid[u] && !kHashed) {
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u] && merge[u]);
+      if (valid[u] && merge[u]) {
         // lanes with the same slot: the lowest lane (smallest i) updates for all
         const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s[u]);
         const uint32_t leads = __ballot_sync(vmask, lead[u] != 0) & peers;
@@ -299,7 +295,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(InsertParams p, uint32_t lo,
 }
 
 // K1 for tiny direct tables (pass 1: 2^(k+1) keys): CTA aggregation in smem
-template <int kIdBits, int kK>
+template <int kIdBits, int kK, bool kFromKeys = false>
 __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint32_t table) {
   extern __shared__ uint32_t s_small[];  // [table] rep, [table] info (dynamic: tiny tables
   uint32_t* s_rep = s_small;              //  leave room for many CTAs per SM)
@@ -320,7 +316,9 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
     if (!valid) continue;
     const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
     const uint32_t b = p.block[q];
-    const uint32_t s = (uint32_t)make_key<kIdBits, false, kK>(p, i, q, b, pol_stream, pol_ids);
+    const uint32_t s = kFromKeys ? (uint32_t)p.keys[i]
+                                 : (uint32_t)make_key<kIdBits, false, kK>(p, i, q, b, pol_stream,
+                                                                          pol_ids);
     p.slot_of[i] = s;
     // lanes are in ascending i: the lowest lane of each key group updates for all
     const uint32_t peers = __match_any_sync(vmask, s);
@@ -511,6 +509,12 @@ __global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
     out[q] = (uint32_t)q;
 }
 
+constexpr uint64_t kBlockedMinTransitions = 1ull << 25;
+constexpr uint64_t kPartMinStates = 1ull << 20;
+
+#include "sortpr_blocked.cuh"
+#include "sortpr_group.cuh"
+
 unsigned grid_for(const Ctx& ctx, uint64_t items, int per_sm = 16) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
                                       (uint64_t)ctx.num_sms * per_sm);
@@ -563,6 +567,194 @@ void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, ui
   }
 }
 
+// K1 from precomputed keys (blocked builder): packed or hashed, direct or probed
+template <int kK>
+void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
+  const unsigned grid = grid_for(ctx, p.m);
+  if (direct && table <= kSmallTable)
+    insert_small_kernel<32, kK, true><<<std::min<unsigned>(grid, ctx.num_sms * 8), 256,
+                                        2 * table * sizeof(uint32_t), ctx.stream>>>(p, (uint32_t)table);
+  else if (hashed)
+    insert_kernel<32, true, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
+  else if (direct)
+    insert_kernel<32, false, true, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
+  else
+    insert_kernel<32, false, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
+  DFM_LAUNCH_CHECK();
+}
+
+bool blocked_disabled() {
+  const char* e = getenv("DFM_SORTPR_BLOCKED");
+  return e != nullptr && e[0] == '0';
+}
+
+// the blocked builder needs u16 range offsets / tile slots and 32-bit positions
+bool layout_possible(uint64_t n, uint32_t k) {
+  const uint64_t T = n * (uint64_t)k;
+  return k > 0 && k <= 1024 && T < (1ull << 32) && ceil_div(n, kRs) <= kMaxRanges &&
+         T >= kBlockedMinTransitions && !blocked_disabled();
+}
+
+void build_layout(Ctx& ctx, const DevDfa& d, Layout& L) {
+  L.n = d.n;
+  L.k = d.k;
+  L.T = L.n * L.k;
+  L.R = (uint32_t)ceil_div(L.n, kRs);
+  L.W = std::max<uint32_t>(32, (kWinElems / L.k) & ~31u);
+  // the scatter kernel stages 6 bytes per window transition + 12 per range in smem
+  while (L.W > 32 && (uint64_t)L.R * 12 + 4 + (uint64_t)L.W * L.k * 6 > (227u << 10))
+    L.W = std::max<uint32_t>(32, (L.W / 2) & ~31u);
+  L.E = L.W * L.k;
+  L.nW = (uint32_t)ceil_div(L.n, L.W);
+  const uint64_t cells = (uint64_t)L.R * L.nW;
+  L.tgt = ctx.slot_t<uint16_t>("ly.tgt", L.T);
+  L.lsf = ctx.slot_t<uint16_t>("ly.lsf", (uint64_t)L.nW * L.E);
+  L.eidx = ctx.slot_t<uint32_t>("ly.eidx", (uint64_t)L.nW * L.E);
+  L.off = ctx.slot_t<uint32_t>("ly.off", cells + 1);
+  L.pre = ctx.slot_t<uint16_t>("ly.pre", cells);
+  L.wstart = ctx.slot_t<uint32_t>("ly.wstart", L.nW + 1);
+  L.v = ctx.slot("ly.v", L.T * 4);
+  uint32_t* cnt_w = ctx.slot_t<uint32_t>("ly.cntw", cells);
+  uint32_t* cnt_j = ctx.slot_t<uint32_t>("ly.cntj", cells);
+  // delta read twice + tgt/lsf writes + the count/offset matrices
+  ProfScope ps(ctx, "layout", L.T * (4ull + 4 + 2 + 2 + 4) + cells * (4ull * 4 + 2 * 2));
+  const unsigned grid = (unsigned)std::min<uint64_t>(L.nW, (uint64_t)ctx.num_sms * 4);
+  lay_count_kernel<<<grid, 512, L.R * 4, ctx.stream>>>(d.delta, L, cnt_w);
+  DFM_LAUNCH_CHECK();
+  lay_transpose_kernel<<<dim3((unsigned)ceil_div(L.R, 32), (unsigned)ceil_div(L.nW, 32)),
+                         dim3(32, 8), 0, ctx.stream>>>(cnt_w, cnt_j, L.nW, L.R);
+  DFM_LAUNCH_CHECK();
+  prims::lookback_scan(ctx, "sc.lyoff", cells, LayOffIn{cnt_j}, LayOffOut{L.off, cells}, nullptr);
+  const size_t smem = (size_t)L.R * 12 + 4 + (size_t)L.E * 6;
+  DFM_CUDA(cudaFuncSetAttribute(lay_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  lay_scatter_kernel<<<(unsigned)std::min<uint64_t>(L.nW, (uint64_t)ctx.num_sms * 2), 1024, smem,
+                       ctx.stream>>>(d.delta, L);
+  DFM_LAUNCH_CHECK();
+}
+
+template <int kIdBits>
+void launch_layout_gather(Ctx& ctx, const Layout& L, const uint32_t* ids) {
+  // ranges per CTA: the slice fills <= 192 KB, but keep >= 2 CTAs per SM busy
+  const uint32_t cmax = std::max<uint32_t>(1, (uint32_t)((uint64_t)kSliceBytes * 8 / ((uint64_t)kRs * kIdBits)));
+  const uint32_t c = std::max<uint32_t>(1, std::min<uint32_t>(cmax, L.R / (2 * ctx.num_sms)));
+  const size_t smem = (size_t)c * kRs * kIdBits / 8 + 16;
+  DFM_CUDA(cudaFuncSetAttribute(lay_gather_kernel<kIdBits>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lay_gather_kernel<kIdBits><<<(unsigned)ceil_div(L.R, c), 1024, smem, ctx.stream>>>(L, ids, c);
+  DFM_LAUNCH_CHECK();
+}
+
+template <int kIdBits, int kK>
+void launch_layout_sig(Ctx& ctx, const SigParams& sp, bool hashed) {
+  using V = typename IdT<kIdBits>::type;
+  const size_t smem = (size_t)sp.L.E * sizeof(V);
+  auto go = [&](auto kern) {
+    DFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<sp.L.nW, 1024, smem, ctx.stream>>>(sp);
+    DFM_LAUNCH_CHECK();
+  };
+  if (hashed) go(lay_sig_kernel<kIdBits, kK, true>);
+  else go(lay_sig_kernel<kIdBits, kK, false>);
+}
+
+template <int kIdBits>
+void layout_keys_bits(Ctx& ctx, const Layout& L, const uint32_t* ids, const SigParams& sp,
+                      bool hashed) {
+  launch_layout_gather<kIdBits>(ctx, L, ids);
+  switch (L.k) {
+    case 2: return launch_layout_sig<kIdBits, 2>(ctx, sp, hashed);
+    case 4: return launch_layout_sig<kIdBits, 4>(ctx, sp, hashed);
+    default: return launch_layout_sig<kIdBits, 0>(ctx, sp, hashed);
+  }
+}
+
+// one pass of the blocked builder: keys[i] (+ signature rows) for the active states
+void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const uint32_t* act,
+                 uint64_t m, const uint32_t* block, int w, bool hashed, uint64_t seed,
+                 unsigned long long* keys, uint32_t* sig, uint32_t row, uint32_t* vals,
+                 const uint8_t* lead) {
+  if (act) {
+    ProfScope ps(ctx, "scan", m * 4 + L.nW * 4ull);
+    lay_wstart_kernel<<<grid_for(ctx, m + 1), 256, 0, ctx.stream>>>(act, m, L.W, L.nW, L.wstart);
+    DFM_LAUNCH_CHECK();
+  }
+  const uint64_t idb = (uint64_t)std::max(8, mirror_bits) / 8;
+  SigParams sp{L,   act ? L.wstart : nullptr, act, block, w, seed, keys, hashed ? sig : nullptr,
+               row, vals, lead};
+  // per transition: tgt 2 + id write + lsf 2 + eidx 4 + id read; id slices once; per active
+  // state: act 4 + own id 4 + key 8 (+ signature row)
+  ProfScope ps(ctx, "sig", L.T * (8 + 2 * idb) + L.n * (uint64_t)mirror_bits / 8 +
+                               m * (4ull + 4 + 8 + (vals ? 5 : 0) + (hashed ? 4ull * row : 0)));
+  const uint32_t* ids32 = static_cast<const uint32_t*>(ids);
+  switch (mirror_bits) {
+    case 1: return layout_keys_bits<1>(ctx, L, ids32, sp, hashed);
+    case 4: return layout_keys_bits<4>(ctx, L, ids32, sp, hashed);
+    case 8: return layout_keys_bits<8>(ctx, L, ids32, sp, hashed);
+    case 16: return layout_keys_bits<16>(ctx, L, ids32, sp, hashed);
+    default: return layout_keys_bits<32>(ctx, L, ids32, sp, hashed);
+  }
+}
+// partitioned grouping of one pass (sortpr_group.cuh); keys/vals from layout_keys
+void group_partitioned(Ctx& ctx, uint64_t m, const uint32_t* act, unsigned long long* keys,
+                       uint32_t* vals, const uint32_t* sig, uint32_t words, uint32_t row,
+                       uint32_t B, uint32_t* block, uint8_t* flag, uint8_t* lead, uint64_t* sc) {
+  auto* k2 = ctx.slot_t<uint64_t>("gp.k2", m);
+  auto* v2 = ctx.slot_t<uint32_t>("gp.v2", m);
+  auto* ok = ctx.slot_t<uint64_t>("gp.ok", m);
+  auto* ov = ctx.slot_t<uint32_t>("gp.ov", m);
+  auto* res = ctx.slot_t<unsigned long long>("gp.res", m);
+  const uint32_t nb = 1u << kGroupBits;
+  uint32_t* bstart = ctx.slot_t<uint32_t>("gp.bstart", nb + 1);
+  uint64_t* Hs = reinterpret_cast<uint64_t*>(keys);
+  uint32_t* Vs = vals;
+  {
+    ProfScope ps(ctx, "group", m * (8ull + 8));  // bucket bounds: one read of the sorted keys
+    if (prims::radix_sort_pairs_bits(ctx, Hs, Vs, k2, v2, m, 0, kGroupBits, false)) {
+      Hs = k2;
+      Vs = v2;
+    }
+    grp_bounds_kernel<<<grid_for(ctx, m + 1), 256, 0, ctx.stream>>>(Hs, m, nb, bstart);
+    DFM_LAUNCH_CHECK();
+  }
+  {
+    // per item: key 8 + val 4 read, record 8 + 4 written (+ signature rows when hashed)
+    ProfScope ps(ctx, "group", m * (24ull + (sig ? 8ull * words : 0)));
+    GroupParams gp{Hs, Vs, bstart, nb, reinterpret_cast<unsigned long long*>(ok), ov,
+                   reinterpret_cast<unsigned long long*>(sc + 1),
+                   reinterpret_cast<unsigned long long*>(sc + 2), sig, words, row, B};
+    const size_t smem = (size_t)kGroupTable * (sizeof(GSlot) + 4);
+    static bool attr = false;
+    if (!attr) {
+      DFM_CUDA(cudaFuncSetAttribute(grp_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      attr = true;
+    }
+    grp_group_kernel<<<nb, 512, smem, ctx.stream>>>(gp);
+    DFM_LAUNCH_CHECK();
+  }
+  // back to i order: one radix pass by the top 8 bits of i, then an L2-local placement
+  const int ib = std::max(1, 64 - __builtin_clzll(std::max<uint64_t>(m - 1, 1)));
+  uint64_t* rk = ok;
+  uint32_t* rv = ov;
+  if (prims::radix_sort_pairs_bits(ctx, ok, ov, k2, v2, m, 32 + std::max(0, ib - 8), 8, false)) {
+    rk = k2;
+    rv = v2;
+  }
+  {
+    ProfScope ps(ctx, "relabel", m * (12ull + 8));
+    grp_place_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+        reinterpret_cast<const unsigned long long*>(rk), rv, m, res);
+    DFM_LAUNCH_CHECK();
+  }
+  {
+    ProfScope ps(ctx, "relabel", m * (8ull + 4 + 4 + 1 + 1));
+    grp_apply_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+        m, act, res, block, flag, lead, reinterpret_cast<const unsigned long long*>(sc + 2));
+    DFM_LAUNCH_CHECK();
+  }
+}
+
 }  // namespace
 
 AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {
@@ -580,7 +772,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint32_t* res = ctx.slot_t<uint32_t>("sh.res", n);
   uint8_t* st = ctx.slot_t<uint8_t>("sh.st", n);
   uint32_t* sig = nullptr;
-  const uint32_t row = (k + 1 + 7) & ~7u;  // signature rows padded to 32-byte sectors
+  // signature rows packed back to back: a warp's consecutive rows cover whole sectors
+  const uint32_t row = k + 1;
   uint64_t* sc = ctx.d_scalars;  // [1] fresh [2] collision [3] next active [4] accepting
   uint32_t* first2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
   DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
@@ -615,6 +808,10 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     DFM_LAUNCH_CHECK();
   };
   build_mirror(B);
+  Layout lay;
+  bool lay_built = false;
+  bool force_global = false;
+  const bool lay_ok = layout_possible(n, k);
   const uint32_t* act = nullptr;  // identity at pass 1
   int act_sel = 0;
   uint64_t m = n;
@@ -636,16 +833,47 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
     uint32_t* act_next = act_buf[act_sel ^ 1];
     if (m > 0) {
-      Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", table * sizeof(Slot)));
-      DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
       const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
       unsigned long long* keys = nullptr;
       if (packed && (mirror_bits == 8 || mirror_bits == 16))
         keys = ctx.slot_t<unsigned long long>("sh.keys", m);
+      // blocked signature builder whenever most states are active (it streams all n*k
+      // transitions); sparse late passes gather directly
+      const bool blocked = lay_ok && m >= n / 4;
+      // partitioned grouping for the large passes (not the tiny direct tables)
+      const bool part = blocked && !force_global && !(direct && table <= kSmallTable) &&
+                        m >= kPartMinStates && m < (1ull << 31);
+      force_global = false;
+      if (blocked) {
+        if (!lay_built) {
+          build_layout(ctx, d, lay);
+          lay_built = true;
+        }
+        keys = ctx.slot_t<unsigned long long>("sh.keys", m);
+        uint32_t* vals = part ? ctx.slot_t<uint32_t>("gp.v", m) : nullptr;
+        layout_keys(ctx, lay, mirror_bits, ids, act, m, block, w, !packed, seed, keys, sig, row,
+                    vals, lead);
+        if (part) {
+          group_partitioned(ctx, m, act, keys, vals, packed ? nullptr : sig, k + 1, row, B, block,
+                            flag, lead, sc);
+          ProfScope p(ctx, "scan", m * 9ull);
+          prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+        }
+      }
+      if (!part) {
+      Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", table * sizeof(Slot)));
+      DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
       InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table, slots,
                       slot_of, packed ? nullptr : sig, row, keys};
-      {
+      if (blocked) {
+        ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
+        switch (k) {
+          case 2: launch_insert_keys<2>(ctx, ip, !packed, direct, table); break;
+          case 4: launch_insert_keys<4>(ctx, ip, !packed, direct, table); break;
+          default: launch_insert_keys<0>(ctx, ip, !packed, direct, table); break;
+        }
+      } else {
         // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
         // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
         ProfScope p(ctx, "sig",
@@ -677,9 +905,14 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         ProfScope p(ctx, "scan", m * 9ull);
         prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
       }
+      }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 24, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
+    if (ctx.h_scalars[2] & kFlagOverflow) {  // partitioned grouping overflowed a bucket:
+      force_global = true;                    // redo the pass with the global table
+      continue;
+    }
     if (ctx.h_scalars[2] != 0) {  // hash collision: redo the pass under a new seed
       seed = seed * kGolden + 0x632BE59BD9B4E019ull;
       continue;

@@ -279,3 +279,38 @@ def test_full_size_properties(eng, eng_radix):
     rq = eng.sort_pr(quot)
     assert rq.partition.num_blocks == nb  # quotient is minimal
     dd.free()
+
+
+def _device_labels(e, dd, n):
+    import torch
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    nb, st = e.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
+    assert st.status == dfm.RunStatus.ok
+    return nb, st.iterations, out
+
+
+@pytest.mark.parametrize("n,k,seed", [(12_000_000, 4, 3), (30_000_000, 2, 4),
+                                      (12_000_000, 3, 5), (7_000_000, 9, 6)])
+def test_blocked_signature_builder(eng, eng_radix, monkeypatch, n, k, seed):
+    """The blocked (target-range bucketed) signature builder takes over the
+    passes whose id mirror exceeds the L2 share; it must give the exact same
+    canonical partition and pass count as the direct-gather path and the radix
+    engine (both pinned against the oracle at smaller sizes)."""
+    dd = eng.random_dfa_device(n, k, seed, 0.5)
+    nb, it, lab = _device_labels(eng, dd, n)
+    monkeypatch.setenv("DFM_SORTPR_BLOCKED", "0")
+    nb0, it0, lab0 = _device_labels(eng, dd, n)
+    monkeypatch.delenv("DFM_SORTPR_BLOCKED")
+    nbr, itr, labr = _device_labels(eng_radix, dd, n)
+    assert (nb, it) == (nb0, it0) == (nbr, itr)
+    assert bool((lab == lab0).all()) and bool((lab == labr).all())
+    dd.free()
+
+
+def test_blocked_builder_vs_oracle(eng):
+    """One blocked-path size checked straight against the CPU oracle."""
+    pair = O.random_dfa(17_000_000, 2, 11, 0.5)
+    ref = O.sort_pr(*pair)
+    r = eng.sort_pr(to_dfa(pair))
+    assert r.stats.iterations == ref.iterations
+    assert (r.partition.block == ref.block).all()
