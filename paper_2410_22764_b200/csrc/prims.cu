@@ -46,10 +46,12 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
   uint32_t* s_start = s_cnt + kRsWarps * 256;  // tile-local digit start
   uint32_t* s_glob = s_start + 256;            // global destination base per digit
   uint32_t* s_misc = s_glob + 256;             // [0] tile id, [1..9] warp sums
+  uint32_t* s_hist = s_misc + 16;              // tile digit histogram (published early)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_misc[0] = atomicAdd(ticket, 1u);
   for (int i = tid; i < kRsWarps * 256; i += kRsThreads) s_cnt[i] = 0;
+  s_hist[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_misc[0];
   const uint64_t tile_base = (uint64_t)tile * kRsTile;
@@ -68,6 +70,14 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
     else v[j] = valid ? vals_in[idx] : 0u;
     dig[j] = valid ? (uint32_t)((k[j] >> shift) & 255) : 256u;
   }
+  // the tile's digit counts go out before the ranking, so successors' look-backs
+  // rarely wait on this tile
+#pragma unroll
+  for (int j = 0; j < kRsItems; ++j)
+    if (dig[j] < 256) atomicAdd(&s_hist[dig[j]], 1u);
+  __syncthreads();
+  if (tile == 0) st_volatile(status + tid, kFlagInc | s_hist[tid]);
+  else st_volatile(status + (uint64_t)tile * 256 + tid, kFlagAgg | s_hist[tid]);
   uint32_t* my_cnt = s_cnt + warp * 256;
 #pragma unroll
   for (int j = 0; j < kRsItems; ++j) {
@@ -94,8 +104,6 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
       run += c;
     }
     total = run;
-    uint64_t* my_status = status + (uint64_t)tile * 256 + d;
-    st_volatile(my_status, (tile == 0 ? kFlagInc : kFlagAgg) | total);
   }
   uint32_t tile_total;
   const uint32_t start = block_exclusive_sum<kRsThreads>(total, s_misc + 1, &tile_total);

@@ -170,7 +170,7 @@ constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsItems = 8;
 constexpr int kRsTile = kRsThreads * kRsItems;  // 4096
-constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 64;
+constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 64 + 1024;
 
 // Sorts (keys, vals) of length count on the low `bits` bits.  ident_vals: the
 // input values are 0..count-1 and `vals` is not read.  Uses alt_keys/alt_vals

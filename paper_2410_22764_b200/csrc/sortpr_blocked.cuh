@@ -62,21 +62,21 @@ __global__ void __launch_bounds__(512) lay_count_kernel(const uint32_t* __restri
     __syncthreads();
     const uint64_t q0 = (uint64_t)w * L.W;
     const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
-    // 8 independent delta loads in flight per thread
-    for (uint32_t a = 0; a < L.k; ++a)
-      for (uint32_t x0 = 0; x0 < wn; x0 += 8 * blockDim.x) {
-        uint32_t t[8];
+    // the window's k x wn transitions as one flat range (rows of wn coalesced
+    // states), 8 independent delta loads in flight per thread
+    const uint32_t ew = wn * L.k;
+    for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
+      uint32_t t[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
-          t[u] = x < wn ? ld_stream(delta + a * L.n + q0 + x, pol) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
-          if (x < wn) atomicAdd(&s_h[t[u] / kRs], 1u);
-        }
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+        const uint32_t a = e / wn;
+        t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * blockDim.x + threadIdx.x < ew) atomicAdd(&s_h[t[u] / kRs], 1u);
+    }
     __syncthreads();
     // counts (w-major, transposed later for the bucket scan) + in-window prefix
     constexpr uint32_t kPer = kMaxRanges / 512;
@@ -155,26 +155,27 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
     }
     if (threadIdx.x == 0) s_pre[L.R] = ew;
     __syncthreads();
-    for (uint32_t a = 0; a < L.k; ++a)
-      for (uint32_t x0 = 0; x0 < wn; x0 += 8 * blockDim.x) {
-        uint32_t t[8];
+    for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
+      uint32_t t[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
-          t[u] = x < wn ? ld_stream(delta + a * L.n + q0 + x, pol) : 0u;
-        }
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+        const uint32_t a = e / wn;
+        t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t x = x0 + u * blockDim.x + threadIdx.x;
-          if (x < wn) {
-            const uint32_t j = t[u] / kRs;
-            const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
-            s_tgt[f] = (uint16_t)(t[u] - j * kRs);
-            s_lsf[f] = (uint16_t)(a * L.W + x);
-            s_j[f] = (uint16_t)j;
-          }
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+        if (e < ew) {
+          const uint32_t a = e / wn, x = e - a * wn;
+          const uint32_t j = t[u] / kRs;
+          const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
+          s_tgt[f] = (uint16_t)(t[u] - j * kRs);
+          s_lsf[f] = (uint16_t)(a * L.W + x);
+          s_j[f] = (uint16_t)j;
         }
       }
+    }
     __syncthreads();
     const uint64_t fb = (uint64_t)w * L.E;
     for (uint32_t f = threadIdx.x; f < ew; f += blockDim.x) {

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(512) grp_group_kernel(GroupParams p) {
       continue;
     }
     uint32_t tsize = 64;
-    while (tsize < kGroupTable && tsize < cnt + cnt / 2) tsize <<= 1;
+    while (tsize < kGroupTable && tsize < cnt + cnt / 4) tsize <<= 1;
     for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x) {
       s_t[s].key = 0;
       s_t[s].rep = 0xFFFFFFFFu;
@@ -114,17 +114,15 @@ __global__ void __launch_bounds__(512) grp_group_kernel(GroupParams p) {
       if (threadIdx.x == 0) atomicOr(p.flags, kFlagOverflow);
       continue;
     }
-    // fresh ids for the groups without the old leader: one atomic per bucket
-    const uint32_t per = (tsize + blockDim.x - 1) / blockDim.x;
-    const uint32_t s0 = threadIdx.x * per;
+    // fresh ids for the groups without the old leader: one global atomic per bucket
     uint32_t mine = 0;
-    for (uint32_t s = s0; s < s0 + per && s < tsize; ++s)
+    for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x)
       mine += (s_t[s].key != 0 && (s_t[s].info >> 31) == 0) ? 1u : 0u;
     uint32_t total;
     uint32_t run = prims::block_exclusive_sum<512>(mine, s_warp, &total);
     if (threadIdx.x == 0) s_base = total ? (uint32_t)atomicAdd(p.fresh, (unsigned long long)total) : 0u;
     __syncthreads();
-    for (uint32_t s = s0; s < s0 + per && s < tsize; ++s)
+    for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x)
       if (s_t[s].key != 0 && (s_t[s].info >> 31) == 0) s_gid[s] = p.B + s_base + run++;
     __syncthreads();
     bool collision = false;

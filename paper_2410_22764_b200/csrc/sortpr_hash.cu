@@ -511,6 +511,8 @@ __global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
 
 constexpr uint64_t kBlockedMinTransitions = 1ull << 25;
 constexpr uint64_t kPartMinStates = 1ull << 20;
+// below this the gathered id mirror stays in L2 and direct gathers win
+constexpr uint64_t kBlockedMinMirror = 32ull << 20;
 
 #include "sortpr_blocked.cuh"
 #include "sortpr_group.cuh"
@@ -581,6 +583,13 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   else
     insert_kernel<32, false, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
   DFM_LAUNCH_CHECK();
+}
+
+// partitioned grouping (sortpr_group.cuh) is opt-in until its radix passes beat the
+// global table: DFM_SORTPR_PARTITION=1
+bool partition_enabled() {
+  const char* e = getenv("DFM_SORTPR_PARTITION");
+  return e != nullptr && e[0] == '1';
 }
 
 bool blocked_disabled() {
@@ -743,7 +752,10 @@ void group_partitioned(Ctx& ctx, uint64_t m, const uint32_t* act, unsigned long 
   }
   {
     ProfScope ps(ctx, "relabel", m * (12ull + 8));
-    grp_place_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+    // resident CTAs only: the grid sweeps the i windows together, so the window being
+    // placed stays in L2 and its sectors leave complete
+    grp_place_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(m, 256), ctx.num_sms * 8ull), 256, 0,
+                       ctx.stream>>>(
         reinterpret_cast<const unsigned long long*>(rk), rv, m, res);
     DFM_LAUNCH_CHECK();
   }
@@ -811,6 +823,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   Layout lay;
   bool lay_built = false;
   bool force_global = false;
+  const bool part_on = partition_enabled();
   const bool lay_ok = layout_possible(n, k);
   const uint32_t* act = nullptr;  // identity at pass 1
   int act_sel = 0;
@@ -840,9 +853,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         keys = ctx.slot_t<unsigned long long>("sh.keys", m);
       // blocked signature builder whenever most states are active (it streams all n*k
       // transitions); sparse late passes gather directly
-      const bool blocked = lay_ok && m >= n / 4;
+      const bool blocked = lay_ok && m >= n / 4 && n * (uint64_t)mirror_bits / 8 > kBlockedMinMirror;
       // partitioned grouping for the large passes (not the tiny direct tables)
-      const bool part = blocked && !force_global && !(direct && table <= kSmallTable) &&
+      const bool part = blocked && part_on && !force_global && !(direct && table <= kSmallTable) &&
                         m >= kPartMinStates && m < (1ull << 31);
       force_global = false;
       if (blocked) {

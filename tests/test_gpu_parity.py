@@ -290,7 +290,7 @@ def _device_labels(e, dd, n):
 
 
 @pytest.mark.parametrize("n,k,seed", [(12_000_000, 4, 3), (30_000_000, 2, 4),
-                                      (12_000_000, 3, 5), (7_000_000, 9, 6)])
+                                      (12_000_000, 3, 5), (9_000_000, 9, 6)])
 def test_blocked_signature_builder(eng, eng_radix, monkeypatch, n, k, seed):
     """The blocked (target-range bucketed) signature builder takes over the
     passes whose id mirror exceeds the L2 share; it must give the exact same
@@ -314,3 +314,14 @@ def test_blocked_builder_vs_oracle(eng):
     r = eng.sort_pr(to_dfa(pair))
     assert r.stats.iterations == ref.iterations
     assert (r.partition.block == ref.block).all()
+
+
+@pytest.mark.parametrize("n,k,seed", [(12_000_000, 4, 3), (9_000_000, 12, 8)])
+def test_partitioned_grouping(eng, monkeypatch, n, k, seed):
+    """The opt-in partitioned shared-memory grouping gives the global-table result."""
+    dd = eng.random_dfa_device(n, k, seed, 0.5)
+    nb, it, lab = _device_labels(eng, dd, n)
+    monkeypatch.setenv("DFM_SORTPR_PARTITION", "1")
+    nb1, it1, lab1 = _device_labels(eng, dd, n)
+    assert (nb, it) == (nb1, it1) and bool((lab == lab1).all())
+    dd.free()
