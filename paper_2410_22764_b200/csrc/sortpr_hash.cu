@@ -185,7 +185,10 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
 }
 
 // K1, hash or large direct table; warp-level aggregation of equal slots
-template <int kIdBits, bool kHashed, bool kDirect, int kK, bool kFromKeys = false>
+constexpr uint32_t kUnique = 0xFFFFFFFFu;  // slot_of mark: key seen once (filtered)
+
+template <int kIdBits, bool kHashed, bool kDirect, int kK, bool kFromKeys = false,
+          bool kFilter = false>
 __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_ids = policy_evict_last();
@@ -204,13 +207,14 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const uint64_t i = base + u * 32 + lane;
-      valid[u] = i < p.m;
+      // filtered passes: states whose key the filter saw once are singleton groups
+      valid[u] = i < p.m && (!kFilter || p.slot_of[i] != kUnique);
       if (valid[u]) {
         const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
-        const uint32_t b = p.block[q];
         lead[u] = p.lead[q];
         key[u] = kFromKeys ? p.keys[i]
-                           : make_key<kIdBits, kHashed, kK>(p, i, q, b, pol_stream, pol_ids);
+                           : make_key<kIdBits, kHashed, kK>(p, i, q, p.block[q], pol_stream,
+                                                             pol_ids);
       }
     }
 #pragma unroll
@@ -337,6 +341,67 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
   }
 }
 
+// Uniqueness filter for hash-table passes (most keys distinct, e.g. the last
+// refinement passes of random DFAs): 2 bits per cell over 2^28 cells = 64 MB, an
+// L2-resident footprint (tools/l2_bench.cu: ~190 G atomics/s vs ~21-25 G/s for
+// a > L2 table).  Keys alone in their cell are singleton groups and skip the
+// global table; only the rest (true duplicates + cell collisions) is inserted.
+constexpr int kFilterCellBits = 28;
+
+__device__ __forceinline__ unsigned long long table_hash(unsigned long long key, bool hashed,
+                                                         uint64_t seed) {
+  return hashed ? key : mix64(key ^ seed);
+}
+
+// keys stream through L2 with evict_first so the 64 MB filter stays resident
+__device__ __forceinline__ unsigned long long ld_key_stream(const unsigned long long* a,
+                                                            uint64_t pol) {
+  unsigned long long v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t atom_or_keep(uint32_t* a, uint32_t v, uint64_t pol) {
+  uint32_t old;
+  asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
+               : "=r"(old) : "l"(a), "r"(v), "l"(pol) : "memory");
+  return old;
+}
+
+__global__ void __launch_bounds__(256) filt_set_kernel(const unsigned long long* __restrict__ keys,
+                                                       uint64_t m, bool hashed, uint64_t seed,
+                                                       uint32_t* F) {
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint64_t c = table_hash(ld_key_stream(keys + i, pol_stream), hashed, seed) >>
+                       (64 - kFilterCellBits);
+    const uint32_t b = (uint32_t)(c & 15) * 2;
+    const uint32_t old = atom_or_keep(&F[c >> 4], 1u << b, pol_keep);
+    if ((old >> b) & 1u) atom_or_keep(&F[c >> 4], 2u << b, pol_keep);
+  }
+}
+
+__global__ void __launch_bounds__(256) filt_mark_kernel(const unsigned long long* __restrict__ keys,
+                                                        uint64_t m, bool hashed, uint64_t seed,
+                                                        const uint32_t* __restrict__ F,
+                                                        uint32_t* __restrict__ slot_of,
+                                                        unsigned long long* dups) {
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t mine = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint64_t c = table_hash(ld_key_stream(keys + i, pol_stream), hashed, seed) >>
+                       (64 - kFilterCellBits);
+    const bool dup = (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
+    slot_of[i] = dup ? 0u : kUnique;
+    mine += dup ? 1u : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(dups, (unsigned long long)mine);
+}
+
 struct ResolveItem {
   uint32_t v;      // 1 = minimum member of a group that gets a fresh id
   uint32_t slot;
@@ -349,8 +414,18 @@ struct ResolveIn {
   const uint32_t* sig;  // nullptr: exact packed keys
   uint32_t words, row;
   unsigned long long* collision;
+  const uint32_t* act;  // filtered passes: kUnique states are singleton groups
+  const uint8_t* lead;
   __device__ ResolveItem operator()(uint64_t i) const {
     const uint32_t s = slot_of[i];
+    if (s == kUnique) {
+      const bool keeper = lead[act ? act[i] : (uint32_t)i] != 0;
+      ResolveItem it;
+      it.v = keeper ? 0u : 1u;
+      it.slot = s;
+      it.flags = 1u | 2u | (keeper ? 4u : 0u);
+      return it;
+    }
     const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
     const uint32_t rep_i = ~sl.x;
     const uint32_t cnt = sl.y & 0x7FFFFFFFu;
@@ -511,6 +586,7 @@ __global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n) {
 
 constexpr uint64_t kBlockedMinTransitions = 1ull << 25;
 constexpr uint64_t kPartMinStates = 1ull << 20;
+constexpr uint64_t kFilterMinStates = 1ull << 22;
 // below this the gathered id mirror stays in L2 and direct gathers win
 constexpr uint64_t kBlockedMinMirror = 32ull << 20;
 
@@ -571,9 +647,13 @@ void launch_insert(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, ui
 
 // K1 from precomputed keys (blocked builder): packed or hashed, direct or probed
 template <int kK>
-void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table) {
+void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direct, uint64_t table,
+                        bool filtered) {
   const unsigned grid = grid_for(ctx, p.m);
-  if (direct && table <= kSmallTable)
+  if (filtered) {
+    if (hashed) insert_kernel<32, true, false, kK, true, true><<<grid, 256, 0, ctx.stream>>>(p);
+    else insert_kernel<32, false, false, kK, true, true><<<grid, 256, 0, ctx.stream>>>(p);
+  } else if (direct && table <= kSmallTable)
     insert_small_kernel<32, kK, true><<<std::min<unsigned>(grid, ctx.num_sms * 8), 256,
                                         2 * table * sizeof(uint32_t), ctx.stream>>>(p, (uint32_t)table);
   else if (hashed)
@@ -841,8 +921,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     const bool packed = kbits <= 63;
     // direct-indexed table (slot = key, no probing) when the key space is small
     const bool direct = packed && kbits <= 30 && (1ull << kbits) <= std::max<uint64_t>(2 * m, 4096);
-    // hash tables: load factor <= 2/3 (capacity need not be a power of two)
-    const uint64_t table = direct ? (1ull << kbits) : std::max<uint64_t>(1024, m + m / 2);
+    // hash tables: load <= 0.4 (a warp waits for its longest probe chain)
+    const uint64_t table = direct ? (1ull << kbits) : std::max<uint64_t>(1024, m * 5 / 2);
     DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
     uint32_t* act_next = act_buf[act_sel ^ 1];
     if (m > 0) {
@@ -875,16 +955,35 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         }
       }
       if (!part) {
-      Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", table * sizeof(Slot)));
-      DFM_CUDA(cudaMemsetAsync(slots, 0, table * sizeof(Slot), ctx.stream));
-      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, table, slots,
+      // uniqueness filter in front of large hash tables (keys are precomputed)
+      const bool filtered = blocked && !direct && m >= kFilterMinStates;
+      uint64_t cap = table;
+      if (filtered) {
+        uint32_t* F = ctx.slot_t<uint32_t>("sh.filter", 1ull << (kFilterCellBits - 4));
+        ProfScope p(ctx, "insert", (1ull << (kFilterCellBits - 2)) + m * (8ull + 8 + 4));
+        DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kFilterCellBits - 2), ctx.stream));
+        DFM_CUDA(cudaMemsetAsync(sc + 6, 0, 8, ctx.stream));
+        filt_set_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(keys, m, !packed, seed, F);
+        DFM_LAUNCH_CHECK();
+        filt_mark_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+            keys, m, !packed, seed, F, slot_of, reinterpret_cast<unsigned long long*>(sc + 6));
+        DFM_LAUNCH_CHECK();
+        DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 6, sc + 6, 8, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        const uint64_t dups = ctx.h_scalars[6];
+        // load <= 0.4: a warp waits for its longest probe chain of DRAM-latency CASes
+        cap = std::max<uint64_t>(1024, dups * 5 / 2);
+      }
+      Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", cap * sizeof(Slot)));
+      DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(Slot), ctx.stream));
+      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, cap, slots,
                       slot_of, packed ? nullptr : sig, row, keys};
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
         switch (k) {
-          case 2: launch_insert_keys<2>(ctx, ip, !packed, direct, table); break;
-          case 4: launch_insert_keys<4>(ctx, ip, !packed, direct, table); break;
-          default: launch_insert_keys<0>(ctx, ip, !packed, direct, table); break;
+          case 2: launch_insert_keys<2>(ctx, ip, !packed, direct, table, filtered); break;
+          case 4: launch_insert_keys<4>(ctx, ip, !packed, direct, table, filtered); break;
+          default: launch_insert_keys<0>(ctx, ip, !packed, direct, table, filtered); break;
         }
       } else {
         // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
@@ -905,7 +1004,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         prims::lookback_scan(
             ctx, "sc.resolve", m,
             ResolveIn{slots, slot_of, packed ? nullptr : sig, k + 1, row,
-                      reinterpret_cast<unsigned long long*>(sc + 2)},
+                      reinterpret_cast<unsigned long long*>(sc + 2), act, lead},
             ResolveOut{slots, act, block, res, st, B}, sc + 1);
       }
       {
