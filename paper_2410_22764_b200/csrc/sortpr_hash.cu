@@ -434,11 +434,14 @@ struct ResolveIn {
     if (!is_rep && sig != nullptr) {  // equal hash: verify the full signature
       const uint32_t* a = sig + i * (uint64_t)row;
       const uint32_t* b = sig + (uint64_t)rep_i * row;
-      for (uint32_t x = 0; x < words; ++x)
-        if (a[x] != b[x]) {
-          atomicOr(collision, 1ull);
-          break;
-        }
+      uint32_t diff = 0;
+      for (uint32_t x = 0; x < words; x += 4) {  // 4 independent words in flight
+#pragma unroll
+        for (uint32_t y = 0; y < 4; ++y)
+          if (x + y < words) diff |= a[x + y] ^ b[x + y];
+        if (diff) break;
+      }
+      if (diff) atomicOr(collision, 1ull);
     }
     ResolveItem it;
     it.v = (is_rep && !keeper) ? 1u : 0u;
@@ -472,6 +475,55 @@ struct ResolveOut {
     }
   }
 };
+
+// K2 without a global scan: fresh ids are handed out by one atomic per CTA step
+// (any numbering of the new blocks yields the same partition; canonical labels
+// come from the leader flags), so every state resolves independently
+constexpr int kResolveItems = 4;
+
+__global__ void __launch_bounds__(256) resolve_kernel(uint64_t m, ResolveIn in, ResolveOut out,
+                                                      unsigned long long* fresh) {
+  constexpr int U = kResolveItems;
+  __shared__ uint32_t s_cnt[8 * U];
+  __shared__ uint32_t s_first;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * U; base < m; base += stride) {
+    ResolveItem it[U];
+    uint32_t want[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = base + u * blockDim.x + threadIdx.x;
+      if (i < m) it[u] = in(i);
+      else it[u].v = 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      want[u] = __ballot_sync(0xffffffffu, it[u].v != 0);
+      if (lane == 0) s_cnt[u * 8 + warp] = __popc(want[u]);
+    }
+    __syncthreads();
+    // exclusive offsets of the (item slot, warp) groups; one atomic for the CTA step
+    if (threadIdx.x == 0) {
+      uint32_t total = 0;
+      for (int g = 0; g < 8 * U; ++g) total += s_cnt[g];
+      s_first = total ? (uint32_t)atomicAdd(fresh, (unsigned long long)total) : 0u;
+    }
+    __syncthreads();
+    uint32_t off = s_first;
+    for (int g = 0; g < (int)warp; ++g) off += s_cnt[g];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = base + u * blockDim.x + threadIdx.x;
+      if (i < m) out(i, off + (uint32_t)__popc(want[u] & ((1u << lane) - 1u)), it[u]);
+      // advance past this slot's remaining warps and the next slot's earlier warps
+      for (int g = (int)warp; g < 8; ++g) off += s_cnt[u * 8 + g];
+      if (u + 1 < U)
+        for (int g = 0; g < (int)warp; ++g) off += s_cnt[(u + 1) * 8 + g];
+    }
+    __syncthreads();
+  }
+}
 
 __global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* __restrict__ act,
                                                     const uint32_t* __restrict__ res,
@@ -1001,11 +1053,12 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       }
       {
         ProfScope p(ctx, "scan", m * (4ull + 16 + 4 + 4 + 1));  // slot_of, slot, own id, res, st
-        prims::lookback_scan(
-            ctx, "sc.resolve", m,
+        resolve_kernel<<<grid_for(ctx, ceil_div(m, kResolveItems)), 256, 0, ctx.stream>>>(
+            m,
             ResolveIn{slots, slot_of, packed ? nullptr : sig, k + 1, row,
                       reinterpret_cast<unsigned long long*>(sc + 2), act, lead},
-            ResolveOut{slots, act, block, res, st, B}, sc + 1);
+            ResolveOut{slots, act, block, res, st, B}, reinterpret_cast<unsigned long long*>(sc + 1));
+        DFM_LAUNCH_CHECK();
       }
       {
         ProfScope p(ctx, "relabel", m * (1ull + 4 + 4 + 4 + 1 + 1));
