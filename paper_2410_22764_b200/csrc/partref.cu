@@ -14,6 +14,7 @@
 // fixpoint is a no-op, so the host reads the per-pass "changed" flags once
 // per batch and the iteration count is the first unchanged pass.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -55,15 +56,79 @@ __global__ void init_leaders_kernel(const uint8_t* __restrict__ acc, uint64_t n,
 
 // split condition (min_partref.hpp:90-99): some letter's successor lies in a
 // different pass-entry block than the leader's successor on that letter
+// (letters in groups of 4: the 8 successor loads, then the 8 label loads, are in
+// flight together — two dependent round trips per group instead of two per letter)
 __device__ __forceinline__ bool splits(const uint32_t* __restrict__ rows, uint64_t n,
                                        uint64_t letters, const uint32_t* __restrict__ cur,
                                        uint32_t q, uint32_t leader) {
   if (q == leader) return false;
-  for (uint64_t a = 0; a < letters; ++a) {
-    const uint32_t* row = rows + a * n;
-    if (cur[row[q]] != cur[row[leader]]) return true;
+  for (uint64_t a0 = 0; a0 < letters; a0 += 4) {
+    uint32_t tq[4], tl[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a0 + u < letters) {
+        tq[u] = rows[(a0 + u) * n + q];
+        tl[u] = rows[(a0 + u) * n + leader];
+      }
+    bool diff = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a0 + u < letters) diff |= cur[tq[u]] != cur[tl[u]];
+    if (diff) return true;
   }
   return false;
+}
+
+// Warp-aggregated election.  In early passes a few huge blocks receive tens of
+// thousands of candidates each, and same-address atomics serialise at one L2
+// slice; lanes of a warp hold consecutive states, so among a warp's splitting
+// lanes with the same leader only the policy's candidate touches the cell —
+// the lowest q for min / arbitrary / CAS, the highest for max.  The cell value
+// is the one the per-state atomics would leave.
+template <int kPolicy>
+__device__ __forceinline__ void elect_cell(unsigned long long* cells, uint32_t leader, uint32_t q,
+                                           uint32_t pass, bool sp, uint32_t vmask) {
+  const uint32_t spm = __ballot_sync(vmask, sp);
+  if (!sp) return;
+  const uint32_t peers = __match_any_sync(spm, leader);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t src = kPolicy == DFM_POLICY_MAX ? 31 - __clz(peers) : __ffs(peers) - 1;
+  if (lane != src) return;
+  if (kPolicy == DFM_POLICY_MIN)
+    atomicMin(&cells[leader], ((unsigned long long)(~pass) << 32) | q);
+  else if (kPolicy == DFM_POLICY_MAX)
+    atomicMax(&cells[leader], ((unsigned long long)pass << 32) | q);
+  else
+    *reinterpret_cast<volatile unsigned long long*>(&cells[leader]) =
+        ((unsigned long long)pass << 32) | q;
+}
+
+// fused CAS (min_partref.hpp:116-132): the group's lowest lane competes for the
+// cell; the first CAS wins and every lane of the group adopts the winner
+__device__ __forceinline__ uint32_t cas_cell(unsigned long long* cells, uint32_t leader, uint32_t q,
+                                             uint32_t pass, bool sp, uint32_t vmask) {
+  const uint32_t spm = __ballot_sync(vmask, sp);
+  if (!sp) return leader;
+  const uint32_t peers = __match_any_sync(spm, leader);
+  const uint32_t src = __ffs(peers) - 1;
+  uint32_t winner = 0;
+  if ((threadIdx.x & 31) == src) {
+    const unsigned long long mine = ((unsigned long long)pass << 32) | q;
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(&cells[leader]);
+    while (true) {
+      if ((uint32_t)(old >> 32) == pass) {
+        winner = (uint32_t)old;
+        break;
+      }
+      const unsigned long long prev = atomicCAS(&cells[leader], old, mine);
+      if (prev == old) {
+        winner = q;
+        break;
+      }
+      old = prev;
+    }
+  }
+  return __shfl_sync(peers, winner, src);
 }
 
 template <int kPolicy>
@@ -74,20 +139,16 @@ __global__ void __launch_bounds__(256) elect_kernel(const uint32_t* __restrict__
                                                     uint8_t* __restrict__ split_flag,
                                                     uint32_t pass) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t qi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; qi < n; qi += stride) {
+  for (uint64_t qb = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); qb < n;
+       qb += stride) {
+    const uint64_t qi = qb + (threadIdx.x & 31);
+    const uint32_t vmask = __ballot_sync(0xffffffffu, qi < n);
+    if (qi >= n) continue;
     const uint32_t q = (uint32_t)qi;
     const uint32_t leader = cur[q];
     const bool s = splits(rows, n, letters, cur, q, leader);
     split_flag[q] = s;
-    if (s) {
-      if (kPolicy == DFM_POLICY_MIN)
-        atomicMin(&cells[leader], ((unsigned long long)(~pass) << 32) | q);
-      else if (kPolicy == DFM_POLICY_MAX)
-        atomicMax(&cells[leader], ((unsigned long long)pass << 32) | q);
-      else
-        *reinterpret_cast<volatile unsigned long long*>(&cells[leader]) =
-            ((unsigned long long)pass << 32) | q;
-    }
+    elect_cell<kPolicy>(cells, leader, q, pass, s, vmask);
   }
 }
 
@@ -118,30 +179,16 @@ __global__ void __launch_bounds__(256) cas_kernel(const uint32_t* __restrict__ r
                                                   uint32_t* __restrict__ changed, uint32_t pass) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   bool any = false;
-  for (uint64_t qi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; qi < n; qi += stride) {
+  for (uint64_t qb = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); qb < n;
+       qb += stride) {
+    const uint64_t qi = qb + (threadIdx.x & 31);
+    const uint32_t vmask = __ballot_sync(0xffffffffu, qi < n);
+    if (qi >= n) continue;
     const uint32_t q = (uint32_t)qi;
     const uint32_t leader = cur[q];
-    if (!splits(rows, n, letters, cur, q, leader)) {
-      nxt[q] = leader;
-      continue;
-    }
-    any = true;
-    const unsigned long long mine = ((unsigned long long)pass << 32) | q;
-    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(&cells[leader]);
-    uint32_t winner;
-    while (true) {
-      if ((uint32_t)(old >> 32) == pass) {
-        winner = (uint32_t)old;
-        break;
-      }
-      const unsigned long long prev = atomicCAS(&cells[leader], old, mine);
-      if (prev == old) {
-        winner = q;
-        break;
-      }
-      old = prev;
-    }
-    nxt[q] = winner;
+    const bool sp = splits(rows, n, letters, cur, q, leader);
+    any |= sp;
+    nxt[q] = cas_cell(cells, leader, q, pass, sp, vmask);
   }
   if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *changed = 1u;
 }
@@ -163,6 +210,8 @@ __global__ void __launch_bounds__(256) double_kernel(const uint32_t* __restrict_
 // whose pass count, not per-pass work, dominates (C1: 16,474 passes on 1e5
 // states; rings and chains: n-1 passes).  Same per-pass semantics as
 // elect/split/cas_kernel above.
+constexpr int kPersistThreads = 1024;
+
 struct PersistentArgs {
   const uint32_t* rows;
   uint64_t n, letters;
@@ -178,9 +227,10 @@ struct PersistentArgs {
 };
 
 template <int kPolicy, bool kCas>
-__global__ void __launch_bounds__(256) persistent_kernel(PersistentArgs a) {
+__global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentArgs a) {
   cg::grid_group g = cg::this_grid();
-  const uint64_t first = g.thread_rank(), nth = g.size();
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   int sel = a.start_sel;
   uint32_t p = 0;
   bool stable = false;
@@ -188,48 +238,40 @@ __global__ void __launch_bounds__(256) persistent_kernel(PersistentArgs a) {
     const uint32_t pass = a.pass0 + p + 1;
     const uint32_t* cur = sel ? a.lab1 : a.lab0;
     uint32_t* nxt = sel ? a.lab0 : a.lab1;
+    // the previous pass's "changed" flag is read here and tested after this pass's
+    // election, off the critical path: a pass after a stable one changes nothing
+    const uint32_t prev_changed =
+        p > 0 ? *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) : 1u;
     bool any = false;
     if (kCas) {
-      for (uint64_t qi = first; qi < a.n; qi += nth) {
+      for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
+        const uint64_t qi = qb + (threadIdx.x & 31);
+        const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
+        if (qi >= a.n) continue;
         const uint32_t q = (uint32_t)qi;
         const uint32_t leader = cur[q];
-        if (!splits(a.rows, a.n, a.letters, cur, q, leader)) {
-          nxt[q] = leader;
-          continue;
-        }
-        any = true;
-        const unsigned long long mine = ((unsigned long long)pass << 32) | q;
-        unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(&a.cells[leader]);
-        uint32_t winner;
-        while (true) {
-          if ((uint32_t)(old >> 32) == pass) {
-            winner = (uint32_t)old;
-            break;
-          }
-          const unsigned long long prev = atomicCAS(&a.cells[leader], old, mine);
-          if (prev == old) {
-            winner = q;
-            break;
-          }
-          old = prev;
-        }
-        nxt[q] = winner;
+        const bool sp = splits(a.rows, a.n, a.letters, cur, q, leader);
+        any |= sp;
+        nxt[q] = cas_cell(a.cells, leader, q, pass, sp, vmask);
+      }
+      if (prev_changed == 0u) {  // pass p was stable; this one rewrote identical labels
+        stable = true;
+        break;
       }
     } else {
-      for (uint64_t qi = first; qi < a.n; qi += nth) {
+      for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
+        const uint64_t qi = qb + (threadIdx.x & 31);
+        const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
+        if (qi >= a.n) continue;
         const uint32_t q = (uint32_t)qi;
         const uint32_t leader = cur[q];
         const bool sp = splits(a.rows, a.n, a.letters, cur, q, leader);
         a.split[q] = sp;
-        if (sp) {
-          if (kPolicy == DFM_POLICY_MIN)
-            atomicMin(&a.cells[leader], ((unsigned long long)(~pass) << 32) | q);
-          else if (kPolicy == DFM_POLICY_MAX)
-            atomicMax(&a.cells[leader], ((unsigned long long)pass << 32) | q);
-          else
-            *reinterpret_cast<volatile unsigned long long*>(&a.cells[leader]) =
-                ((unsigned long long)pass << 32) | q;
-        }
+        elect_cell<kPolicy>(a.cells, leader, q, pass, sp, vmask);
+      }
+      if (prev_changed == 0u) {  // pass p was stable; election cells are epoch-tagged
+        stable = true;
+        break;
       }
       g.sync();
       for (uint64_t qi = first; qi < a.n; qi += nth) {
@@ -246,11 +288,9 @@ __global__ void __launch_bounds__(256) persistent_kernel(PersistentArgs a) {
     g.sync();
     sel ^= 1;
     ++p;
-    if (*reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u) {
-      stable = true;
-      break;
-    }
   }
+  if (!stable && p > 0 && *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u)
+    stable = true;
   if (first == 0) {
     a.out[0] = p;
     a.out[1] = stable ? 1u : 0u;
@@ -309,9 +349,9 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
         : policy == DFM_POLICY_MAX ? persistent_kernel<DFM_POLICY_MAX, false>
                                    : persistent_kernel<DFM_POLICY_ARBITRARY, false>;
     int per_sm = 0;
-    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPersistThreads, 0));
     const unsigned pgrid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, 256)));
+        1, std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, kPersistThreads)));
     while (true) {
       if (dl.expired()) {
         out.status = DFM_STATUS_TIMEOUT;
@@ -324,7 +364,8 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       void* args[] = {&pa};
       {
         ProfScope p(ctx, "elect", 0);
-        DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, 256, args, 0, ctx.stream));
+        DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, kPersistThreads, args, 0,
+                                             ctx.stream));
         DFM_LAUNCH_CHECK();
       }
       DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, pout, 12, cudaMemcpyDeviceToHost, ctx.stream));
