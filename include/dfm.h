@@ -186,6 +186,27 @@ int dfm_run_algorithm_dev(dfm_ctx* ctx, int32_t algo, const dfm_ddfa* dd, int32_
                           const dfm_limits* limits, void* block_out_dev, uint32_t* num_blocks_out,
                           dfm_stats* stats);
 
+/* ---------------------------------------------------------------- post-/pre-processing */
+/* quotient, core.hpp:256-290: the automaton induced on the blocks of a CANONICAL
+ * partition (block: n labels, e.g. a minimizer's block_out).  delta_out: k*num_blocks
+ * u32 (row a at a*num_blocks), acc_out: num_blocks u8; either may be NULL.  Returns
+ * DFM_ERR_INVALID with the reference's std::invalid_argument message in
+ * dfm_last_error ("partition is not in canonical form", "inconsistent partition:
+ * block B mixes accepting and rejecting states" / "... splits on letter A"). */
+int dfm_quotient(dfm_ctx* ctx, const dfm_dfa* d, const uint32_t* block, uint32_t num_blocks,
+                 uint32_t* delta_out, uint8_t* acc_out, uint32_t* initial_out);
+/* Same on the device: block_dev = device canonical labels (dfm_run_algorithm_dev's
+ * block_out_dev); *out is a new device DFA (free with dfm_ddfa_free). */
+int dfm_ddfa_quotient(dfm_ctx* ctx, const dfm_ddfa* dd, const void* block_dev,
+                      uint32_t num_blocks, dfm_ddfa** out);
+/* remove_unreachable, core.hpp:152-187: keeps the states reachable from the initial
+ * state, renumbered densely in ascending original order.  delta_out/acc_out need room
+ * for the input's k*n / n entries; *num_states_out = kept states. */
+int dfm_remove_unreachable(dfm_ctx* ctx, const dfm_dfa* d, uint32_t* num_states_out,
+                           uint32_t* delta_out, uint8_t* acc_out, uint32_t* initial_out);
+int dfm_ddfa_remove_unreachable(dfm_ctx* ctx, const dfm_ddfa* dd, dfm_ddfa** out);
+int dfm_ddfa_initial(const dfm_ddfa* dd, uint32_t* initial);
+
 /* ---------------------------------------------------------------- host generators */
 /* Multi-threaded, bit-exact with generators.hpp (SplitMix64 draw j = mix(seed+(j+1)*gamma)). */
 int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double accept_prob,

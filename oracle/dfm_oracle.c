@@ -579,3 +579,86 @@ int orc_trans_minimize(const orc_dfa* d, uint64_t max_memory_bytes, uint32_t* bl
   free(label);
   return 0;
 }
+
+/* ------------------------------------------------------------------ quotient
+ * core.hpp:256-290: check the partition is canonical (:259-262), then the first
+ * state of each block defines its row (:270-277); every later state must agree
+ * on acceptance (:279-281) and on each letter's target block (:282-286). */
+int orc_quotient(const orc_dfa* d, const uint32_t* block, uint32_t num_blocks, uint32_t* delta_out,
+                 uint8_t* acc_out, uint32_t* initial_out, uint32_t* bad_block,
+                 uint32_t* bad_letter) {
+  const uint32_t n = d->n, k = d->k;
+  uint32_t* canon = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  const uint32_t nb = orc_canonicalize(block, n, canon);
+  int bad = nb != num_blocks;
+  for (uint32_t q = 0; q < n && !bad; ++q) bad = canon[q] != block[q];
+  free(canon);
+  if (bad) return 1;
+  uint8_t* defined = (uint8_t*)calloc(num_blocks ? num_blocks : 1, 1);
+  for (uint32_t b = 0; b < num_blocks; ++b) acc_out[b] = 0;
+  for (size_t i = 0; i < (size_t)k * num_blocks; ++i) delta_out[i] = 0;
+  int rc = 0;
+  for (uint32_t q = 0; q < n && rc == 0; ++q) {
+    const uint32_t b = block[q];
+    if (!defined[b]) {
+      defined[b] = 1;
+      acc_out[b] = d->acc[q];
+      for (uint32_t a = 0; a < k; ++a)
+        delta_out[(size_t)a * num_blocks + b] = block[d->delta[(size_t)a * n + q]];
+      continue;
+    }
+    if (acc_out[b] != d->acc[q]) {
+      rc = 2;
+      *bad_block = b;
+      break;
+    }
+    for (uint32_t a = 0; a < k; ++a)
+      if (delta_out[(size_t)a * num_blocks + b] != block[d->delta[(size_t)a * n + q]]) {
+        rc = 3;
+        *bad_block = b;
+        *bad_letter = a;
+        break;
+      }
+  }
+  free(defined);
+  if (rc == 0) *initial_out = n ? block[d->initial] : 0;
+  return rc;
+}
+
+/* ------------------------------------------------------------------ remove_unreachable
+ * core.hpp:152-187: breadth-first search from the initial state (:153-166), dense
+ * renumbering in ascending original order (:167-171), induced rows (:172-186). */
+uint32_t orc_remove_unreachable(const orc_dfa* d, uint32_t* delta_out, uint8_t* acc_out,
+                                uint32_t* initial_out) {
+  const uint32_t n = d->n, k = d->k;
+  if (n == 0) return 0;
+  uint8_t* seen = (uint8_t*)calloc(n, 1);
+  uint32_t* queue = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  size_t tail = 0;
+  queue[tail++] = d->initial;
+  seen[d->initial] = 1;
+  for (size_t head = 0; head < tail; ++head) {
+    const uint32_t q = queue[head];
+    for (uint32_t a = 0; a < k; ++a) {
+      const uint32_t t = d->delta[(size_t)a * n + q];
+      if (!seen[t]) {
+        seen[t] = 1;
+        queue[tail++] = t;
+      }
+    }
+  }
+  uint32_t* renumber = queue; /* reuse */
+  uint32_t kept = 0;
+  for (uint32_t q = 0; q < n; ++q) renumber[q] = seen[q] ? kept++ : 0;
+  for (uint32_t q = 0; q < n; ++q) {
+    if (!seen[q]) continue;
+    const uint32_t nq = renumber[q];
+    acc_out[nq] = d->acc[q];
+    for (uint32_t a = 0; a < k; ++a)
+      delta_out[(size_t)a * kept + nq] = renumber[d->delta[(size_t)a * n + q]];
+  }
+  *initial_out = renumber[d->initial];
+  free(seen);
+  free(queue);
+  return kept;
+}

@@ -269,6 +269,52 @@ def trans_minimize(delta, acc, max_memory_bytes: int = 16 << 30, inspect: dict |
 
 
 # ---------------------------------------------------------------- the reference itself
+# ---------------------------------------------------------------- post-processing
+class QuotientError(ValueError):
+    """The reference's std::invalid_argument from quotient (core.hpp:256-290)."""
+
+
+def quotient(delta, acc, block, num_blocks: int, initial: int = 0):
+    """core.hpp:256-290 restated (orc_quotient): (delta_q, acc_q, initial_q) or
+    QuotientError with the reference's message."""
+    delta = np.ascontiguousarray(delta, dtype=np.uint32)
+    acc = np.ascontiguousarray(acc, dtype=np.uint8)
+    block = np.ascontiguousarray(block, dtype=np.uint32)
+    k, n = delta.shape[0], acc.size
+    if block.size != n:
+        raise QuotientError("partition covers a different state count")
+    d = _OrcDfa(n, k, delta.ctypes.data if delta.size else None, acc.ctypes.data, initial)
+    dq = np.zeros((k, max(num_blocks, 0)), np.uint32)
+    aq = np.zeros(max(num_blocks, 0), np.uint8)
+    iq, bb, bl = C.c_uint32(0), C.c_uint32(0), C.c_uint32(0)
+    rc = _lib.orc_quotient(C.byref(d), block.ctypes.data_as(C.c_void_p), C.c_uint32(num_blocks),
+                           dq.ctypes.data_as(C.c_void_p), aq.ctypes.data_as(C.c_void_p),
+                           C.byref(iq), C.byref(bb), C.byref(bl))
+    if rc == 1:
+        raise QuotientError("partition is not in canonical form")
+    if rc == 2:
+        raise QuotientError(f"inconsistent partition: block {bb.value} mixes accepting and "
+                            "rejecting states")
+    if rc == 3:
+        raise QuotientError(f"inconsistent partition: block {bb.value} splits on letter {bl.value}")
+    return dq, aq, int(iq.value)
+
+
+def remove_unreachable(delta, acc, initial: int = 0):
+    """core.hpp:152-187 restated (orc_remove_unreachable): (delta', acc', initial')."""
+    delta = np.ascontiguousarray(delta, dtype=np.uint32)
+    acc = np.ascontiguousarray(acc, dtype=np.uint8)
+    k, n = delta.shape[0], acc.size
+    d = _OrcDfa(n, k, delta.ctypes.data if delta.size else None, acc.ctypes.data, initial)
+    flat = np.zeros(max(k * n, 1), np.uint32)
+    ao = np.zeros(max(n, 1), np.uint8)
+    io = C.c_uint32(0)
+    _lib.orc_remove_unreachable.restype = C.c_uint32
+    kept = int(_lib.orc_remove_unreachable(C.byref(d), flat.ctypes.data_as(C.c_void_p),
+                                           ao.ctypes.data_as(C.c_void_p), C.byref(io)))
+    return flat[: k * kept].reshape(k, kept).copy(), ao[:kept].copy(), int(io.value)
+
+
 class Reference:
     """The unmodified reference (oracle/_ref) behind ref_shim.cpp."""
 
@@ -413,3 +459,37 @@ class Reference:
         self.lib.ref_chain_dfa(C.c_uint32(length), delta.ctypes.data_as(C.c_void_p),
                                acc.ctypes.data_as(C.c_void_p))
         return delta, acc
+
+
+def _ref_quotient(self, delta, acc, block, num_blocks: int, initial: int = 0):
+    delta, acc, n, k = self._args(delta, acc)
+    block = np.ascontiguousarray(block, dtype=np.uint32)
+    dq = np.zeros((delta.shape[0], max(num_blocks, 0)), np.uint32)
+    aq = np.zeros(max(num_blocks, 0), np.uint8)
+    iq = C.c_uint32(0)
+    err = C.create_string_buffer(256)
+    rc = self.lib.ref_quotient(n, k, delta.ctypes.data_as(C.c_void_p), acc.ctypes.data_as(C.c_void_p),
+                               C.c_uint32(initial), block.ctypes.data_as(C.c_void_p),
+                               C.c_uint32(num_blocks), dq.ctypes.data_as(C.c_void_p),
+                               aq.ctypes.data_as(C.c_void_p), C.byref(iq), err, C.c_uint32(256))
+    if rc != 0:
+        raise QuotientError(err.value.decode())
+    return dq, aq, int(iq.value)
+
+
+def _ref_remove_unreachable(self, delta, acc, initial: int = 0):
+    delta, acc, n, k = self._args(delta, acc)
+    flat = np.zeros(max(delta.size, 1), np.uint32)
+    ao = np.zeros(max(acc.size, 1), np.uint8)
+    io = C.c_uint32(0)
+    self.lib.ref_remove_unreachable.restype = C.c_uint32
+    kept = int(self.lib.ref_remove_unreachable(n, k, delta.ctypes.data_as(C.c_void_p),
+                                               acc.ctypes.data_as(C.c_void_p), C.c_uint32(initial),
+                                               flat.ctypes.data_as(C.c_void_p),
+                                               ao.ctypes.data_as(C.c_void_p), C.byref(io)))
+    kk = delta.shape[0]
+    return flat[: kk * kept].reshape(kk, kept).copy(), ao[:kept].copy(), int(io.value)
+
+
+Reference.quotient = _ref_quotient
+Reference.remove_unreachable = _ref_remove_unreachable

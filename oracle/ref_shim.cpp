@@ -8,6 +8,7 @@
 // min_trans.hpp:81, core.hpp:220, generators.hpp:36-145).
 #include <cstdint>
 #include <cstring>
+#include <stdexcept>
 #include <vector>
 
 #include "dfamin/dfamin.hpp"
@@ -173,6 +174,38 @@ void ref_bit_splitter(uint32_t bits, uint32_t* delta, uint8_t* acc) {
 }
 void ref_chain_dfa(uint32_t len, uint32_t* delta, uint8_t* acc) {
   copy_dfa(chain_dfa(len), delta, acc);
+}
+
+// quotient (core.hpp:256): 0 ok, 1 invalid_argument (message copied to err)
+int ref_quotient(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                 uint32_t initial, const uint32_t* block, uint32_t num_blocks, uint32_t* delta_out,
+                 uint8_t* acc_out, uint32_t* initial_out, char* err, uint32_t err_cap) {
+  Dfa d = make(n, k, delta, acc, initial);
+  Partition p;
+  p.block.assign(block, block + n);
+  p.num_blocks = num_blocks;
+  try {
+    Dfa q = quotient(d, p);
+    copy_dfa(q, delta_out, acc_out);
+    *initial_out = q.initial;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    if (err && err_cap) {
+      std::strncpy(err, e.what(), err_cap - 1);
+      err[err_cap - 1] = 0;
+    }
+    return 1;
+  }
+}
+
+// remove_unreachable (core.hpp:152): returns the kept state count
+uint32_t ref_remove_unreachable(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc,
+                                uint32_t initial, uint32_t* delta_out, uint8_t* acc_out,
+                                uint32_t* initial_out) {
+  Dfa q = remove_unreachable(make(n, k, delta, acc, initial));
+  copy_dfa(q, delta_out, acc_out);
+  *initial_out = q.initial;
+  return q.num_states;
 }
 
 }  // extern "C"

@@ -273,6 +273,11 @@ def _load():
         "dfm_run_algorithm_dev": (C.c_int, [vp, i32, vp, i32, C.POINTER(_CLimits), vp,
                                             C.POINTER(u32), C.POINTER(_CStats)]),
         "dfm_gen_random_dfa": (C.c_int, [u32, u32, u64, C.c_double, vp, vp]),
+        "dfm_quotient": (C.c_int, [vp, vp, vp, u32, vp, vp, C.POINTER(u32)]),
+        "dfm_ddfa_quotient": (C.c_int, [vp, vp, vp, u32, C.POINTER(vp)]),
+        "dfm_remove_unreachable": (C.c_int, [vp, vp, C.POINTER(u32), vp, vp, C.POINTER(u32)]),
+        "dfm_ddfa_remove_unreachable": (C.c_int, [vp, vp, C.POINTER(vp)]),
+        "dfm_ddfa_initial": (C.c_int, [vp, C.POINTER(u32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -516,6 +521,38 @@ class Engine:
                                                C.byref(nb), C.byref(st)))
         return self._result(block, nb, st)
 
+    # -- post-/pre-processing (core.hpp:152-187, 256-290)
+    def quotient(self, d: Dfa, p: Partition) -> Dfa:
+        """core.hpp:256-290 on the GPU.  Raises ValueError with the reference's
+        std::invalid_argument message for a non-canonical or inconsistent partition."""
+        block = np.ascontiguousarray(p.block, dtype=np.uint32)
+        if block.size != d.num_states:
+            raise ValueError("partition covers a different state count")
+        nb = int(p.num_blocks)
+        cd, keep = self._cdfa(d)
+        delta = np.empty((d.alphabet_size, nb), np.uint32)
+        acc = np.empty(nb, np.uint8)
+        init = C.c_uint32(0)
+        rc = self.lib.dfm_quotient(self.handle, C.byref(cd), block.ctypes.data, nb,
+                                   delta.ctypes.data, acc.ctypes.data, C.byref(init))
+        if rc == 1:  # DFM_ERR_INVALID: the reference throws std::invalid_argument
+            raise ValueError((self.lib.dfm_last_error(self.handle) or b"").decode())
+        self._check(rc)
+        return Dfa(nb, d.alphabet_size, delta, acc, int(init.value))
+
+    def remove_unreachable(self, d: Dfa) -> Dfa:
+        """core.hpp:152-187 on the GPU (breadth-first search + dense renumbering)."""
+        cd, keep = self._cdfa(d)
+        delta = np.empty(max(d.alphabet_size * d.num_states, 1), np.uint32)
+        acc = np.empty(d.num_states, np.uint8)
+        kept, init = C.c_uint32(0), C.c_uint32(0)
+        self._check(self.lib.dfm_remove_unreachable(self.handle, C.byref(cd), C.byref(kept),
+                                                    delta.ctypes.data, acc.ctypes.data,
+                                                    C.byref(init)))
+        n = int(kept.value)
+        rows = delta[: d.alphabet_size * n].reshape(d.alphabet_size, n).copy()
+        return Dfa(n, d.alphabet_size, rows, acc[:n].copy(), int(init.value))
+
     # -- device-resident path (bench "value", sharded driver)
     def upload(self, d: Dfa) -> "DeviceDfa":
         cd, keep = self._cdfa(d)
@@ -598,7 +635,28 @@ class DeviceDfa:
         acc = np.empty(self.num_states, np.uint8)
         self.engine._check(self.engine.lib.dfm_ddfa_download(self.engine.handle, self.handle,
                                                              delta.ctypes.data, acc.ctypes.data))
-        return Dfa(self.num_states, self.alphabet_size, delta, acc, 0)
+        init = C.c_uint32(0)
+        self.engine._check(self.engine.lib.dfm_ddfa_initial(self.handle, C.byref(init)))
+        return Dfa(self.num_states, self.alphabet_size, delta, acc, int(init.value))
+
+    def quotient(self, block_dev_ptr: int, num_blocks: int) -> "DeviceDfa":
+        """Device quotient by canonical device labels (run_device(..., block_out_ptr))."""
+        h = C.c_void_p()
+        e = self.engine
+        rc = e.lib.dfm_ddfa_quotient(e.handle, self.handle, block_dev_ptr, num_blocks, C.byref(h))
+        if rc == 1:
+            raise ValueError((e.lib.dfm_last_error(e.handle) or b"").decode())
+        e._check(rc)
+        return DeviceDfa(e, h, num_blocks, self.alphabet_size)
+
+    def remove_unreachable(self) -> "DeviceDfa":
+        h = C.c_void_p()
+        e = self.engine
+        e._check(e.lib.dfm_ddfa_remove_unreachable(e.handle, self.handle, C.byref(h)))
+        n = C.c_uint32(0)
+        k = C.c_uint32(0)
+        e._check(e.lib.dfm_ddfa_shape(h, C.byref(n), C.byref(k)))
+        return DeviceDfa(e, h, int(n.value), int(k.value))
 
     def free(self) -> None:
         if self.handle:
@@ -650,3 +708,11 @@ def trans_minimize(d: Dfa, limits: Optional[Limits] = None,
 
 def run_algorithm(algo: Algo, d: Dfa, cfg: Optional[AlgoRunConfig] = None) -> MinResult:
     return default_engine().run_algorithm(algo, d, cfg)
+
+
+def quotient(d: Dfa, p: Partition) -> Dfa:  # core.hpp:256
+    return default_engine().quotient(d, p)
+
+
+def remove_unreachable(d: Dfa) -> Dfa:  # core.hpp:152
+    return default_engine().remove_unreachable(d)

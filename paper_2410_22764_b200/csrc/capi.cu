@@ -416,6 +416,75 @@ int dfm_run_algorithm_dev(dfm_ctx* c, int32_t algo, const dfm_ddfa* d, int32_t p
   });
 }
 
+int dfm_quotient(dfm_ctx* c, const dfm_dfa* d, const uint32_t* block, uint32_t num_blocks,
+                 uint32_t* delta_out, uint8_t* acc_out, uint32_t* initial_out) {
+  return guarded(c, [&](Ctx& ctx) {
+    if (block == nullptr) throw Error(DFM_ERR_INVALID, "null partition");
+    const DevDfa dd = upload(ctx, d, "qt.in", false);
+    uint32_t* blk = ctx.slot_t<uint32_t>("qt.block", dd.n);
+    DFM_CUDA(cudaMemcpyAsync(blk, block, (uint64_t)dd.n * 4, cudaMemcpyHostToDevice, ctx.stream));
+    DevDfa q = quotient_dev(ctx, dd, blk, num_blocks);
+    if (delta_out)
+      DFM_CUDA(cudaMemcpyAsync(delta_out, q.delta, (uint64_t)q.n * q.k * 4, cudaMemcpyDeviceToHost,
+                               ctx.stream));
+    if (acc_out)
+      DFM_CUDA(cudaMemcpyAsync(acc_out, q.acc, q.n, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (initial_out) *initial_out = q.initial;
+    cudaFree(q.delta);
+    cudaFree(q.acc);
+  });
+}
+
+int dfm_ddfa_quotient(dfm_ctx* c, const dfm_ddfa* d, const void* block_dev, uint32_t num_blocks,
+                      dfm_ddfa** out) {
+  if (out == nullptr) return DFM_ERR_INVALID;
+  *out = nullptr;
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa* dd = as_dd(d);
+    if (dd == nullptr || block_dev == nullptr) throw Error(DFM_ERR_INVALID, "null input");
+    DevDfa* q = new DevDfa(quotient_dev(ctx, *dd, static_cast<const uint32_t*>(block_dev),
+                                        num_blocks));
+    *out = reinterpret_cast<dfm_ddfa*>(q);
+  });
+}
+
+int dfm_remove_unreachable(dfm_ctx* c, const dfm_dfa* d, uint32_t* num_states_out,
+                           uint32_t* delta_out, uint8_t* acc_out, uint32_t* initial_out) {
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa dd = upload(ctx, d, "ur.in", false);
+    DevDfa r = remove_unreachable_dev(ctx, dd);
+    if (delta_out)
+      DFM_CUDA(cudaMemcpyAsync(delta_out, r.delta, (uint64_t)r.n * r.k * 4, cudaMemcpyDeviceToHost,
+                               ctx.stream));
+    if (acc_out)
+      DFM_CUDA(cudaMemcpyAsync(acc_out, r.acc, r.n, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    if (num_states_out) *num_states_out = r.n;
+    if (initial_out) *initial_out = r.initial;
+    cudaFree(r.delta);
+    cudaFree(r.acc);
+  });
+}
+
+int dfm_ddfa_remove_unreachable(dfm_ctx* c, const dfm_ddfa* d, dfm_ddfa** out) {
+  if (out == nullptr) return DFM_ERR_INVALID;
+  *out = nullptr;
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa* dd = as_dd(d);
+    if (dd == nullptr) throw Error(DFM_ERR_INVALID, "null device dfa");
+    DevDfa* r = new DevDfa(remove_unreachable_dev(ctx, *dd));
+    *out = reinterpret_cast<dfm_ddfa*>(r);
+  });
+}
+
+int dfm_ddfa_initial(const dfm_ddfa* d, uint32_t* initial) {
+  const DevDfa* dd = as_dd(d);
+  if (dd == nullptr || initial == nullptr) return DFM_ERR_INVALID;
+  *initial = dd->initial;
+  return DFM_OK;
+}
+
 int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double p, uint32_t* delta,
                        uint8_t* acc) {
   if (n < 1 || k < 1 || delta == nullptr || acc == nullptr) return DFM_ERR_INVALID;

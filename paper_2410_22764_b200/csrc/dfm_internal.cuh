@@ -163,6 +163,11 @@ AlgoOut run_trans_minimize(Ctx& ctx, const DevDfa& d, const dfm_limits& lim, con
                            uint8_t* apart_host, uint64_t* popcounts, uint32_t pop_cap);
 // canonical relabel of raw labels (< n) into ctx slot "canon"; returns block count
 uint32_t canonicalize_dev(Ctx& ctx, const uint32_t* raw, uint64_t n, uint32_t* out);
+// quotient (core.hpp:256-290) of a canonical device partition; throws Error
+// (DFM_ERR_INVALID) with the reference's invalid_argument messages
+DevDfa quotient_dev(Ctx& ctx, const DevDfa& d, const uint32_t* block, uint32_t num_blocks);
+// remove_unreachable (core.hpp:152-187)
+DevDfa remove_unreachable_dev(Ctx& ctx, const DevDfa& d);
 // device random_dfa
 void random_dfa_dev(Ctx& ctx, DevDfa& d, uint32_t n, uint32_t k, uint64_t seed, double p);
 

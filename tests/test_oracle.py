@@ -141,3 +141,34 @@ def test_oracle_equals_reference_random():
         assert (O.moore(d, a).block == R.moore(d, a).block).all()
         if n <= 24:
             assert (O.trans_minimize(d, a).block == R.trans_minimize(d, a).block).all()
+
+
+def test_post_processing_vs_reference():
+    """quotient / remove_unreachable restated (dfm_oracle.c) == the reference itself."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    R = O.Reference()
+    rng = np.random.default_rng(5)
+    for t in range(200):
+        n = int(rng.integers(1, 60))
+        k = int(rng.integers(0, 4))
+        d, a = O.random_dfa(n, k, int(rng.integers(1, 2 ** 62)), [0, 0.1, 0.5, 1][t % 4])
+        ini = int(rng.integers(0, n))
+        x, y = O.remove_unreachable(d, a, ini), R.remove_unreachable(d, a, ini)
+        assert (x[0] == y[0]).all() and (x[1] == y[1]).all() and x[2] == y[2]
+        r = O.sort_pr(d, a)
+        x, y = O.quotient(d, a, r.block, r.num_blocks, ini), R.quotient(d, a, r.block, r.num_blocks, ini)
+        assert (x[0] == y[0]).all() and (x[1] == y[1]).all() and x[2] == y[2]
+        bad = rng.integers(0, 3, n).astype(np.uint32)
+        c, nb = O.canonicalize(bad)
+        for blk, nbb in ((bad, 3), (c, nb), (c, nb + 1)):
+            e1 = e2 = None
+            try:
+                O.quotient(d, a, blk, nbb, ini)
+            except O.QuotientError as e:
+                e1 = str(e)
+            try:
+                R.quotient(d, a, blk, nbb, ini)
+            except O.QuotientError as e:
+                e2 = str(e)
+            assert e1 == e2
