@@ -379,6 +379,52 @@ inline MinResult trans_minimize(const Dfa& d, const Limits& limits = {},
   return r;
 }
 
+// quotient, core.hpp:256-290: throws std::invalid_argument with the reference's
+// message for a non-canonical or inconsistent partition
+inline Dfa quotient(const Dfa& d, const Partition& p) {
+  if (p.block.size() != d.num_states)
+    throw std::invalid_argument("partition covers a different state count");
+  Engine& e = Engine::thread_default();
+  detail::View v(d);
+  const std::uint32_t nb = p.num_blocks;
+  std::vector<std::uint32_t> flat((std::size_t)d.alphabet_size * nb);
+  Dfa out;
+  out.num_states = nb;
+  out.alphabet_size = d.alphabet_size;
+  out.accepting.assign(nb, 0);
+  std::uint32_t init = 0;
+  const int rc = dfm_quotient(e.get(), &v.c, p.block.data(), nb, flat.data(), out.accepting.data(),
+                              &init);
+  if (rc == DFM_ERR_INVALID) throw std::invalid_argument(dfm_last_error(e.get()));
+  e.check(rc);
+  out.delta.assign(d.alphabet_size, std::vector<State>(nb));
+  for (std::uint32_t a = 0; a < d.alphabet_size; ++a)
+    std::copy(flat.begin() + (std::size_t)a * nb, flat.begin() + (std::size_t)(a + 1) * nb,
+              out.delta[a].begin());
+  out.initial = init;
+  return out;
+}
+
+// remove_unreachable, core.hpp:152-187
+inline Dfa remove_unreachable(const Dfa& d) {
+  Engine& e = Engine::thread_default();
+  detail::View v(d);
+  std::vector<std::uint32_t> flat((std::size_t)d.alphabet_size * d.num_states);
+  std::vector<std::uint8_t> acc(d.num_states);
+  std::uint32_t kept = 0, init = 0;
+  e.check(dfm_remove_unreachable(e.get(), &v.c, &kept, flat.data(), acc.data(), &init));
+  Dfa out;
+  out.num_states = kept;
+  out.alphabet_size = d.alphabet_size;
+  out.delta.assign(d.alphabet_size, std::vector<State>(kept));
+  for (std::uint32_t a = 0; a < d.alphabet_size; ++a)
+    std::copy(flat.begin() + (std::size_t)a * kept, flat.begin() + (std::size_t)(a + 1) * kept,
+              out.delta[a].begin());
+  out.accepting.assign(acc.begin(), acc.begin() + kept);
+  out.initial = init;
+  return out;
+}
+
 inline MinResult run_algorithm(Algo algo, const Dfa& d, const AlgoRunConfig& cfg = {}) {
   switch (algo) {  // bench.hpp:83-112
     case Algo::trans: return ::dfamin::b200::trans_minimize(d, cfg.limits);

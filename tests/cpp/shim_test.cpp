@@ -136,6 +136,26 @@ int main() {
       CHECK(r.stats.status == RunStatus::ok && r.partition.num_blocks == d.num_states);
     }
   }
+  {  // core.hpp:152-187 / 256-290: quotient of a ring by its (singleton) partition is
+     // itself; a chain entered mid-way keeps its tail; a bad partition throws
+    const Dfa d = ring(fib_word(6));
+    const MinResult r = B::sort_pr(d);
+    const Dfa q = B::quotient(d, r.partition);
+    CHECK(q.num_states == r.partition.num_blocks && B::sort_pr(q).partition.num_blocks == q.num_states);
+    Dfa c = chain(100);
+    c.initial = 90;
+    const Dfa t = B::remove_unreachable(c);
+    CHECK(t.num_states == 10 && t.initial == 0 && t.accepting[9] == 1);
+    auto bad = r.partition;
+    bad.block[0] = 1;
+    bool threw = false;
+    try {
+      B::quotient(d, bad);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   std::printf("%d failures\n", failures);
   return failures;
 }
