@@ -127,15 +127,11 @@ def measured_peaks():
 
 
 def int8_peak():
-    """Dense int8 tensor peak: no measured int8 figure exists for this pool, so use
-    2x the measured dense bf16 GEMM rate (UMMA kind::i8 issues K=32 per instruction
-    vs K=16 for bf16 at the same rate); nominal B200 dense int8 is 4.5 POP/s."""
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return 2.0 * float(p["bf16_tflops"]), "2 x measured bf16 burst (MEASURED_PEAKS.json)"
-    except Exception:
-        return 4500.0, "nominal dense int8 (4.5 POP/s)"
+    """Dense int8 tensor peak.  The measured cuBLASLt int8 GEMM (profiles/int8_peak.json,
+    3.09 POP/s) is slower than this repo's own tcgen05 kind::i8 squaring, so it is no
+    ceiling: the roofline uses the nominal dense B200 int8 peak, 4.5 POP/s."""
+    return 4500.0, "nominal dense int8 (4.5 POP/s; cuBLASLt int8 measured 3.09 POP/s, " \
+                    "profiles/int8_peak.json)"
 
 
 def ncu_traffic(family: str):

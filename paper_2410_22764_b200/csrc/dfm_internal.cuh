@@ -64,7 +64,11 @@ struct ProfScope {
   const char* name;
   uint64_t bytes;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool stopped = false;
   ProfScope(Ctx& c, const char* n, uint64_t algo_bytes = 0);
+  // end the timed region early; `bytes` may still be set before destruction (work
+  // counts known only after a device read-back, e.g. persistent-kernel passes)
+  void stop();
   ~ProfScope();
 };
 

@@ -321,6 +321,11 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
   uint32_t* lead2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
   const unsigned grid = grid_for(ctx, n);
 
+  // algorithmic bytes per pass: own label 4, one letter's delta(q) and
+  // delta(leader) 8 and their two labels 8, split flag 1, then the split phase's label,
+  // flag, cell and new label 13 — the reference's early exit (min_partref.hpp:93-97)
+  // means most states read one letter; the SURVEY 8(d) figure n(16k'+8) is the bound
+  const uint64_t pass_bytes = n * (fused_cas ? 4ull + 16 + 8 + 4 : 4ull + 16 + 1 + 13);
   DFM_CUDA(cudaMemsetAsync(lead2, 0xFF, 8, ctx.stream));
   DFM_CUDA(cudaMemsetAsync(cells, (!fused_cas && policy == DFM_POLICY_MIN) ? 0xFF : 0x00, n * 8,
                            ctx.stream));
@@ -362,15 +367,15 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
                         sel, pout};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&pa};
-      {
-        ProfScope p(ctx, "elect", 0);
-        DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, kPersistThreads, args, 0,
-                                             ctx.stream));
-        DFM_LAUNCH_CHECK();
-      }
+      ProfScope prof(ctx, "elect", 0);
+      DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, kPersistThreads, args, 0,
+                                           ctx.stream));
+      DFM_LAUNCH_CHECK();
+      prof.stop();
       DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, pout, 12, cudaMemcpyDeviceToHost, ctx.stream));
       ctx.sync();
       const uint32_t* h = reinterpret_cast<const uint32_t*>(ctx.h_scalars + 20);
+      prof.bytes = (uint64_t)h[0] * pass_bytes;
       pass += h[0];
       sel = (int)h[2];
       if (h[1]) break;
@@ -400,14 +405,13 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       const uint32_t* cur = lab[sel];
       uint32_t* nxt = lab[sel ^ 1];
       if (fused_cas) {
-        ProfScope p(ctx, "elect", n * (16ull * letters + 8));  // SURVEY 8(d) upper bound
+        ProfScope p(ctx, "elect", pass_bytes);
         cas_kernel<<<grid, 256, 0, ctx.stream>>>(rows, n, letters, cur, cells, nxt, changed + b,
                                                  pass);
         DFM_LAUNCH_CHECK();
       } else {
         {
-          // label 4 + per letter (2 delta + 2 label gathers) 16 + flag 1: SURVEY 8(d) bound
-          ProfScope p(ctx, "elect", n * (16ull * letters + 5));
+          ProfScope p(ctx, "elect", n * (4ull + 16 + 1));
           if (policy == DFM_POLICY_MIN)
             elect_kernel<DFM_POLICY_MIN><<<grid, 256, 0, ctx.stream>>>(rows, n, letters, cur, cells,
                                                                        split_flag, pass);

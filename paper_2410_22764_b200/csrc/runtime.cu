@@ -150,9 +150,15 @@ ProfScope::ProfScope(Ctx& c, const char* n, uint64_t algo_bytes)
   DFM_CUDA(cudaEventRecord(ev0, ctx.stream));
 }
 
+void ProfScope::stop() {
+  if (!ctx.profiling || ev0 == nullptr || stopped) return;
+  cudaEventRecord(ev1, ctx.stream);
+  stopped = true;
+}
+
 ProfScope::~ProfScope() {
   if (!ctx.profiling || ev0 == nullptr) return;
-  cudaEventRecord(ev1, ctx.stream);
+  if (!stopped) cudaEventRecord(ev1, ctx.stream);
   ctx.pending.push_back({name, ev0, ev1, bytes});
   if (ctx.pending.size() > 4096) {
     try {
