@@ -207,6 +207,15 @@ int dfm_remove_unreachable(dfm_ctx* ctx, const dfm_dfa* d, uint32_t* num_states_
 int dfm_ddfa_remove_unreachable(dfm_ctx* ctx, const dfm_ddfa* dd, dfm_ddfa** out);
 int dfm_ddfa_initial(const dfm_ddfa* dd, uint32_t* initial);
 
+/* ---------------------------------------------------------------- bulk input path */
+/* Binary DFA file beside the reference's text format (ingest.hpp:286-369):
+ * "DFMBIN01" | u32 n | u32 k | u32 initial | u32 0 | acc[n] u8 | pad to 4 | delta[k][n]
+ * u32 (the reference's SoA rows).  Host write; device load through double-buffered
+ * pinned staging (file reads overlap the H2D copies) and device save. */
+int dfm_write_dfa_bin(const char* path, const dfm_dfa* d);
+int dfm_ddfa_load_bin(dfm_ctx* ctx, const char* path, dfm_ddfa** out);
+int dfm_ddfa_save_bin(dfm_ctx* ctx, const dfm_ddfa* dd, const char* path);
+
 /* ---------------------------------------------------------------- host generators */
 /* Multi-threaded, bit-exact with generators.hpp (SplitMix64 draw j = mix(seed+(j+1)*gamma)). */
 int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double accept_prob,

@@ -278,6 +278,9 @@ def _load():
         "dfm_remove_unreachable": (C.c_int, [vp, vp, C.POINTER(u32), vp, vp, C.POINTER(u32)]),
         "dfm_ddfa_remove_unreachable": (C.c_int, [vp, vp, C.POINTER(vp)]),
         "dfm_ddfa_initial": (C.c_int, [vp, C.POINTER(u32)]),
+        "dfm_write_dfa_bin": (C.c_int, [C.c_char_p, vp]),
+        "dfm_ddfa_load_bin": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+        "dfm_ddfa_save_bin": (C.c_int, [vp, vp, C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -553,6 +556,14 @@ class Engine:
         rows = delta[: d.alphabet_size * n].reshape(d.alphabet_size, n).copy()
         return Dfa(n, d.alphabet_size, rows, acc[:n].copy(), int(init.value))
 
+    # -- bulk input path (binary DFA files, csrc/io.cu)
+    def load_bin(self, path: str) -> "DeviceDfa":
+        h = C.c_void_p()
+        self._check(self.lib.dfm_ddfa_load_bin(self.handle, os.fsencode(path), C.byref(h)))
+        n, k = C.c_uint32(0), C.c_uint32(0)
+        self._check(self.lib.dfm_ddfa_shape(h, C.byref(n), C.byref(k)))
+        return DeviceDfa(self, h, int(n.value), int(k.value))
+
     # -- device-resident path (bench "value", sharded driver)
     def upload(self, d: Dfa) -> "DeviceDfa":
         cd, keep = self._cdfa(d)
@@ -649,6 +660,10 @@ class DeviceDfa:
         e._check(rc)
         return DeviceDfa(e, h, num_blocks, self.alphabet_size)
 
+    def save_bin(self, path: str) -> None:
+        e = self.engine
+        e._check(e.lib.dfm_ddfa_save_bin(e.handle, self.handle, os.fsencode(path)))
+
     def remove_unreachable(self) -> "DeviceDfa":
         h = C.c_void_p()
         e = self.engine
@@ -716,3 +731,28 @@ def quotient(d: Dfa, p: Partition) -> Dfa:  # core.hpp:256
 
 def remove_unreachable(d: Dfa) -> Dfa:  # core.hpp:152
     return default_engine().remove_unreachable(d)
+
+
+_BIN_MAGIC = b"DFMBIN01"
+
+
+def write_dfa_bin(path: str, d: Dfa) -> None:
+    """Binary DFA file (include/dfm.h, dfm_write_dfa_bin) — host only, no GPU needed."""
+    lib = _load()
+    cd, keep = Engine._cdfa(d)
+    rc = lib.dfm_write_dfa_bin(os.fsencode(path), C.byref(cd))
+    if rc != 0:
+        raise EngineError(rc, f"cannot write {path}")
+
+
+def read_dfa_bin(path: str) -> Dfa:
+    """Host reader of the binary format (memory-mapped, zero-copy rows)."""
+    raw = np.memmap(path, dtype=np.uint8, mode="r")
+    if bytes(raw[:8]) != _BIN_MAGIC:
+        raise ValueError(f"{path}: not a DFMBIN01 file")
+    n, k, initial, _ = np.frombuffer(raw[8:24].tobytes(), dtype="<u4")
+    n, k = int(n), int(k)
+    acc = np.array(raw[24:24 + n])
+    off = 24 + ((n + 3) & ~3)
+    delta = np.frombuffer(raw[off:off + 4 * n * k].tobytes(), dtype="<u4").reshape(k, n).copy()
+    return Dfa(n, k, delta, acc, int(initial))

@@ -478,6 +478,44 @@ int dfm_ddfa_remove_unreachable(dfm_ctx* c, const dfm_ddfa* d, dfm_ddfa** out) {
   });
 }
 
+int dfm_write_dfa_bin(const char* path, const dfm_dfa* d) {
+  if (path == nullptr) return DFM_ERR_INVALID;
+  try {
+    check_host_dfa(d);
+    write_dfa_bin(path, d->num_states, d->alphabet_size, d->initial, d->delta, d->accepting);
+    return DFM_OK;
+  } catch (const Error& e) {
+    g_create_error = e.what();
+    return e.code;
+  }
+}
+
+int dfm_ddfa_load_bin(dfm_ctx* c, const char* path, dfm_ddfa** out) {
+  if (out == nullptr || path == nullptr) return DFM_ERR_INVALID;
+  *out = nullptr;
+  return guarded(c, [&](Ctx& ctx) {
+    DevDfa* dd = new DevDfa(load_dfa_bin(ctx, path));
+    try {
+      validate_targets(ctx, *dd);
+    } catch (...) {
+      cudaFree(dd->delta);
+      cudaFree(dd->acc);
+      delete dd;
+      throw;
+    }
+    *out = reinterpret_cast<dfm_ddfa*>(dd);
+  });
+}
+
+int dfm_ddfa_save_bin(dfm_ctx* c, const dfm_ddfa* d, const char* path) {
+  if (path == nullptr) return DFM_ERR_INVALID;
+  return guarded(c, [&](Ctx& ctx) {
+    const DevDfa* dd = as_dd(d);
+    if (dd == nullptr) throw Error(DFM_ERR_INVALID, "null device dfa");
+    save_dfa_bin(ctx, *dd, path);
+  });
+}
+
 int dfm_ddfa_initial(const dfm_ddfa* d, uint32_t* initial) {
   const DevDfa* dd = as_dd(d);
   if (dd == nullptr || initial == nullptr) return DFM_ERR_INVALID;

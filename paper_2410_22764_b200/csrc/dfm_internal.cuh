@@ -172,6 +172,11 @@ uint32_t canonicalize_dev(Ctx& ctx, const uint32_t* raw, uint64_t n, uint32_t* o
 DevDfa quotient_dev(Ctx& ctx, const DevDfa& d, const uint32_t* block, uint32_t num_blocks);
 // remove_unreachable (core.hpp:152-187)
 DevDfa remove_unreachable_dev(Ctx& ctx, const DevDfa& d);
+// binary DFA files (csrc/io.cu): host write, device load / save
+void write_dfa_bin(const char* path, uint32_t n, uint32_t k, uint32_t initial,
+                   const uint32_t* const* rows, const uint8_t* acc);
+DevDfa load_dfa_bin(Ctx& ctx, const char* path);
+void save_dfa_bin(Ctx& ctx, const DevDfa& dd, const char* path);
 // device random_dfa
 void random_dfa_dev(Ctx& ctx, DevDfa& d, uint32_t n, uint32_t k, uint64_t seed, double p);
 
