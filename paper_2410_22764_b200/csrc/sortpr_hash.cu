@@ -488,12 +488,16 @@ struct ResolveOut {
 // come from the leader flags), so every state resolves independently
 constexpr int kResolveItems = 4;
 
+// *inactive is set when some group is a singleton (its state leaves the active list):
+// passes without one reuse the active list instead of compacting it
 __global__ void __launch_bounds__(256) resolve_kernel(uint64_t m, ResolveIn in, ResolveOut out,
-                                                      unsigned long long* fresh) {
+                                                      unsigned long long* fresh,
+                                                      unsigned long long* inactive) {
   constexpr int U = kResolveItems;
   __shared__ uint32_t s_cnt[8 * U];
   __shared__ uint32_t s_first;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool any_single = false;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * U; base < m; base += stride) {
     ResolveItem it[U];
@@ -501,8 +505,12 @@ __global__ void __launch_bounds__(256) resolve_kernel(uint64_t m, ResolveIn in, 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = base + u * blockDim.x + threadIdx.x;
-      if (i < m) it[u] = in(i);
-      else it[u].v = 0;
+      if (i < m) {
+        it[u] = in(i);
+        any_single |= (it[u].flags & 3u) == 3u;  // the rep of a one-member group
+      } else {
+        it[u].v = 0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -530,6 +538,7 @@ __global__ void __launch_bounds__(256) resolve_kernel(uint64_t m, ResolveIn in, 
     }
     __syncthreads();
   }
+  if (__syncthreads_or(any_single) && threadIdx.x == 0) atomicOr(inactive, 1ull);
 }
 
 __global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* __restrict__ act,
@@ -983,7 +992,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     // hash tables: load <= 0.4 (a warp waits for its longest probe chain)
     const uint64_t table = direct ? (1ull << kbits) : std::max<uint64_t>(1024, m * 5 / 2);
     DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
+    DFM_CUDA(cudaMemsetAsync(sc + 8, 0, 8, ctx.stream));
     uint32_t* act_next = act_buf[act_sel ^ 1];
+    bool act_scanned = false;  // the partitioned path compacts inside the pass
     if (m > 0) {
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
       const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
@@ -1011,6 +1022,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
                             flag, lead, sc);
           ProfScope p(ctx, "scan", m * 9ull);
           prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+          act_scanned = true;
         }
       }
       if (!part) {
@@ -1072,7 +1084,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
             m,
             ResolveIn{slots, slot_of, packed ? nullptr : sig, k + 1, row,
                       reinterpret_cast<unsigned long long*>(sc + 2), act, lead},
-            ResolveOut{slots, act, block, res, st, B}, reinterpret_cast<unsigned long long*>(sc + 1));
+            ResolveOut{slots, act, block, res, st, B}, reinterpret_cast<unsigned long long*>(sc + 1),
+            reinterpret_cast<unsigned long long*>(sc + 8));
         DFM_LAUNCH_CHECK();
       }
       {
@@ -1081,13 +1094,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
                                                                block, flag, lead, sc);
         DFM_LAUNCH_CHECK();
       }
-      {
-        ProfScope p(ctx, "scan", m * 9ull);
-        prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
-      }
       }
     }
-    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 24, cudaMemcpyDeviceToHost, ctx.stream));
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 64, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
     if (ctx.h_scalars[2] & kFlagOverflow) {  // partitioned grouping overflowed a bucket:
       force_global = true;                    // redo the pass with the global table
@@ -1108,9 +1117,19 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     }
     if (fresh == 0) break;  // fixpoint, min_sort.hpp:111-117
     B = B_next;
-    m = ctx.h_scalars[3];
-    act = act_next;
-    act_sel ^= 1;
+    if (!act_scanned && m > 0 && ctx.h_scalars[8] != 0) {
+      // some states became singletons: compact the active list (ascending q)
+      ProfScope p(ctx, "scan", m * 9ull);
+      prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+      DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 3, sc + 3, 8, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      act_scanned = true;
+    }
+    if (act_scanned) {
+      m = ctx.h_scalars[3];
+      act = act_next;
+      act_sel ^= 1;
+    }
     build_mirror(B);  // id mirror for the next pass's gathers
   }
   out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
