@@ -289,6 +289,7 @@ struct SigParams {
   // and vals[i] = i | lead << 31
   uint32_t* vals;
   const uint8_t* lead;
+  uint32_t* present;  // direct keys: bitmap of the keys present (rank-compacted table)
 };
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
@@ -342,6 +343,11 @@ __global__ void __launch_bounds__(1024) lay_sig_kernel(SigParams p) {
         for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
           key = (key << p.w) | (uint32_t)s_tile[a * L.W + x];
         p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
+        if (p.present) {  // test before set: most keys of a dense pass are repeats
+          const uint32_t bit = 1u << (key & 31);
+          uint32_t* word = p.present + (key >> 5);
+          if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
+        }
       } else {
         uint32_t* row = p.sig + i * (uint64_t)p.row;
         row[0] = b;

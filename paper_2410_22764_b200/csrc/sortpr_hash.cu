@@ -66,6 +66,10 @@ struct InsertParams {
   uint32_t* __restrict__ sig;
   uint32_t row;  // signature row stride (words)
   unsigned long long* keys;  // precomputed exact keys (swept passes), else unused
+  // rank-compacted direct table: slot = rank of the key among the keys present
+  // (bitmap + per-word exclusive popcount); no same-slot warp aggregation
+  const uint32_t* present;
+  const uint32_t* present_pre;
 };
 
 // L2 eviction policies: the delta stream is read once per pass (evict first) so
@@ -222,7 +226,12 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       const uint64_t i = base + u * 32 + lane;
       if (valid[u]) {
         if (kDirect) {
-          s[u] = key[u];
+          if (p.present) {
+            const uint32_t w = (uint32_t)(key[u] >> 5);
+            s[u] = p.present_pre[w] + __popc(p.present[w] & ((1u << (key[u] & 31)) - 1u));
+          } else {
+            s[u] = key[u];
+          }
         } else {
           // stored key: never 0 (0 marks an empty slot); start slot = mulhi(hash, capacity)
           const unsigned long long stored = kHashed ? (key[u] | 1ull) : key[u] + 1ull;
@@ -256,6 +265,13 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
           s[u] = t;
         }
         p.slot_of[i] = (uint32_t)s[u];
+      }
+      if (kDirect && p.present) {  // many distinct keys: consecutive states rarely share one
+        if (valid[u]) {
+          atomicMax(&p.slots[s[u]].rep, ~(uint32_t)i);
+          atomicAdd(&p.slots[s[u]].info, 1u | (lead[u] ? 0x80000000u : 0u));
+        }
+        continue;
       }
       const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u] && merge[u]);
       if (valid[u] && merge[u]) {
@@ -562,6 +578,15 @@ __global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* 
   }
 }
 
+struct PresentIn {
+  const uint32_t* present;
+  __device__ uint32_t operator()(uint64_t w) const { return __popc(present[w]); }
+};
+struct PresentOut {
+  uint32_t* pre;
+  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { pre[w] = excl; }
+};
+
 struct ActIn {
   const uint32_t* act;
   const uint8_t* flag;
@@ -830,7 +855,7 @@ void layout_keys_bits(Ctx& ctx, const Layout& L, const uint32_t* ids, const SigP
 void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const uint32_t* act,
                  uint64_t m, const uint32_t* block, int w, bool hashed, uint64_t seed,
                  unsigned long long* keys, uint32_t* sig, uint32_t row, uint32_t* vals,
-                 const uint8_t* lead) {
+                 const uint8_t* lead, uint32_t* present) {
   if (act) {
     ProfScope ps(ctx, "scan", m * 4 + L.nW * 4ull);
     lay_wstart_kernel<<<grid_for(ctx, m + 1), 256, 0, ctx.stream>>>(act, m, L.W, L.nW, L.wstart);
@@ -838,7 +863,7 @@ void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const ui
   }
   const uint64_t idb = (uint64_t)std::max(8, mirror_bits) / 8;
   SigParams sp{L,   act ? L.wstart : nullptr, act, block, w, seed, keys, hashed ? sig : nullptr,
-               row, vals, lead};
+               row, vals, lead, present};
   // per transition: tgt 2 + id write + lsf 2 + eidx 4 + id read; id slices once; per active
   // state: act 4 + own id 4 + key 8 (+ signature row)
   ProfScope ps(ctx, "sig", L.T * (8 + 2 * idb) + L.n * (uint64_t)mirror_bits / 8 +
@@ -999,6 +1024,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
       const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
       unsigned long long* keys = nullptr;
+      uint32_t* present = nullptr;  // rank-compacted direct table (blocked passes)
+      uint32_t* present_pre = nullptr;
       if (packed && (mirror_bits == 8 || mirror_bits == 16))
         keys = ctx.slot_t<unsigned long long>("sh.keys", m);
       // blocked signature builder whenever most states are active (it streams all n*k
@@ -1015,8 +1042,14 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         }
         keys = ctx.slot_t<unsigned long long>("sh.keys", m);
         uint32_t* vals = part ? ctx.slot_t<uint32_t>("gp.v", m) : nullptr;
+        if (!part && direct && table > kSmallTable) {
+          const uint64_t words = ceil_div(table, 32);
+          present = ctx.slot_t<uint32_t>("sh.present", words);
+          present_pre = ctx.slot_t<uint32_t>("sh.presentpre", words);
+          DFM_CUDA(cudaMemsetAsync(present, 0, words * 4, ctx.stream));
+        }
         layout_keys(ctx, lay, mirror_bits, ids, act, m, block, w, !packed, seed, keys, sig, row,
-                    vals, lead);
+                    vals, lead, present);
         if (part) {
           group_partitioned(ctx, m, act, keys, vals, packed ? nullptr : sig, k + 1, row, B, block,
                             flag, lead, sc);
@@ -1029,6 +1062,16 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       // uniqueness filter in front of large hash tables (keys are precomputed)
       const bool filtered = blocked && !direct && m >= kFilterMinStates;
       uint64_t cap = table;
+      if (present) {
+        // dense slots for the keys present: exclusive popcount over the bitmap words
+        const uint64_t words = ceil_div(table, 32);
+        ProfScope p(ctx, "insert", words * 8);
+        prims::lookback_scan(ctx, "sc.present", words, PresentIn{present},
+                             PresentOut{present_pre}, sc + 9);
+        DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 9, sc + 9, 8, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+        cap = std::max<uint64_t>(1, ctx.h_scalars[9]);
+      }
       if (filtered) {
         uint32_t* F = ctx.slot_t<uint32_t>("sh.filter", 1ull << (kFilterCellBits - 4));
         uint64_t dups = m;
@@ -1056,7 +1099,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", cap * sizeof(Slot)));
       DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(Slot), ctx.stream));
       InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, cap, slots,
-                      slot_of, packed ? nullptr : sig, row, keys};
+                      slot_of, packed ? nullptr : sig, row, keys, present,
+                      present ? present_pre : nullptr};
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
         switch (k) {
