@@ -63,19 +63,43 @@ __global__ void __launch_bounds__(512) lay_count_kernel(const uint32_t* __restri
     const uint64_t q0 = (uint64_t)w * L.W;
     const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
     // the window's k x wn transitions as one flat range (rows of wn coalesced
-    // states), 8 independent delta loads in flight per thread
+    // states): 16-byte loads when rows are 16-byte aligned, 4 in flight per thread
     const uint32_t ew = wn * L.k;
-    for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
-      uint32_t t[8];
+    if ((L.n & 3) == 0) {
+      const uint32_t w4 = wn / 4, ew4 = ew / 4;
+      for (uint32_t e0 = 0; e0 < ew4; e0 += 4 * blockDim.x) {
+        uint4 t[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
-        const uint32_t a = e / wn;
-        t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          const uint32_t a = e / w4;
+          if (e < ew4)
+            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                : "=r"(t[u].x), "=r"(t[u].y), "=r"(t[u].z), "=r"(t[u].w)
+                : "l"(delta + a * L.n + q0 + 4 * (e - a * w4)), "l"(pol));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * blockDim.x + threadIdx.x < ew4) {
+            atomicAdd(&s_h[t[u].x / kRs], 1u);
+            atomicAdd(&s_h[t[u].y / kRs], 1u);
+            atomicAdd(&s_h[t[u].z / kRs], 1u);
+            atomicAdd(&s_h[t[u].w / kRs], 1u);
+          }
       }
+    } else {
+      for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
+        uint32_t t[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (e0 + u * blockDim.x + threadIdx.x < ew) atomicAdd(&s_h[t[u] / kRs], 1u);
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          const uint32_t a = e / wn;
+          t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u * blockDim.x + threadIdx.x < ew) atomicAdd(&s_h[t[u] / kRs], 1u);
+      }
     }
     __syncthreads();
     // counts (w-major, transposed later for the bucket scan) + in-window prefix
@@ -131,10 +155,20 @@ struct LayOffOut {
 
 // ---- layout build: bucket every transition (tgt) and its tile slot (lsf).
 // Both are staged in shared memory in the window's flattened order (sub-run j
-// at pre(w, j)) with the sub-run index; lsf leaves as one coalesced chunk, tgt
-// and dst (the flattened position) as contiguous runs at off(j, w).
+// at pre(w, j)); lsf leaves as one coalesced chunk, and one warp per sub-run
+// writes its tgt run at the bucket position off(j, w) and the positions (eidx).
+__device__ __forceinline__ void lay_stage(uint32_t t, uint32_t a, uint32_t x, uint32_t W,
+                                          uint32_t* s_cur, const uint32_t* s_pre,
+                                          uint16_t* s_tgt, uint16_t* s_lsf, uint16_t* s_j) {
+  const uint32_t j = t / kRs;
+  const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
+  s_tgt[f] = (uint16_t)(t - j * kRs);
+  s_lsf[f] = (uint16_t)(a * W + x);
+  s_j[f] = (uint16_t)j;
+}
+
 __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __restrict__ delta,
-                                                          Layout L) {
+                                                           Layout L) {
   // s_cur[R], s_off[R], s_pre[R+1], then u16 s_lsf[E], s_tgt[E], s_j[E]
   extern __shared__ uint32_t s_lay[];
   uint32_t* s_cur = s_lay;
@@ -144,44 +178,88 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
   uint16_t* s_tgt = s_lsf + L.E;
   uint16_t* s_j = s_tgt + L.E;
   const uint64_t pol = policy_evict_first();
+  // the next window's sub-run starts are loaded while the current one is written out
+  constexpr uint32_t kPf = kMaxRanges / 1024;
+  uint32_t pf_off[kPf], pf_pre[kPf];
+  auto prefetch = [&](uint32_t w) {
+#pragma unroll
+    for (uint32_t u = 0; u < kPf; ++u) {
+      const uint32_t j = threadIdx.x + u * blockDim.x;
+      if (w < L.nW && j < L.R) {
+        pf_off[u] = L.off[(uint64_t)j * L.nW + w];
+        pf_pre[u] = L.pre[(uint64_t)w * L.R + j];
+      }
+    }
+  };
+  prefetch(blockIdx.x);
   for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
     const uint64_t q0 = (uint64_t)w * L.W;
     const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
     const uint32_t ew = wn * L.k;
-    for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) {
-      s_cur[j] = 0;
-      s_off[j] = L.off[(uint64_t)j * L.nW + w];
-      s_pre[j] = L.pre[(uint64_t)w * L.R + j];
+#pragma unroll
+    for (uint32_t u = 0; u < kPf; ++u) {
+      const uint32_t j = threadIdx.x + u * blockDim.x;
+      if (j < L.R) {
+        s_cur[j] = 0;
+        s_off[j] = pf_off[u];
+        s_pre[j] = pf_pre[u];
+      }
     }
     if (threadIdx.x == 0) s_pre[L.R] = ew;
     __syncthreads();
-    for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
-      uint32_t t[8];
+    if ((L.n & 3) == 0) {  // 16-byte row loads
+      const uint32_t w4 = wn / 4, ew4 = ew / 4;
+      for (uint32_t e0 = 0; e0 < ew4; e0 += 2 * blockDim.x) {
+        uint4 t[2];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
-        const uint32_t a = e / wn;
-        t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          const uint32_t a = e / w4;
+          if (e < ew4)
+            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                : "=r"(t[u].x), "=r"(t[u].y), "=r"(t[u].z), "=r"(t[u].w)
+                : "l"(delta + a * L.n + q0 + 4 * (e - a * w4)), "l"(pol));
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          if (e < ew4) {
+            const uint32_t a = e / w4, x = 4 * (e - a * w4);
+            lay_stage(t[u].x, a, x, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+            lay_stage(t[u].y, a, x + 1, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+            lay_stage(t[u].z, a, x + 2, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+            lay_stage(t[u].w, a, x + 3, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+          }
+        }
       }
+    } else {
+      for (uint32_t e0 = 0; e0 < ew; e0 += 8 * blockDim.x) {
+        uint32_t t[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
-        if (e < ew) {
-          const uint32_t a = e / wn, x = e - a * wn;
-          const uint32_t j = t[u] / kRs;
-          const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
-          s_tgt[f] = (uint16_t)(t[u] - j * kRs);
-          s_lsf[f] = (uint16_t)(a * L.W + x);
-          s_j[f] = (uint16_t)j;
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          const uint32_t a = e / wn;
+          t[u] = e < ew ? ld_stream(delta + a * L.n + q0 + (e - a * wn), pol) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
+          if (e < ew) {
+            const uint32_t a = e / wn;
+            lay_stage(t[u], a, e - a * wn, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+          }
         }
       }
     }
     __syncthreads();
+    prefetch(w + gridDim.x);
+    // bucket position of flattened slot f of sub-run j = off(j, w) - pre(w, j) + f
+    for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) s_off[j] -= s_pre[j];
+    __syncthreads();
     const uint64_t fb = (uint64_t)w * L.E;
     for (uint32_t f = threadIdx.x; f < ew; f += blockDim.x) {
+      const uint32_t e = s_off[s_j[f]] + f;
       L.lsf[fb + f] = s_lsf[f];
-      const uint32_t j = s_j[f];
-      const uint32_t e = s_off[j] + (f - s_pre[j]);
       L.tgt[e] = s_tgt[f];
       L.eidx[fb + f] = e;
     }
