@@ -371,8 +371,9 @@ struct SigParams {
 };
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
+// narrow tiles (<= 64 KB) fit two CTAs per SM: cap registers at 32 for that
 template <int kIdBits, int kK, bool kHashed>
-__global__ void __launch_bounds__(1024) lay_sig_kernel(SigParams p) {
+__global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(SigParams p) {
   using V = typename IdT<kIdBits>::type;
   extern __shared__ uint4 s_tile4[];
   V* s_tile = reinterpret_cast<V*>(s_tile4);  // [k][W]
@@ -386,11 +387,13 @@ __global__ void __launch_bounds__(1024) lay_sig_kernel(SigParams p) {
     const uint32_t ew = wn * k;
     const uint64_t fb = (uint64_t)w * L.E;
     // lane-consecutive transitions (coalesced slot / position loads; the ids come
-    // in runs of ~16 per sub-run), 8 in flight per thread
-    for (uint32_t f0 = threadIdx.x; f0 < ew; f0 += 8 * blockDim.x) {
-      uint32_t sl[8], ee[8];
+    // in runs of ~16 per sub-run), U in flight per thread (fewer under the 32-register
+    // cap of the two-CTA narrow tiles)
+    constexpr int U = kIdBits <= 16 ? 4 : 8;
+    for (uint32_t f0 = threadIdx.x; f0 < ew; f0 += U * blockDim.x) {
+      uint32_t sl[U], ee[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint32_t f = f0 + u * blockDim.x;
         sl[u] = 0;
         ee[u] = 0;
@@ -401,11 +404,11 @@ __global__ void __launch_bounds__(1024) lay_sig_kernel(SigParams p) {
               : "=r"(ee[u]) : "l"(L.eidx + fb + f), "l"(pol));
         }
       }
-      V x[8];
+      V x[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = (f0 + u * blockDim.x < ew) ? vin[ee[u]] : (V)0;
+      for (int u = 0; u < U; ++u) x[u] = (f0 + u * blockDim.x < ew) ? vin[ee[u]] : (V)0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < U; ++u)
         if (f0 + u * blockDim.x < ew) s_tile[sl[u]] = x[u];
     }
     __syncthreads();
