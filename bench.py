@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the state-sharded sortPR")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the state-sharded sortPR driver even at N = 1 (its own baseline)")
     return ap.parse_args()
 
 
@@ -423,7 +425,8 @@ def run_sharded(args, rank: int, world: int, local: int):
     launches0 = eng.kernel_launches()
     clocks = ClockSampler(local)
     clocks.start()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
     step_ms = []
     for _ in range(args.steps):
@@ -435,13 +438,15 @@ def run_sharded(args, rank: int, world: int, local: int):
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize(dev)
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     clk = clocks.stop()
     launches = eng.kernel_launches() - launches0
     eng.set_profiling(False)
     prof = eng.profile()
     t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
     transitions = float(n_total) * args.k * r.iterations
     value = transitions / (ms_per_step / 1e3)
@@ -455,7 +460,8 @@ def run_sharded(args, rank: int, world: int, local: int):
         out = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
         e_ms = []
         for _ in range(args.e2e_steps):
-            dist.barrier()
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             rr = sharded_sort_pr(pin_d.to(dev, non_blocking=True), pin_a.to(dev, non_blocking=True),
                                  n_total, lo, comm, ops)
@@ -463,7 +469,8 @@ def run_sharded(args, rank: int, world: int, local: int):
             torch.cuda.synchronize(dev)
             e_ms.append((time.perf_counter() - t0) * 1e3)
         et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": transitions / (float(et.item()) / 1e3), "unit": UNIT,
                "ms_per_step": float(et.item()),
                "h2d_bytes_per_step": (4 * args.k + 1) * n_total,
@@ -510,7 +517,7 @@ def main():
         torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        if world > 1 and args.algo == "sort" and not args.replicas:
+        if (world > 1 or args.sharded) and args.algo == "sort" and not args.replicas:
             run_sharded(args, rank, world, local)
         else:
             run_ours(args, rank, world, local)
