@@ -298,6 +298,195 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant for tiny inputs (rings and chains of a few thousand states run
+// n-1 passes): the whole working set — successor rows, both label buffers,
+// election cells, split flags — lives in the (distributed) shared memory of a
+// thread-block cluster; CTA r owns states [r*S, (r+1)*S) and any state's data is
+// one (DSMEM) access away; the two barriers per pass are cluster barriers instead
+// of grid-wide ones.  Same per-pass semantics as persistent_kernel.  Used for
+// single-CTA instances only (see run_leader_election for the measurements).
+struct ClusterArgs {
+  const uint32_t* rows;  // global [letters][n]
+  uint64_t n, letters;
+  uint32_t S;            // states per CTA
+  uint32_t* lab0;        // global label buffers (in/out)
+  uint32_t* lab1;
+  uint32_t pass0, max_passes;
+  int start_sel;
+  uint32_t* out;         // [0] passes executed, [1] stable, [2] buffer holding the labels
+};
+
+// DSMEM accesses through explicit shared::cluster addresses.  Election cells are
+// 32-bit (64-bit min/max on another CTA's shared memory is not a native atomic on
+// sm_100: ptxas lowers it to a local-CTA CAS fallback) and double-buffered by pass
+// parity instead of epoch-tagged: a CTA clears its own cells of the next pass while
+// the current pass runs (their last readers finished before this pass's barrier).
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_min_u32(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared::cluster.min.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_max_u32(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared::cluster.max.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_cas_u32(uint32_t addr, uint32_t cmp, uint32_t val) {
+  uint32_t old;
+  asm volatile("atom.shared::cluster.cas.b32 %0, [%1], %2, %3;"
+               : "=r"(old) : "r"(addr), "r"(cmp), "r"(val) : "memory");
+  return old;
+}
+__device__ __forceinline__ void dsmem_or_u32(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+template <int kPolicy, bool kCas>
+__global__ void __launch_bounds__(1024, 1) cluster_pr_kernel(ClusterArgs a) {
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t me = cl.block_rank();
+  const uint32_t S = a.S;
+  extern __shared__ uint32_t s_dyn[];
+  // per CTA: cells[2][S] | lab0[S] | lab1[S] | rows[letters][S] | split[S] u8
+  uint32_t* s_cells = s_dyn;
+  uint32_t* s_lab0 = s_cells + 2 * S;
+  uint32_t* s_lab1 = s_lab0 + S;
+  uint32_t* s_rows = s_lab1 + S;
+  uint8_t* s_split = reinterpret_cast<uint8_t*>(s_rows + (uint64_t)a.letters * S);
+  __shared__ uint32_t s_changed[3];  // per-pass flags, rotating (see the reset below)
+  const uint64_t base = (uint64_t)me * S;
+  const uint32_t own = base >= a.n ? 0u : (uint32_t)(a.n - base < S ? a.n - base : S);
+  // MIN: cells hold q (empty ~0); MAX / arbitrary / CAS: q + 1 (empty 0)
+  const uint32_t empty = (!kCas && kPolicy == DFM_POLICY_MIN) ? 0xFFFFFFFFu : 0u;
+  const uint32_t* gin = a.start_sel ? a.lab1 : a.lab0;
+  for (uint32_t i = threadIdx.x; i < own; i += blockDim.x) {
+    s_cells[i] = empty;
+    s_cells[S + i] = empty;
+    s_lab0[i] = gin[base + i];
+    for (uint64_t c = 0; c < a.letters; ++c) s_rows[c * S + i] = a.rows[c * a.n + base + i];
+  }
+  if (threadIdx.x < 3) s_changed[threadIdx.x] = 0;
+  cl.sync();
+  auto rlab = [&](const uint32_t* local, uint32_t x) -> uint32_t {
+    return *(cl.map_shared_rank(local, x / S) + (x % S));
+  };
+  auto rrow = [&](uint64_t c, uint32_t x) -> uint32_t {
+    return *(cl.map_shared_rank(s_rows, x / S) + c * S + (x % S));
+  };
+  const uint32_t flag0 = dsmem_addr(s_changed, 0);
+  int sel = 0;  // local buffer holding the current labels (s_lab0 after the load)
+  uint32_t p = 0;
+  bool stable = false;
+  const uint32_t lane = threadIdx.x & 31;
+  while (p < a.max_passes) {
+    const uint32_t* cur = sel ? s_lab1 : s_lab0;
+    uint32_t* nxt = sel ? s_lab0 : s_lab1;
+    uint32_t* cells = s_cells + (p & 1) * S;
+    // pass p writes flag p % 3; flag (p + 1) % 3 was last read at the end of pass
+    // p - 2, which every CTA has left (two cluster barriers since)
+    if (me == 0 && threadIdx.x == 0) s_changed[(p + 1) % 3] = 0;
+    {  // the next pass's cells: last read in pass p - 1's split phase
+      uint32_t* nc = s_cells + ((p + 1) & 1) * S;
+      for (uint32_t i = threadIdx.x; i < own; i += blockDim.x) nc[i] = empty;
+    }
+    auto rcell = [&](uint32_t x) -> uint32_t { return dsmem_addr(cells + (x % S), x / S); };
+    bool any = false;
+    for (uint32_t ib = threadIdx.x & ~31u; ib < own; ib += blockDim.x) {
+      const uint32_t i = ib + lane;
+      const bool valid = i < own;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+      if (!valid) continue;
+      const uint32_t q = (uint32_t)(base + i);
+      const uint32_t leader = cur[i];
+      bool sp = false;
+      if (q != leader) {
+        for (uint64_t c0 = 0; c0 < a.letters && !sp; c0 += 4) {
+          uint32_t tq[4], tl[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + u < a.letters) {
+              tq[u] = s_rows[(c0 + u) * S + i];
+              tl[u] = rrow(c0 + u, leader);
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (c0 + u < a.letters) sp |= rlab(cur, tq[u]) != rlab(cur, tl[u]);
+        }
+      }
+      // warp-aggregated election (see elect_cell): consecutive lanes hold consecutive q
+      const uint32_t spm = __ballot_sync(vmask, sp);
+      if (kCas) {
+        any |= sp;
+        uint32_t win = leader;
+        if (sp) {
+          const uint32_t peers = __match_any_sync(spm, leader);
+          const uint32_t src = __ffs(peers) - 1;
+          uint32_t w = 0;
+          if (lane == src) {  // first CAS into an empty cell wins
+            const uint32_t prev = dsmem_cas_u32(rcell(leader), 0u, q + 1);
+            w = prev == 0u ? q : prev - 1;
+          }
+          win = __shfl_sync(peers, w, src);
+        }
+        nxt[i] = win;
+      } else {
+        s_split[i] = sp;
+        if (sp) {
+          const uint32_t peers = __match_any_sync(spm, leader);
+          const uint32_t src = kPolicy == DFM_POLICY_MAX ? 31 - __clz(peers) : __ffs(peers) - 1;
+          if (lane == src) {
+            if (kPolicy == DFM_POLICY_MIN) dsmem_min_u32(rcell(leader), q);
+            else if (kPolicy == DFM_POLICY_MAX) dsmem_max_u32(rcell(leader), q + 1);
+            else dsmem_st_u32(rcell(leader), q + 1);
+          }
+        }
+      }
+    }
+    if (!kCas) {
+      cl.sync();
+      for (uint32_t i = threadIdx.x; i < own; i += blockDim.x) {
+        const uint32_t c = cur[i];
+        if (s_split[i]) {
+          const uint32_t v = dsmem_ld_u32(rcell(c));
+          nxt[i] = kPolicy == DFM_POLICY_MIN ? v : v - 1;
+          any = true;
+        } else {
+          nxt[i] = c;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) dsmem_or_u32(flag0 + 4 * (p % 3), 1u);
+    cl.sync();
+    sel ^= 1;
+    ++p;
+    if (dsmem_ld_u32(flag0 + 4 * ((p - 1) % 3)) == 0u) {
+      stable = true;
+      break;
+    }
+  }
+  // labels back to global (the buffer the host expects next)
+  const uint32_t* fin = sel ? s_lab1 : s_lab0;
+  uint32_t* gout = ((a.start_sel + (int)p) & 1) ? a.lab1 : a.lab0;
+  for (uint32_t i = threadIdx.x; i < own; i += blockDim.x) gout[base + i] = fin[i];
+  if (me == 0 && threadIdx.x == 0) {
+    a.out[0] = p;
+    a.out[1] = stable ? 1u : 0u;
+    a.out[2] = (uint32_t)((a.start_sel + (int)p) & 1);
+  }
+  cl.sync();  // no CTA leaves while others may still read its shared memory
+}
+
 unsigned grid_for(const Ctx& ctx, uint64_t items) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
                                       (uint64_t)ctx.num_sms * 16);
@@ -306,6 +495,12 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 }  // namespace
 
 constexpr uint64_t kPersistentMaxStates = 1ull << 22;
+constexpr uint64_t kClusterMaxStates = 4096;
+
+bool cluster_disabled() {
+  const char* e = getenv("DFM_NAIVE_CLUSTER");
+  return e != nullptr && e[0] == '0';
+}
 
 AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uint64_t letters,
                             int policy, bool fused_cas, const Deadline& dl,
@@ -339,6 +534,66 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
   int sel = 0;
   uint32_t pass = 0;
   const bool tracing_ = trace && trace->on_pass;
+  // smallest cluster (<= 16 CTAs of ~200 KB) that holds the whole working set
+  const uint64_t per_state = 8 + 4 + 4 + 4 * letters + 1;  // cells x2, labels x2, rows, flag
+  const uint64_t kClusterSmem = 200ull << 10;
+  const uint32_t S_max = (uint32_t)std::min<uint64_t>(kClusterSmem / per_state, 1u << 20);
+  const uint32_t csize = (uint32_t)std::max<uint64_t>(1, ceil_div(n, std::max<uint32_t>(S_max, 1)));
+  // Measured (B200, tools/dbg_cluster_time.py): the cluster wins only while the
+  // instance fits one CTA — fib_dfa(17) (2,584 states, 2,583 passes) 7.7 vs 9.7 ms —
+  // and loses beyond (random 8e3 states: 17.3 vs 7.0 ms in one CTA, 2e4 states: 52.7 vs
+  // 18.4 ms over 3 CTAs): DSMEM random accesses and one SM's issue rate cap a pass
+  // long before the grid barriers do.  So: single-CTA instances of <= 4096 states.
+  if (!tracing_ && n <= kClusterMaxStates && csize == 1 && !cluster_disabled()) {
+    const uint32_t S = (uint32_t)ceil_div(n, csize);
+    const size_t smem = (size_t)S * per_state + 16;
+    void (*kern)(ClusterArgs) =
+        fused_cas ? cluster_pr_kernel<DFM_POLICY_ARBITRARY, true>
+        : policy == DFM_POLICY_MIN ? cluster_pr_kernel<DFM_POLICY_MIN, false>
+        : policy == DFM_POLICY_MAX ? cluster_pr_kernel<DFM_POLICY_MAX, false>
+                                   : cluster_pr_kernel<DFM_POLICY_ARBITRARY, false>;
+    DFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    uint32_t* cout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
+    const uint32_t kChunkMax = 1u << 16;
+    uint32_t chunk = 64;
+    while (true) {
+      if (dl.expired()) {
+        out.status = DFM_STATUS_TIMEOUT;
+        return out;
+      }
+      ClusterArgs ca{rows, n, letters, S, lab[0], lab[1], pass, chunk, sel, cout};
+      chunk = std::min(kChunkMax, chunk * 4);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(csize);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = ctx.stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = csize;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      ProfScope prof(ctx, "elect", 0);
+      DFM_CUDA(cudaLaunchKernelEx(&cfg, kern, ca));
+      DFM_LAUNCH_CHECK();
+      prof.stop();
+      DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, cout, 12, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(ctx.h_scalars + 20);
+      prof.bytes = (uint64_t)h[0] * pass_bytes;
+      pass += h[0];
+      sel = (int)h[2];
+      if (h[1]) break;
+    }
+    out.iterations = pass;
+    out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+    out.num_blocks = canonicalize_dev(ctx, lab[sel], n, out.canon_dev);
+    out.status = DFM_STATUS_OK;
+    return out;
+  }
   if (!tracing_ && n <= kPersistentMaxStates) {
     // one cooperative launch per chunk of passes; the deadline is checked between
     // chunks (the reference checks it before every pass, min_partref.hpp:78-83), so
