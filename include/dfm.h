@@ -233,10 +233,19 @@ int dfm_gen_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double accept_prob
 int dfm_shard_signature(dfm_ctx* ctx, const void* delta_local, uint64_t n_local, uint32_t k,
                         const void* block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
                         void* keys_out, void* sig_out, void* dest_out);
+/* Same with the block vector at id_bytes = 1/2/4 per state (all-gathered at the
+ * narrowest width that holds B ids) and, when pack_bits > 0 ((k+1)*pack_bits <= 63),
+ * EXACT packed keys (block, successor ids) + 1 instead of hashes: sig_out is then
+ * not written (may be NULL) and the grouping needs no verification (words = 0). */
+int dfm_shard_signature_ex(dfm_ctx* ctx, const void* delta_local, uint64_t n_local, uint32_t k,
+                           const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                           uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
+                           void* dest_out);
 /* Exact grouping of `count` received (key, signature-row) pairs: label_out[i] = dense
  * local group id in [0, *groups_out).  Equal-hash members are verified word by word
- * against the group's first member; *collision_out = 1 when two different rows share a
- * key (the driver then redoes the pass under another seed). */
+ * against the group's first member (words = 0: exact keys, no rows, sig may be NULL);
+ * *collision_out = 1 when two different rows share a key (the driver then redoes the
+ * pass under another seed). */
 int dfm_shard_group(dfm_ctx* ctx, const void* keys, const void* sig, uint32_t words,
                     uint64_t count, void* label_out, uint64_t* groups_out, int* collision_out);
 /* In-place stable LSD radix sort of (u64 key, u32 value) pairs on the low `bits` bits. */

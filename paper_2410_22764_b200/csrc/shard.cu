@@ -26,6 +26,45 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Exact packed keys while (k+1) * bits(B-1) <= 63 (the early passes): no signature
+// rows to route or verify; ids are read from the all-gathered block vector at its
+// narrow width (1/2/4 bytes while B <= 2^8 / 2^16 / 2^32)
+template <typename Id>
+__global__ void __launch_bounds__(256) shard_packed_kernel(
+    const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k, const Id* __restrict__ block_full,
+    uint64_t lo, uint32_t w, uint32_t ranks, unsigned long long* __restrict__ keys,
+    uint32_t* __restrict__ dest) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += stride) {
+    unsigned long long key = block_full[lo + i];
+    for (uint32_t a = 0; a < k; ++a) key = (key << w) | block_full[delta[(uint64_t)a * n_local + i]];
+    keys[i] = key + 1ull;  // never 0: 0 marks an empty table slot
+    dest[i] = (uint32_t)__umul64hi(mix64(key ^ 0xD1B54A32D192ED03ull), ranks);
+  }
+}
+
+template <typename Id>
+__global__ void __launch_bounds__(256) shard_sig_kernel_w(
+    const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k,
+    const Id* __restrict__ block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
+    unsigned long long* __restrict__ keys, uint32_t* __restrict__ sig,
+    uint32_t* __restrict__ dest) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += stride) {
+    const uint32_t b = block_full[lo + i];
+    uint32_t* row = sig + i * (uint64_t)(k + 1);
+    row[0] = b;
+    unsigned long long h = mix64(seed * kGolden + b);
+    for (uint32_t a = 0; a < k; ++a) {
+      const uint32_t s = block_full[delta[(uint64_t)a * n_local + i]];
+      row[a + 1] = s;
+      h = mix64(h + kGolden + s);
+    }
+    keys[i] = h | 1ull;
+    dest[i] = (uint32_t)__umul64hi(mix64(h ^ 0xD1B54A32D192ED03ull), ranks);
+  }
+}
+
 __global__ void __launch_bounds__(256) shard_sig_kernel(
     const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k,
     const uint32_t* __restrict__ block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
@@ -53,60 +92,189 @@ struct GSlot {
   uint32_t gid;
 };
 
-__global__ void __launch_bounds__(256) group_insert_kernel(const unsigned long long* __restrict__ keys,
-                                                           uint64_t count, GSlot* slots,
-                                                           uint64_t cap, uint32_t* __restrict__ slot_of) {
+// Grouping of the received keys (64-bit signature hashes, never 0) — the hash
+// engine's recipe (sortpr_hash.cu): a two-level uniqueness filter (2-bit cells,
+// 64 MB, L2-resident) lets keys that are alone in their cell skip the table;
+// the rest goes through an open-addressing table at load <= 0.4; group ids come
+// from one atomic per CTA step (no global scan).
+constexpr uint32_t kUniq = 0xFFFFFFFFu;
+constexpr int kCellBits = 28;
+constexpr uint64_t kFilterMin = 1ull << 22;
+
+__device__ __forceinline__ uint64_t cell_of(unsigned long long key, int level) {
+  return (key >> (level == 0 ? 64 - kCellBits : 8)) & ((1ull << kCellBits) - 1);
+}
+
+__global__ void __launch_bounds__(256) gfilt_set_kernel(const unsigned long long* __restrict__ keys,
+                                                        uint64_t count, uint32_t* F, int level,
+                                                        const uint32_t* __restrict__ slot_of) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const unsigned long long key = keys[i];
-    uint64_t t = __umul64hi(key, cap);
-    while (true) {
-      const unsigned long long cur = atomicCAS(&slots[t].key, 0ull, key);
-      if (cur == 0ull || cur == key) break;
-      if (++t == cap) t = 0;
-    }
-    slot_of[i] = (uint32_t)t;
-    atomicMax(&slots[t].rep, ~(uint32_t)i);
+    if (level > 0 && slot_of[i] == kUniq) continue;
+    const uint64_t c = cell_of(keys[i], level);
+    const uint32_t bit = (uint32_t)(c & 15) * 2;
+    // test before set: heavily repeated keys (early passes) would serialise their
+    // atomics on a few cells; a cell already marked "seen twice" needs no update
+    if (((*reinterpret_cast<volatile uint32_t*>(&F[c >> 4]) >> bit) & 3u) == 3u) continue;
+    const uint32_t old = atomicOr(&F[c >> 4], 1u << bit);
+    if ((old >> bit) & 1u) atomicOr(&F[c >> 4], 2u << bit);
   }
 }
 
-struct GroupIn {
-  const GSlot* slots;
-  const uint32_t* slot_of;
-  const uint32_t* sig;
-  uint32_t words;
-  unsigned long long* collision;
-  __device__ uint32_t operator()(uint64_t i) const {
-    const uint32_t rep = ~slots[slot_of[i]].rep;
-    if (rep == (uint32_t)i) return 1u;
-    const uint32_t* a = sig + i * (uint64_t)words;
-    const uint32_t* b = sig + (uint64_t)rep * words;
-    for (uint32_t x = 0; x < words; ++x)
-      if (a[x] != b[x]) {
-        atomicOr(collision, 1ull);
-        break;
-      }
-    return 0u;
+__global__ void __launch_bounds__(256) gfilt_mark_kernel(const unsigned long long* __restrict__ keys,
+                                                         uint64_t count, const uint32_t* __restrict__ F,
+                                                         int level, uint32_t* __restrict__ slot_of,
+                                                         unsigned long long* dups) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t mine = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (level > 0 && slot_of[i] == kUniq) continue;
+    const uint64_t c = cell_of(keys[i], level);
+    const bool dup = (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
+    slot_of[i] = dup ? 0u : kUniq;
+    mine += dup ? 1u : 0u;
   }
-};
-struct GroupOut {
-  GSlot* slots;
-  const uint32_t* slot_of;
-  uint32_t* label;
-  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
-    if (v) {
-      slots[slot_of[i]].gid = excl;
-      label[i] = excl;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(dups, (unsigned long long)mine);
+}
+
+// Insert with CTA-level pre-aggregation: a tile's keys first meet in a shared-memory
+// table, and each distinct key of the tile costs one global CAS + one atomicMax —
+// early passes have a handful of keys over 1e8 items, and per-item atomics on the
+// same few slots would serialise.  Keys that do not fit the tile table go straight
+// to the global table.
+constexpr int kTileItems = 2048;
+constexpr int kTileTable = 2048;
+
+__device__ __forceinline__ uint64_t global_insert(GSlot* slots, uint64_t cap,
+                                                  unsigned long long key) {
+  uint64_t t = __umul64hi(mix64(key), cap);
+  while (true) {
+    const unsigned long long cur = atomicCAS(&slots[t].key, 0ull, key);
+    if (cur == 0ull || cur == key) return t;
+    if (++t == cap) t = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) group_insert_kernel(const unsigned long long* __restrict__ keys,
+                                                           uint64_t count, GSlot* slots,
+                                                           uint64_t cap, uint32_t* __restrict__ slot_of) {
+  __shared__ unsigned long long s_key[kTileTable];
+  __shared__ uint32_t s_min[kTileTable];
+  __shared__ uint32_t s_gslot[kTileTable];
+  constexpr int kPer = kTileItems / 256;
+  for (uint64_t base = (uint64_t)blockIdx.x * kTileItems; base < count;
+       base += (uint64_t)gridDim.x * kTileItems) {
+    for (int t = threadIdx.x; t < kTileTable; t += blockDim.x) {
+      s_key[t] = 0;
+      s_min[t] = 0xFFFFFFFFu;
     }
+    __syncthreads();
+    int ent[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint64_t i = base + u * 256 + threadIdx.x;
+      ent[u] = -2;  // -2: nothing to do, -1: global path, >= 0: tile entry
+      if (i >= count || slot_of[i] == kUniq) continue;
+      const unsigned long long key = keys[i];
+      uint32_t t = (uint32_t)mix64(key) & (kTileTable - 1);
+      ent[u] = -1;
+      for (int probe = 0; probe < 16; ++probe) {
+        const unsigned long long cur = atomicCAS(&s_key[t], 0ull, key);
+        if (cur == 0ull || cur == key) {
+          ent[u] = (int)t;
+          atomicMin(&s_min[t], (uint32_t)i);
+          break;
+        }
+        t = (t + 1) & (kTileTable - 1);
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kTileTable; t += blockDim.x)
+      if (s_key[t] != 0ull) {
+        const uint64_t g = global_insert(slots, cap, s_key[t]);
+        atomicMax(&slots[g].rep, ~s_min[t]);
+        s_gslot[t] = (uint32_t)g;
+      }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const uint64_t i = base + u * 256 + threadIdx.x;
+      if (ent[u] >= 0) {
+        slot_of[i] = s_gslot[ent[u]];
+      } else if (ent[u] == -1) {
+        const uint64_t g = global_insert(slots, cap, keys[i]);
+        atomicMax(&slots[g].rep, ~(uint32_t)i);
+        slot_of[i] = (uint32_t)g;
+      }
+    }
+    __syncthreads();
   }
-};
+}
+
+// a member is the representative of its group if it is alone (filter) or the table's
+// minimum; representatives take an id from one atomic per CTA step
+__global__ void __launch_bounds__(256) group_label_kernel(uint64_t count, GSlot* slots,
+                                                          const uint32_t* __restrict__ slot_of,
+                                                          const uint32_t* __restrict__ sig,
+                                                          uint32_t words, uint32_t* __restrict__ label,
+                                                          unsigned long long* groups,
+                                                          unsigned long long* collision) {
+  __shared__ uint32_t s_cnt[8];
+  __shared__ uint32_t s_first;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < count; base += stride) {
+    const uint64_t i = base + threadIdx.x;
+    bool rep = false;
+    uint32_t s = kUniq;
+    if (i < count) {
+      s = slot_of[i];
+      if (s == kUniq) {
+        rep = true;
+      } else {
+        const uint32_t r = ~slots[s].rep;
+        rep = r == (uint32_t)i;
+        if (!rep && words > 0) {  // equal hash: verify the whole signature vs the representative
+          const uint32_t* a = sig + i * (uint64_t)words;
+          const uint32_t* b = sig + (uint64_t)r * words;
+          for (uint32_t x = 0; x < words; ++x)
+            if (a[x] != b[x]) {
+              atomicOr(collision, 1ull);
+              break;
+            }
+        }
+      }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, rep);
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int g = 0; g < 8; ++g) t += s_cnt[g];
+      s_first = t ? (uint32_t)atomicAdd(groups, (unsigned long long)t) : 0u;
+    }
+    __syncthreads();
+    uint32_t off = s_first;
+    for (uint32_t g = 0; g < warp; ++g) off += s_cnt[g];
+    if (rep) {
+      const uint32_t gid = off + __popc(m & ((1u << lane) - 1u));
+      label[i] = gid;
+      if (s != kUniq) slots[s].gid = gid;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void group_members_kernel(uint64_t count, const GSlot* __restrict__ slots,
                                      const uint32_t* __restrict__ slot_of,
                                      uint32_t* __restrict__ label) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    const GSlot& s = slots[slot_of[i]];
-    if (~s.rep != (uint32_t)i) label[i] = s.gid;
+    const uint32_t s = slot_of[i];
+    if (s == kUniq) continue;
+    if (~slots[s].rep != (uint32_t)i) label[i] = slots[s].gid;
   }
 }
 
@@ -176,25 +344,97 @@ int dfm_shard_signature(dfm_ctx* c, const void* delta_local, uint64_t n_local, u
   });
 }
 
+int dfm_shard_signature_ex(dfm_ctx* c, const void* delta_local, uint64_t n_local, uint32_t k,
+                           const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                           uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
+                           void* dest_out) {
+  return guarded_shard(c, [&](Ctx& ctx) {
+    if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
+    if (id_bytes != 1 && id_bytes != 2 && id_bytes != 4)
+      throw Error(DFM_ERR_INVALID, "id_bytes must be 1, 2 or 4");
+    if (pack_bits && (uint64_t)(k + 1) * pack_bits > 63)
+      throw Error(DFM_ERR_INVALID, "packed key does not fit 63 bits");
+    if (n_local == 0) return;
+    const auto* d = static_cast<const uint32_t*>(delta_local);
+    auto* keys = static_cast<unsigned long long*>(keys_out);
+    auto* dest = static_cast<uint32_t*>(dest_out);
+    const unsigned g = grid_for(ctx, n_local);
+    if (pack_bits) {
+      ProfScope p(ctx, "sig", n_local * (4ull * k + (uint64_t)id_bytes * (k + 1) + 8 + 4));
+      if (id_bytes == 1)
+        shard_packed_kernel<uint8_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint8_t*>(block_full), lo, pack_bits, ranks, keys, dest);
+      else if (id_bytes == 2)
+        shard_packed_kernel<uint16_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint16_t*>(block_full), lo, pack_bits, ranks, keys,
+            dest);
+      else
+        shard_packed_kernel<uint32_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint32_t*>(block_full), lo, pack_bits, ranks, keys,
+            dest);
+    } else {
+      auto* sig = static_cast<uint32_t*>(sig_out);
+      ProfScope p(ctx, "sig", n_local * (4ull * k + (uint64_t)id_bytes * (k + 1) + 8 +
+                                         4ull * (k + 1) + 4));
+      if (id_bytes == 1)
+        shard_sig_kernel_w<uint8_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint8_t*>(block_full), lo, seed, ranks, keys, sig, dest);
+      else if (id_bytes == 2)
+        shard_sig_kernel_w<uint16_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint16_t*>(block_full), lo, seed, ranks, keys, sig,
+            dest);
+      else
+        shard_sig_kernel_w<uint32_t><<<g, 256, 0, ctx.stream>>>(
+            d, n_local, k, static_cast<const uint32_t*>(block_full), lo, seed, ranks, keys, sig,
+            dest);
+    }
+    DFM_LAUNCH_CHECK();
+  });
+}
+
 int dfm_shard_group(dfm_ctx* c, const void* keys, const void* sig, uint32_t words, uint64_t count,
                     void* label_out, uint64_t* groups_out, int* collision_out) {
   return guarded_shard(c, [&](Ctx& ctx) {
     if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "too many items for one rank");
-    uint64_t* sc = ctx.d_scalars + 48;  // [0] groups [1] collision
-    DFM_CUDA(cudaMemsetAsync(sc, 0, 16, ctx.stream));
+    uint64_t* sc = ctx.d_scalars + 48;  // [0] groups [1] collision [2] filter duplicates
+    DFM_CUDA(cudaMemsetAsync(sc, 0, 24, ctx.stream));
     if (count > 0) {
-      const uint64_t cap = std::max<uint64_t>(1024, count + count / 2);
-      auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
       uint32_t* slot_of = ctx.slot_t<uint32_t>("shard.slotof", count);
-      DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
+      uint64_t dups = count;
       ProfScope p(ctx, "group", count * (8ull + 16 + 4 + 4 + 4 + 4ull * words));
-      group_insert_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+      if (count >= kFilterMin) {
+        uint32_t* F = ctx.slot_t<uint32_t>("shard.filter", 1ull << (kCellBits - 4));
+        for (int level = 0; level < 2 && dups >= kFilterMin; ++level) {
+          DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kCellBits - 2), ctx.stream));
+          DFM_CUDA(cudaMemsetAsync(sc + 2, 0, 8, ctx.stream));
+          gfilt_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+              static_cast<const unsigned long long*>(keys), count, F, level, slot_of);
+          DFM_LAUNCH_CHECK();
+          gfilt_mark_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+              static_cast<const unsigned long long*>(keys), count, F, level, slot_of,
+              reinterpret_cast<unsigned long long*>(sc + 2));
+          DFM_LAUNCH_CHECK();
+          DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 50, sc + 2, 8, cudaMemcpyDeviceToHost,
+                                   ctx.stream));
+          ctx.sync();
+          dups = ctx.h_scalars[50];
+        }
+      } else {
+        DFM_CUDA(cudaMemsetAsync(slot_of, 0, count * 4, ctx.stream));
+      }
+      const uint64_t cap = std::max<uint64_t>(1024, dups * 5 / 2);  // load <= 0.4
+      auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
+      DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
+      group_insert_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(count, kTileItems),
+                                                         ctx.num_sms * 8ull),
+                            256, 0, ctx.stream>>>(
           static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
       DFM_LAUNCH_CHECK();
-      prims::lookback_scan(ctx, "sc.shard", count,
-                           GroupIn{slots, slot_of, static_cast<const uint32_t*>(sig), words,
-                                   reinterpret_cast<unsigned long long*>(sc + 1)},
-                           GroupOut{slots, slot_of, static_cast<uint32_t*>(label_out)}, sc);
+      group_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+          count, slots, slot_of, static_cast<const uint32_t*>(sig), words,
+          static_cast<uint32_t*>(label_out), reinterpret_cast<unsigned long long*>(sc),
+          reinterpret_cast<unsigned long long*>(sc + 1));
+      DFM_LAUNCH_CHECK();
       group_members_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
           count, slots, slot_of, static_cast<uint32_t*>(label_out));
       DFM_LAUNCH_CHECK();

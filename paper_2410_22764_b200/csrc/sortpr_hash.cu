@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(256) filt_set_kernel(const unsigned long long*
     const uint64_t c = (table_hash(ld_key_stream(keys + i, pol_stream), hashed, seed) >> shift) &
                        ((1ull << kFilterCellBits) - 1);
     const uint32_t b = (uint32_t)(c & 15) * 2;
+    // test before set: a cell already marked "seen twice" needs no atomic (repeated keys)
+    if (((*reinterpret_cast<volatile uint32_t*>(&F[c >> 4]) >> b) & 3u) == 3u) continue;
     const uint32_t old = atom_or_keep(&F[c >> 4], 1u << b, pol_keep);
     if ((old >> b) & 1u) atom_or_keep(&F[c >> 4], 2u << b, pol_keep);
   }

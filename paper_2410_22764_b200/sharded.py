@@ -44,9 +44,16 @@ class Comm:
         return t.cpu() if self.stage else t
 
     def all_gather(self, t: torch.Tensor, counts) -> torch.Tensor:
-        """Concatenate every rank's `t` (rank r contributes counts[r] elements)."""
+        """Concatenate every rank's `t` (rank r contributes counts[r] elements).  Narrow
+        id vectors (uint8 / int16) travel as they are over NCCL (int16 as byte pairs);
+        gloo (the CPU tests) lacks those types and gets int32."""
         if self.world == 1:
             return t
+        if t.dtype in (torch.uint8, torch.int16) and self.stage:
+            return self.all_gather(t.to(torch.int32), counts).to(t.dtype)
+        if t.dtype == torch.int16:
+            b = self.all_gather(t.contiguous().view(torch.uint8), [2 * int(c) for c in counts])
+            return b.view(torch.int16)
         width = int(max(counts))  # collectives need equal sizes: pad, gather, trim
         src = self._to(t)
         if src.numel() < width:
@@ -89,12 +96,15 @@ class CudaShardOps:
         lib = self.lib
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         lib.dfm_shard_signature.argtypes = [vp, vp, u64, u32, vp, u64, u64, u32, vp, vp, vp]
+        lib.dfm_shard_signature_ex.argtypes = [vp, vp, u64, u32, vp, u32, u64, u64, u32, u32, vp,
+                                                vp, vp]
         lib.dfm_shard_group.argtypes = [vp, vp, vp, u32, u64, vp, C.POINTER(u64),
                                         C.POINTER(C.c_int)]
         lib.dfm_sort_pairs.argtypes = [vp, vp, vp, u64, u32]
         lib.dfm_canonicalize_dev.argtypes = [vp, vp, u64, vp, C.POINTER(u32)]
         lib.dfm_random_dfa_slice_dev.argtypes = [vp, u64, u32, u64, C.c_double, u64, u64, vp, vp]
-        for f in ("dfm_shard_signature", "dfm_shard_group", "dfm_sort_pairs",
+        for f in ("dfm_shard_signature", "dfm_shard_signature_ex", "dfm_shard_group",
+                  "dfm_sort_pairs",
                   "dfm_canonicalize_dev", "dfm_random_dfa_slice_dev"):
             getattr(lib, f).restype = C.c_int
 
@@ -102,22 +112,29 @@ class CudaShardOps:
     def device(self):
         return torch.device("cuda", self.eng.device)
 
-    def signature(self, delta_local, block_full, lo: int, seed: int, ranks: int):
+    def signature(self, delta_local, block_full, lo: int, seed: int, ranks: int,
+                  pack_bits: int = 0):
+        """Keys of the owned states; pack_bits > 0: exact packed keys, no rows (sig None).
+        block_full may be uint8 / int16 / int32 (the narrowest width holding the ids)."""
         k, n_local = delta_local.shape
         keys = torch.empty(n_local, dtype=torch.int64, device=self.device)
-        sig = torch.empty((n_local, k + 1), dtype=torch.int32, device=self.device)
+        sig = None if pack_bits else torch.empty((n_local, k + 1), dtype=torch.int32,
+                                                 device=self.device)
         dest = torch.empty(n_local, dtype=torch.int32, device=self.device)
-        self.eng._check(self.lib.dfm_shard_signature(
-            self.eng.handle, delta_local.data_ptr(), n_local, k, block_full.data_ptr(), lo,
-            seed & (2 ** 64 - 1), ranks, keys.data_ptr(), sig.data_ptr(), dest.data_ptr()))
+        self.eng._check(self.lib.dfm_shard_signature_ex(
+            self.eng.handle, delta_local.data_ptr(), n_local, k, block_full.data_ptr(),
+            block_full.element_size(), lo, seed & (2 ** 64 - 1), ranks, pack_bits,
+            keys.data_ptr(), sig.data_ptr() if sig is not None else None, dest.data_ptr()))
         return keys, sig, dest
 
     def route(self, dest, ranks: int):
-        """Stable order of items by destination rank + per-rank counts."""
+        """Stable order of items by destination rank + per-rank counts (None = identity
+        order at one rank).  Counts come from one reduction per rank: a bincount over a
+        handful of bins serialises its atomics on a few addresses."""
         n = dest.numel()
-        counts = torch.bincount(dest.long(), minlength=ranks).cpu().tolist()
         if ranks == 1 or n == 0:
-            return torch.arange(n, dtype=torch.int64, device=self.device), counts
+            return None, [n] + [0] * (ranks - 1)
+        counts = torch.stack([(dest == r).sum() for r in range(ranks)]).cpu().tolist()
         keys = dest.to(torch.int64).contiguous()
         order = torch.arange(n, dtype=torch.int32, device=self.device)
         bits = max(1, (ranks - 1).bit_length())
@@ -126,11 +143,13 @@ class CudaShardOps:
         return order.long(), counts
 
     def group(self, keys, sig):
-        n, words = sig.shape
+        n = keys.numel()
+        words = sig.shape[1] if sig is not None else 0
         label = torch.empty(n, dtype=torch.int32, device=self.device)
         groups = C.c_uint64(0)
         coll = C.c_int(0)
-        self.eng._check(self.lib.dfm_shard_group(self.eng.handle, keys.data_ptr(), sig.data_ptr(),
+        self.eng._check(self.lib.dfm_shard_group(self.eng.handle, keys.data_ptr(),
+                                                 sig.data_ptr() if sig is not None else None,
                                                  words, n, label.data_ptr(), C.byref(groups),
                                                  C.byref(coll)))
         return label, int(groups.value), bool(coll.value)
@@ -166,9 +185,11 @@ def shard_bounds(n_total: int, world: int, rank: int):
 
 
 def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total: int, lo: int,
-                    comm: Comm, ops, max_passes: int | None = None) -> ShardedResult:
+                    comm: Comm, ops, max_passes: int | None = None,
+                    allow_packed: bool = True) -> ShardedResult:
     """sortPR over state shards.  delta_local: (k, n_local) int32 global targets;
-    acc_local: (n_local,) uint8.  Returns this rank's canonical labels."""
+    acc_local: (n_local,) uint8.  Returns this rank's canonical labels.
+    allow_packed=False keeps hashed keys + verification in every pass (tests)."""
     world, rank = comm.world, comm.rank
     k, n_local = delta_local.shape
     sizes = [hi - lo_ for lo_, hi in (shard_bounds(n_total, world, r) for r in range(world))]
@@ -183,12 +204,22 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
     while True:
         if max_passes is not None and iterations >= max_passes:
             break
-        block_full = comm.all_gather(block, sizes)
-        keys, sig, dest = ops.signature(delta_local, block_full, lo, seed, world)
+        # ids travel at the narrowest width holding B values; while the whole key
+        # (block, k successor ids) fits 63 bits it is packed exactly (no rows)
+        w = max(1, (B - 1).bit_length())
+        pack = w if allow_packed and (k + 1) * w <= 63 else 0
+        narrow = torch.uint8 if B <= 256 else torch.int16 if B <= 65536 else torch.int32
+        block_full = comm.all_gather(block.to(narrow), sizes)
+        keys, sig, dest = ops.signature(delta_local, block_full, lo, seed, world, pack)
         order, send_counts = ops.route(dest, world)
-        recv_counts = [c[rank] for c in comm.all_gather_ints(send_counts)]
-        rkeys = comm.all_to_all(keys[order], send_counts, recv_counts)
-        rsig = comm.all_to_all(sig[order], send_counts, recv_counts)
+        if order is None:  # one rank: every key is grouped here, in place
+            recv_counts = send_counts
+            rkeys, rsig = keys, sig
+        else:
+            recv_counts = [c[rank] for c in comm.all_gather_ints(send_counts)]
+            rkeys = comm.all_to_all(keys[order], send_counts, recv_counts)
+            rsig = (comm.all_to_all(sig[order], send_counts, recv_counts)
+                    if sig is not None else None)
         label, groups, collision = ops.group(rkeys, rsig)
         stats = comm.all_gather_ints([groups, int(collision)])
         if any(s[1] for s in stats):  # a collision on any rank voids the pass everywhere
@@ -197,9 +228,12 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
             continue
         offset = sum(s[0] for s in stats[:rank])
         B_new = sum(s[0] for s in stats)
-        back = comm.all_to_all(label + offset, recv_counts, send_counts)
-        new_block = torch.empty_like(block)
-        new_block[order] = back.to(new_block.dtype)
+        if order is None:
+            new_block = (label + offset).to(block.dtype)
+        else:
+            back = comm.all_to_all(label + offset, recv_counts, send_counts)
+            new_block = torch.empty_like(block)
+            new_block[order] = back.to(new_block.dtype)
         iterations += 1
         block = new_block
         if B_new == B:  # fixpoint, min_sort.hpp:111-117

@@ -21,10 +21,20 @@ class CpuShardOps:
     def __init__(self, weak_first_seed: bool = False):
         self.weak = weak_first_seed
 
-    def signature(self, delta_local, block_full, lo, seed, ranks):
+    def signature(self, delta_local, block_full, lo, seed, ranks, pack_bits=0):
         d = delta_local.numpy().astype(np.int64)
-        bf = block_full.numpy()
+        bf = block_full.numpy().astype(np.int64) & 0xFFFFFFFF  # int16 ids arrive signed
+        if block_full.dtype == torch.int16:
+            bf = bf & 0xFFFF
         n = d.shape[1]
+        if pack_bits:  # exact packed key + 1, no rows
+            key = bf[lo:lo + n].astype(np.uint64)
+            for a in range(d.shape[0]):
+                key = (key << np.uint64(pack_bits)) | bf[d[a]].astype(np.uint64)
+            with np.errstate(over="ignore"):
+                dest = (_mix(key ^ np.uint64(0xD1B54A32D192ED03)) % np.uint64(ranks)).astype(np.int32)
+            return (torch.from_numpy((key + np.uint64(1)).view(np.int64).copy()), None,
+                    torch.from_numpy(dest))
         rows = np.empty((n, d.shape[0] + 1), np.uint32)
         rows[:, 0] = bf[lo:lo + n]
         for a in range(d.shape[0]):
@@ -49,10 +59,12 @@ class CpuShardOps:
         if keys.numel() == 0:
             return torch.empty(0, dtype=torch.int32), 0, False
         k = keys.numpy()
-        rows = sig.numpy()
         _, first, inv = np.unique(k, return_index=True, return_inverse=True)
-        # collision: some key carries two different rows
-        collision = bool((rows != rows[first][inv]).any())
+        # collision: some key carries two different rows (exact packed keys: none)
+        collision = False
+        if sig is not None:
+            rows = sig.numpy()
+            collision = bool((rows != rows[first][inv]).any())
         order = np.argsort(first, kind="stable")
         rank = np.empty_like(order)
         rank[order] = np.arange(order.size)

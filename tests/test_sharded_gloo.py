@@ -33,8 +33,11 @@ def _worker(rank, world, port, cases, weak, q):
     for delta, acc in cases:
         n = acc.size
         lo, hi = shard_bounds(n, world, rank)
+        # the forced-collision run keeps hashed keys in every pass (packed exact keys
+        # of the early passes cannot collide)
         r = sharded_sort_pr(torch.from_numpy(delta[:, lo:hi].astype(np.int32)),
-                            torch.from_numpy(acc[lo:hi]), n, lo, Comm(), CpuShardOps(weak))
+                            torch.from_numpy(acc[lo:hi]), n, lo, Comm(), CpuShardOps(weak),
+                            allow_packed=not weak)
         out.append((lo, r.block_local.numpy().copy(), r.num_blocks, r.iterations, r.retries))
     q.put((rank, out))
     dist.destroy_process_group()
