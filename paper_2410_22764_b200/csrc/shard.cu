@@ -402,7 +402,9 @@ int dfm_shard_group(dfm_ctx* c, const void* keys, const void* sig, uint32_t word
       uint32_t* slot_of = ctx.slot_t<uint32_t>("shard.slotof", count);
       uint64_t dups = count;
       ProfScope p(ctx, "group", count * (8ull + 16 + 4 + 4 + 4 + 4ull * words));
-      if (count >= kFilterMin) {
+      // the filter pays off for hashed keys (late, mostly-distinct passes); exact packed
+      // keys belong to the early passes, where a few keys repeat over all items
+      if (count >= kFilterMin && words > 0) {
         uint32_t* F = ctx.slot_t<uint32_t>("shard.filter", 1ull << (kCellBits - 4));
         for (int level = 0; level < 2 && dups >= kFilterMin; ++level) {
           DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kCellBits - 2), ctx.stream));

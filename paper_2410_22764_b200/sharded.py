@@ -239,6 +239,11 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
         if B_new == B:  # fixpoint, min_sort.hpp:111-117
             break
         B = B_new
+        if B == n_total:
+            # every block is a singleton: the next pass sees n distinct keys (each holds
+            # its own block id), grows nothing and ends the loop — count it, skip it
+            iterations += 1
+            break
     block_full = comm.all_gather(block, sizes)
     canon, nb = ops.canonicalize(block_full)
     return ShardedResult(canon[lo:lo + n_local].clone(), nb, iterations, retries)
