@@ -70,6 +70,7 @@ struct InsertParams {
   // (bitmap + per-word exclusive popcount); no same-slot warp aggregation
   const uint32_t* present;
   const uint32_t* present_pre;
+  const uint32_t* cand;  // filtered passes: the states left for the table (m = their count)
 };
 
 // L2 eviction policies: the delta stream is read once per pass (evict first) so
@@ -209,10 +210,14 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
     bool valid[2];
     bool merge[2] = {!kHashed, !kHashed};  // slot needs the aggregated rep/info update
 #pragma unroll
+    uint64_t idx[2];
+#pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const uint64_t i = base + u * 32 + lane;
-      // filtered passes: states whose key the filter saw once are singleton groups
-      valid[u] = i < p.m && (!kFilter || p.slot_of[i] != kUnique);
+      const uint64_t j = base + u * 32 + lane;
+      // filtered passes iterate the candidate list (keys the filter saw repeated)
+      valid[u] = j < p.m;
+      idx[u] = kFilter ? (valid[u] ? p.cand[j] : 0) : j;
+      const uint64_t i = idx[u];
       if (valid[u]) {
         const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
         lead[u] = p.lead[q];
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const uint64_t i = base + u * 32 + lane;
+      const uint64_t i = idx[u];
       if (valid[u]) {
         if (kDirect) {
           if (p.present) {
@@ -275,11 +280,13 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       }
       const uint32_t vmask = __ballot_sync(0xffffffffu, valid[u] && merge[u]);
       if (valid[u] && merge[u]) {
-        // lanes with the same slot: the lowest lane (smallest i) updates for all
+        // lanes with the same slot: the lowest lane updates for all, with the group's
+        // minimum state (candidate lists are not in ascending order)
         const uint32_t peers = __match_any_sync(vmask, (unsigned long long)s[u]);
         const uint32_t leads = __ballot_sync(vmask, lead[u] != 0) & peers;
+        const uint32_t imin = __reduce_min_sync(peers, (uint32_t)i);
         if (lane == (uint32_t)(__ffs(peers) - 1)) {
-          atomicMax(&p.slots[s[u]].rep, ~(uint32_t)i);
+          atomicMax(&p.slots[s[u]].rep, ~imin);
           atomicAdd(&p.slots[s[u]].info, (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u));
         }
       }
@@ -388,44 +395,54 @@ __device__ __forceinline__ uint32_t atom_or_keep(uint32_t* a, uint32_t v, uint64
 __global__ void __launch_bounds__(256) filt_set_kernel(const unsigned long long* __restrict__ keys,
                                                        uint64_t m, bool hashed, uint64_t seed,
                                                        uint32_t* F, int level,
-                                                       const uint32_t* __restrict__ slot_of) {
+                                                       const uint32_t* __restrict__ cand) {
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
   const int shift = level == 0 ? 64 - kFilterCellBits : 8;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    if (level > 0 && slot_of[i] == kUnique) continue;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint64_t i = cand ? cand[j] : j;  // level 1: the candidates level 0 left
     const uint64_t c = (table_hash(ld_key_stream(keys + i, pol_stream), hashed, seed) >> shift) &
                        ((1ull << kFilterCellBits) - 1);
     const uint32_t b = (uint32_t)(c & 15) * 2;
-    // test before set: a cell already marked "seen twice" needs no atomic (repeated keys)
-    if (((*reinterpret_cast<volatile uint32_t*>(&F[c >> 4]) >> b) & 3u) == 3u) continue;
     const uint32_t old = atom_or_keep(&F[c >> 4], 1u << b, pol_keep);
     if ((old >> b) & 1u) atom_or_keep(&F[c >> 4], 2u << b, pol_keep);
   }
 }
 
+// mark: keys alone in their cell leave (slot_of = kUnique), the others stay candidates
 __global__ void __launch_bounds__(256) filt_mark_kernel(const unsigned long long* __restrict__ keys,
                                                         uint64_t m, bool hashed, uint64_t seed,
                                                         const uint32_t* __restrict__ F,
-                                                        uint32_t* __restrict__ slot_of,
-                                                        unsigned long long* dups, int level) {
+                                                        uint32_t* __restrict__ slot_of, int level,
+                                                        const uint32_t* __restrict__ cand) {
   const uint64_t pol_stream = policy_evict_first();
   const int shift = level == 0 ? 64 - kFilterCellBits : 8;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint32_t mine = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-    if (level > 0 && slot_of[i] == kUnique) continue;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint64_t i = cand ? cand[j] : j;
     const uint64_t c = (table_hash(ld_key_stream(keys + i, pol_stream), hashed, seed) >> shift) &
                        ((1ull << kFilterCellBits) - 1);
     const bool dup = (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
     slot_of[i] = dup ? 0u : kUnique;
-    mine += dup ? 1u : 0u;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(dups, (unsigned long long)mine);
 }
+
+// candidates in ascending state order (look-back scan over the previous list)
+struct CandIn {
+  const uint32_t* cand;  // nullptr: the identity list 0..m-1
+  const uint32_t* slot_of;
+  __device__ uint32_t operator()(uint64_t j) const {
+    return slot_of[cand ? cand[j] : (uint32_t)j] != kUnique ? 1u : 0u;
+  }
+};
+struct CandOut {
+  const uint32_t* cand;
+  uint32_t* out;
+  __device__ void operator()(uint64_t j, uint32_t excl, uint32_t v) const {
+    if (v) out[excl] = cand ? cand[j] : (uint32_t)j;
+  }
+};
 
 struct ResolveItem {
   uint32_t v;      // 1 = minimum member of a group that gets a fresh id
@@ -1064,6 +1081,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       // uniqueness filter in front of large hash tables (keys are precomputed)
       const bool filtered = blocked && !direct && m >= kFilterMinStates;
       uint64_t cap = table;
+      const uint32_t* cand = nullptr;  // filtered: the states that reach the table
+      uint64_t ncand = 0;
       if (present) {
         // dense slots for the keys present: exclusive popcount over the bitmap words
         const uint64_t words = ceil_div(table, 32);
@@ -1076,6 +1095,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       }
       if (filtered) {
         uint32_t* F = ctx.slot_t<uint32_t>("sh.filter", 1ull << (kFilterCellBits - 4));
+        uint32_t* cbuf[2] = {ctx.slot_t<uint32_t>("sh.cand0", m), ctx.slot_t<uint32_t>("sh.cand1", m)};
         uint64_t dups = m;
         // a second level on independent hash bits re-tests only the first level's
         // candidates: ~31 % -> ~4 % of the keys reach the table at 1e8 distinct keys
@@ -1083,26 +1103,30 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           ProfScope p(ctx, "insert", (1ull << (kFilterCellBits - 2)) + dups * (8ull + 8 + 4));
           DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kFilterCellBits - 2), ctx.stream));
           DFM_CUDA(cudaMemsetAsync(sc + 6, 0, 8, ctx.stream));
-          filt_set_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(keys, m, !packed, seed, F,
-                                                                    level, slot_of);
+          const uint32_t* cin = level == 0 ? nullptr : cand;
+          filt_set_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(keys, dups, !packed, seed,
+                                                                       F, level, cin);
           DFM_LAUNCH_CHECK();
-          filt_mark_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
-              keys, m, !packed, seed, F, slot_of, reinterpret_cast<unsigned long long*>(sc + 6),
-              level);
+          filt_mark_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(
+              keys, dups, !packed, seed, F, slot_of, level, cin);
           DFM_LAUNCH_CHECK();
+          prims::lookback_scan(ctx, "sc.cand", dups, CandIn{cin, slot_of},
+                               CandOut{cin, cbuf[level]}, sc + 6);
           DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 6, sc + 6, 8, cudaMemcpyDeviceToHost,
                                    ctx.stream));
           ctx.sync();
           dups = ctx.h_scalars[6];
+          cand = cbuf[level];
         }
+        ncand = dups;
         // load <= 0.4: a warp waits for its longest probe chain of DRAM-latency CASes
         cap = std::max<uint64_t>(1024, dups * 5 / 2);
       }
       Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", cap * sizeof(Slot)));
       DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(Slot), ctx.stream));
-      InsertParams ip{d.delta, n, k, block, ids, act, lead, m, w, seed, cap, slots,
-                      slot_of, packed ? nullptr : sig, row, keys, present,
-                      present ? present_pre : nullptr};
+      InsertParams ip{d.delta, n, k, block, ids, act, lead, filtered ? ncand : m, w, seed, cap,
+                      slots, slot_of, packed ? nullptr : sig, row, keys, present,
+                      present ? present_pre : nullptr, filtered ? cand : nullptr};
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
         switch (k) {
