@@ -152,6 +152,7 @@ struct AlgoOut {
   uint64_t iterations = 0, closure_steps = 0, peak_memory_estimate = 0;
   int32_t status = DFM_STATUS_OK;
   uint32_t* canon_dev = nullptr;  // canonical labels on device (ctx slot "canon")
+  bool canon_identity = false;    // every block a singleton: canonical labels = 0..n-1
 };
 
 // ---- algorithm drivers (device-resident input, results on device) ----

@@ -1208,6 +1208,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     iota_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(out.canon_dev, n);
     DFM_LAUNCH_CHECK();
     out.num_blocks = B;
+    out.canon_identity = true;
   } else {
     uint32_t* cob = ctx.slot_t<uint32_t>("sh.cob", n);
     ProfScope p(ctx, "canon", n * 13ull);
