@@ -290,7 +290,8 @@ def _device_labels(e, dd, n):
 
 
 @pytest.mark.parametrize("n,k,seed", [(12_000_000, 4, 3), (30_000_000, 2, 4),
-                                      (12_000_000, 3, 5), (9_000_000, 9, 6)])
+                                      (12_000_000, 3, 5), (9_000_000, 9, 6),
+                                      (12_000_001, 3, 7), (9_000_003, 5, 8)])
 def test_blocked_signature_builder(eng, eng_radix, monkeypatch, n, k, seed):
     """The blocked (target-range bucketed) signature builder takes over the
     passes whose id mirror exceeds the L2 share; it must give the exact same
