@@ -221,8 +221,10 @@ def make_family(args):
 
 def workload_name(args):
     if args.family == "random" and args.algo == "sort":
-        return (f"sortPR on random_dfa(n={args.n:.0e}, k={args.k}, seed={args.seed}, p={args.p}) "
-                "— north-star 1-GPU config (SURVEY 8(d) C5)")
+        tag = {(100_000_000, 4): " — north-star 1-GPU config (SURVEY 8(d) C5)",
+               (100_000, 2): " — SURVEY 8(d) C1 (the reference's CPU-runnable config)"}
+        return (f"sortPR on random_dfa(n={args.n:.0e}, k={args.k}, seed={args.seed}, p={args.p})"
+                + tag.get((args.n, args.k), ""))
     fam = {"random": f"random_dfa(n={args.n}, k={args.k}, seed={args.seed})",
            "chain": f"chain_dfa({args.n})", "comb": f"comb({args.n},3)",
            "fib": f"fib_dfa({args.n})", "bits": f"bit_splitter({args.n})",

@@ -28,7 +28,11 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "prims.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dfm {
 namespace {
@@ -619,9 +623,11 @@ struct ActOut {
   }
 };
 
-__global__ void init_kernel(const uint8_t* __restrict__ acc, uint64_t n, bool split,
+// split: both an accepting and a rejecting state exist (min_sort.hpp:80-88)
+__global__ void init_kernel(const uint8_t* __restrict__ acc, uint64_t n,
                             const uint32_t* __restrict__ first2, uint32_t* __restrict__ block,
                             uint8_t* __restrict__ lead) {
+  const bool split = first2[0] != kNoLeader && first2[1] != kNoLeader;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
     const uint32_t b = (split && acc[q] == 0) ? 1u : 0u;
@@ -704,6 +710,7 @@ constexpr uint64_t kBlockedMinMirror = 32ull << 20;
 
 #include "sortpr_blocked.cuh"
 #include "sortpr_group.cuh"
+#include "sortpr_small.cuh"
 
 unsigned grid_for(const Ctx& ctx, uint64_t items, int per_sm = 16) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
@@ -775,6 +782,93 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   else
     insert_kernel<32, false, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
   DFM_LAUNCH_CHECK();
+}
+
+bool small_enabled() {
+  const char* e = getenv("DFM_SORTPR_SMALL");
+  return e == nullptr || e[0] != '0';
+}
+
+unsigned small_grid(const Ctx& ctx, uint64_t n) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    DFM_CUDA(cudaFuncSetAttribute(small_sortpr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmallSmem));
+    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_sortpr_kernel,
+                                                           kSmallThreads, kSmallSmem));
+  }
+  // >= 256 states per CTA (fewer CTAs: cheaper grid barriers), all SMs once n > 37,888
+  const uint64_t grid = std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, 256));
+  return grid * kSmallThreads * kSmallPer >= n ? (unsigned)grid : 0u;
+}
+
+bool small_timing() {
+  const char* e = getenv("DFM_SMALL_TIMING");
+  return e != nullptr && e[0] == '1';
+}
+
+// Small automata: the whole minimization in one persistent kernel (sortpr_small.cuh):
+// initial partition, every pass, canonical labels.  Returns 1 at the fixpoint
+// (canonical labels in `canon`), 0 when the host loop must take over (keys wider
+// than 62 bits; block / lead / B and the pass count are then in its format), -1 on
+// deadline expiry.
+constexpr uint64_t kSmallSeed = 0x5EED5A11ull;
+
+int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint32_t* block,
+              uint8_t* lead, uint8_t* flag, uint32_t* first2, uint32_t* canon, uint32_t& B,
+              uint64_t& iterations) {
+  const uint32_t n = d.n;
+  const uint64_t cap0 = small_cap(n);
+  Slot* t0 = static_cast<Slot*>(ctx.slot("ss.tab0", cap0 * sizeof(Slot)));
+  Slot* t1 = static_cast<Slot*>(ctx.slot("ss.tab1", cap0 * sizeof(Slot)));
+  auto* ctr = ctx.slot_t<unsigned long long>("ss.ctr", 6);
+  auto* st = ctx.slot_t<uint32_t>("ss.state", 4);
+  uint32_t* cob = ctx.slot_t<uint32_t>("ss.cob", n);
+  uint32_t* cta_cnt = ctx.slot_t<uint32_t>("ss.ctacnt", grid);
+  uint32_t* h = reinterpret_cast<uint32_t*>(ctx.h_scalars + 24);
+  h[1] = 0;
+  const bool timing = small_timing();
+  unsigned long long* tdbg =
+      timing ? ctx.slot_t<unsigned long long>("ss.tdbg", 8 * 4096 + 1) : nullptr;
+  // per pass and state: delta k*4, ids (k+1)*4, flag + lead 2, slot CAS/atomics 16,
+  // slot read 8, id write 4
+  const uint64_t pass_bytes = (uint64_t)n * (8ull * d.k + 34);
+  const uint32_t per_cta = (uint32_t)ceil_div(ceil_div(n, grid), 32) * 32;
+  uint32_t chunk = 64;
+  bool first_launch = true;
+  while (true) {
+    if (dl.expired()) return -1;
+    SmallArgs a{d.delta, n,  d.k,   block, lead,    flag,         t0,     t1,
+                ctr,     st, chunk, kSmallSeed, per_cta, d.acc, first2, first_launch,
+                canon,   cob, cta_cnt, tdbg};
+    first_launch = false;
+    chunk = std::min<uint32_t>(4096, chunk * 2);
+    void* args[] = {&a};
+    const uint32_t before = h[1];
+    ProfScope prof(ctx, "small", 0);
+    DFM_CUDA(cudaLaunchCooperativeKernel((const void*)small_sortpr_kernel, grid, kSmallThreads,
+                                         args, kSmallSmem, ctx.stream));
+    DFM_LAUNCH_CHECK();
+    prof.stop();
+    DFM_CUDA(cudaMemcpyAsync(h, st, 16, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const uint32_t done = h[1] - before;
+    prof.bytes = (uint64_t)done * pass_bytes;
+    if (timing) {
+      std::vector<unsigned long long> t(8 * done + 1);
+      DFM_CUDA(cudaMemcpy(t.data(), tdbg, t.size() * 8, cudaMemcpyDeviceToHost));
+      auto us = [&](uint32_t x, int a, int b) {
+        return t[8 * x + b] > t[8 * x + a] ? (t[8 * x + b] - t[8 * x + a]) * 1e-3 : 0.0;
+      };
+      for (uint32_t x = 0; x < done; ++x)
+        fprintf(stderr, "small pass %u: A %.2f us (keys %.2f flush %.2f)  B %.2f us\n",
+                before + x + 1, us(x, 0, 1), us(x, 0, 4), us(x, 4, 5), us(x, 1, 2));
+    }
+    B = h[0];
+    iterations = h[1];
+    if (h[3] == 1) return 1;
+    if (h[3] == 2) return 0;
+  }
 }
 
 // partitioned grouping (sortpr_group.cuh) is opt-in until its radix passes beat the
@@ -982,21 +1076,40 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint32_t* first2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
   DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
   DFM_CUDA(cudaMemsetAsync(first2, 0xFF, 8, ctx.stream));
-  {
-    ProfScope p(ctx, "init", n * 2);
-    first_states_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2);
-    DFM_LAUNCH_CHECK();
-  }
-  DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 16, first2, 8, cudaMemcpyDeviceToHost, ctx.stream));
-  ctx.sync();
-  const uint32_t fa = (uint32_t)(ctx.h_scalars[16] & 0xFFFFFFFFu);
-  const uint32_t fr = (uint32_t)(ctx.h_scalars[16] >> 32);
-  const bool split = fa != kNoLeader && fr != kNoLeader;  // min_sort.hpp:80-88
-  uint32_t B = split ? 2u : 1u;
-  {
-    ProfScope p(ctx, "init", n * 10);
-    init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, first2, block, lead);
-    DFM_LAUNCH_CHECK();
+  const unsigned sgrid =
+      (n <= kSmallMaxStates && !(trace && trace->on_pass) && small_enabled()) ? small_grid(ctx, n)
+                                                                              : 0u;
+  uint32_t B = 0;
+  if (sgrid) {
+    out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+    const int r = run_small(ctx, d, dl, sgrid, block, lead, flag, first2, out.canon_dev, B,
+                            out.iterations);
+    if (r < 0) {
+      out.status = DFM_STATUS_TIMEOUT;
+      return out;
+    }
+    if (r == 1) {
+      out.num_blocks = B;
+      out.canon_identity = B == n;
+      out.status = DFM_STATUS_OK;
+      return out;
+    }
+  } else {
+    {
+      ProfScope p(ctx, "init", n * 2);
+      first_states_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2);
+      DFM_LAUNCH_CHECK();
+    }
+    {
+      ProfScope p(ctx, "init", n * 10);
+      init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2, block, lead);
+      DFM_LAUNCH_CHECK();
+    }
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 16, first2, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const uint32_t fa = (uint32_t)(ctx.h_scalars[16] & 0xFFFFFFFFu);
+    const uint32_t fr = (uint32_t)(ctx.h_scalars[16] >> 32);
+    B = (fa != kNoLeader && fr != kNoLeader) ? 2u : 1u;  // min_sort.hpp:80-88
   }
   int mirror_bits = 0;  // id width of the current gather source (32 = block itself)
   auto build_mirror = [&](uint32_t blocks) {
@@ -1215,9 +1328,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     prims::lookback_scan(ctx, "sc.canon", n, LeadIn{lead}, LeadOut{block, cob}, sc + 5);
     canon_gather_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, cob, out.canon_dev);
     DFM_LAUNCH_CHECK();
-    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 5, sc + 5, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    ctx.sync();
-    out.num_blocks = (uint32_t)ctx.h_scalars[5];
+    out.num_blocks = B;  // one leader per block
   }
   out.status = DFM_STATUS_OK;
   return out;

@@ -326,3 +326,31 @@ def test_partitioned_grouping(eng, monkeypatch, n, k, seed):
     nb1, it1, lab1 = _device_labels(eng, dd, n)
     assert (nb, it) == (nb1, it1) and bool((lab == lab1).all())
     dd.free()
+
+
+@pytest.mark.parametrize("case", [
+    ("random", 100_000, 2, 1, 0.5),    # C1: every pass inside the persistent kernel
+    ("random", 50_000, 8, 3, 0.5),     # keys outgrow 62 bits: the host loop takes over
+    ("random", 3_000, 70, 4, 0.3),     # (k+1) > 62: host loop from the first pass
+    ("random", 1 << 20, 1, 5, 0.5),    # largest small-kernel size, 8 states per thread
+    ("random", 777, 3, 6, 0.0),        # one initial block
+    ("fib", 20, 0, 0, 0.0),            # 10,945 states, N-1 passes over several launches
+    ("chain", 5_000, 0, 0, 0.0),
+    ("comb", 2_000, 3, 0, 0.0),
+])
+def test_small_persistent_sortpr(eng, monkeypatch, case):
+    """sortPR's single-kernel path for n <= 2^20 (sortpr_small.cuh) against the
+    oracle and against the host-driven loop (DFM_SORTPR_SMALL=0)."""
+    kind, n, k, seed, p = case
+    pair = {"random": lambda: O.random_dfa(n, k, seed, p), "fib": lambda: O.fib_dfa(n),
+            "chain": lambda: O.chain_dfa(n), "comb": lambda: O.comb_dfa(n, k)}[kind]()
+    d = to_dfa(pair)
+    ref = O.sort_pr(*pair)
+    r = eng.sort_pr(d)
+    assert r.stats.status == dfm.RunStatus.ok
+    assert (r.partition.num_blocks, r.stats.iterations) == (ref.num_blocks, ref.iterations)
+    assert (r.partition.block == ref.block).all()
+    monkeypatch.setenv("DFM_SORTPR_SMALL", "0")
+    r2 = eng.sort_pr(d)
+    assert r2.stats.iterations == r.stats.iterations
+    assert (r2.partition.block == r.partition.block).all()
