@@ -834,13 +834,15 @@ int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint
   // slot read 8, id write 4
   const uint64_t pass_bytes = (uint64_t)n * (8ull * d.k + 34);
   const uint32_t per_cta = (uint32_t)ceil_div(ceil_div(n, grid), 32) * 32;
+  uint32_t tab = 1024;
+  while (tab < 2 * per_cta && tab < kSmallTab) tab <<= 1;
   uint32_t chunk = 64;
   bool first_launch = true;
   while (true) {
     if (dl.expired()) return -1;
-    SmallArgs a{d.delta, n,  d.k,   block, lead,    flag,         t0,     t1,
-                ctr,     st, chunk, kSmallSeed, per_cta, d.acc, first2, first_launch,
-                canon,   cob, cta_cnt, tdbg};
+    SmallArgs a{d.delta, n,          d.k,     block,    lead,  flag,   t0,
+                t1,      ctr,        st,      chunk,    kSmallSeed,     per_cta,
+                tab - 1, d.acc,      first2,  first_launch, canon, cob, cta_cnt, tdbg};
     first_launch = false;
     chunk = std::min<uint32_t>(4096, chunk * 2);
     void* args[] = {&a};

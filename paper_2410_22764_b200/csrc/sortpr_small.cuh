@@ -37,7 +37,8 @@ struct SmallArgs {
   uint32_t* state;          // [0] B [1] passes so far [2] active states [3] 1 = fixpoint, 2 = wide keys
   uint32_t max_passes;
   uint64_t seed;
-  uint32_t per_cta;  // states per CTA (<= kSmallThreads * kSmallPer)
+  uint32_t per_cta;   // states per CTA (<= kSmallThreads * kSmallPer)
+  uint32_t tab_mask;  // shared table slots - 1 (power of two >= 2 * per_cta, <= kSmallTab)
   // first launch: initial partition in the prologue (first_states/init of the host loop)
   const uint8_t* acc;
   uint32_t* first2;  // [0] first accepting, [1] first rejecting (host-set to kNoLeader)
@@ -142,9 +143,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
   const uint32_t base_q = blockIdx.x * a.per_cta + threadIdx.x;
   __shared__ uint32_t s_warp[kSmallThreads / 32 + 1];
   __shared__ uint32_t s_base;
+  __shared__ uint32_t s_cnt;  // occupied shared slots (flush list length)
   auto owned = [&](int j) { return threadIdx.x + j * kSmallThreads < a.per_cta &&
                                    base_q + j * kSmallThreads < a.n; };
   uint32_t B, pass, m;
+  // the thread's own states live in registers across passes (only their owner
+  // writes them); the global copies serve the successor gathers and a relaunch
+  uint32_t myb[kSmallPer];  // block id
+  uint32_t mys[kSmallPer];  // bit0 in a block of >= 2 states, bit1 leader
   if (a.init) {
     // initial partition {accepting, rejecting} and its leaders (min_sort.hpp:80-88)
     uint32_t fa = kNoLeader, fr = kNoLeader;
@@ -175,9 +181,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
 #pragma unroll
     for (int j = 0; j < kSmallPer; ++j) {
       const uint32_t q = base_q + j * kSmallThreads;
+      myb[j] = 0;
+      mys[j] = 0;
       if (owned(j)) {
-        a.block[q] = (split && a.acc[q] == 0) ? 1u : 0u;
-        a.lead[q] = (q == fa || q == fr || (!split && q == 0)) ? 1 : 0;
+        myb[j] = (split && a.acc[q] == 0) ? 1u : 0u;
+        const bool ld = q == fa || q == fr || (!split && q == 0);
+        mys[j] = 1u | (ld ? 2u : 0u);
+        a.block[q] = myb[j];
+        a.lead[q] = ld ? 1 : 0;
         a.flag[q] = 1;
       }
     }
@@ -189,9 +200,28 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
     B = a.state[0];
     pass = a.state[1];
     m = a.state[2];
+#pragma unroll
+    for (int j = 0; j < kSmallPer; ++j) {
+      const uint32_t q = base_q + j * kSmallThreads;
+      myb[j] = 0;
+      mys[j] = 0;
+      if (owned(j)) {
+        myb[j] = a.block[q];
+        mys[j] = (a.flag[q] ? 1u : 0u) | (a.lead[q] ? 2u : 0u);
+      }
+    }
   }
   uint32_t status = 0;
   const bool timing = a.tdbg != nullptr && first == 0;
+  auto clear_shared = [&]() {
+    for (uint32_t i = threadIdx.x; i <= a.tab_mask; i += blockDim.x) {
+      s_key[i] = 0;
+      s_rep[i] = 0;
+      s_info[i] = 0;
+    }
+    if (threadIdx.x == 0) s_cnt = 0;
+  };
+  clear_shared();
   for (uint32_t it = 0; it < a.max_passes; ++it) {
     if (timing) a.tdbg[8 * it] = small_now();
     const int w = B <= 1 ? 1 : 32 - __clz(B - 1);
@@ -214,10 +244,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
     }
     // ---- A: insert, aggregated per CTA in a shared-memory table first (early passes
     // have a few huge groups: one global atomic per group per CTA, not per state)
-    for (uint32_t i = threadIdx.x; i < kSmallTab; i += blockDim.x) {
-      s_key[i] = 0;
-      s_rep[i] = 0;
-      s_info[i] = 0;
+    unsigned long long keys[kSmallPer];
+#pragma unroll
+    for (int j = 0; j < kSmallPer; ++j) {  // all gathers of the thread in flight together
+      const uint32_t q = base_q + j * kSmallThreads;
+      keys[j] = myb[j];
+      if (mys[j] & 1u)
+        for (uint32_t x = 0; x < a.k; ++x)
+          keys[j] = (keys[j] << w) | __ldcg(a.block + __ldg(a.delta + (uint64_t)x * a.n + q));
     }
     __syncthreads();
     uint32_t slot[kSmallPer];  // shared index, or global slot | kGlobalSlot
@@ -227,22 +261,20 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
       const uint32_t q = base_q + j * kSmallThreads;
       stat[j] = 0;
       slot[j] = 0;
-      const bool act = owned(j) && __ldcg(a.flag + q) != 0;
+      const bool act = (mys[j] & 1u) != 0;
       const uint32_t vmask = __ballot_sync(0xffffffffu, act);
       if (vmask == 0) continue;
       if (act) {
-        unsigned long long key = __ldcg(a.block + q);
-        for (uint32_t x = 0; x < a.k; ++x)
-          key = (key << w) | __ldcg(a.block + __ldg(a.delta + (uint64_t)x * a.n + q));
+        const unsigned long long key = keys[j];
         // lanes with equal keys: the lowest (= minimum q) inserts for all
         const uint32_t peers = __match_any_sync(vmask, key);
-        const uint32_t leads = __ballot_sync(vmask, __ldcg(a.lead + q) != 0) & peers;
+        const uint32_t leads = __ballot_sync(vmask, (mys[j] & 2u) != 0) & peers;
         const int low = __ffs(peers) - 1;
         uint32_t t = 0;
         if (lane == (uint32_t)low) {
           const unsigned long long stored = key + 1ull;
           const uint32_t add = (uint32_t)__popc(peers) | (leads ? 0x80000000u : 0u);
-          uint32_t h = (uint32_t)mix64(key ^ ~a.seed) & (kSmallTab - 1);
+          uint32_t h = (uint32_t)mix64(key ^ ~a.seed) & a.tab_mask;
           bool local = false;
           for (int probe = 0; probe < 32; ++probe) {
             const unsigned long long cur = atomicCAS(&s_key[h], 0ull, stored);
@@ -250,7 +282,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
               local = true;
               break;
             }
-            h = (h + 1) & (kSmallTab - 1);
+            h = (h + 1) & a.tab_mask;
           }
           if (local) {
             atomicMax(&s_rep[h], ~q);
@@ -266,14 +298,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
     }
     __syncthreads();
     if (timing) a.tdbg[8 * it + 4] = small_now();
-    {  // the CTA's distinct keys, compacted, then one global claim per thread
-      uint32_t cnt = 0;
-      for (uint32_t i = threadIdx.x; i < kSmallTab; i += blockDim.x) cnt += s_key[i] != 0ull;
-      uint32_t tot;
-      uint32_t off = prims::block_exclusive_sum<kSmallThreads>(cnt, s_warp, &tot);
-      for (uint32_t i = threadIdx.x; i < kSmallTab; i += blockDim.x)
-        if (s_key[i] != 0ull) s_list[off++] = i;
+    {  // the CTA's distinct keys, compacted (any order), then one global claim per thread
+      for (uint32_t i0 = threadIdx.x & ~31u; i0 <= a.tab_mask; i0 += blockDim.x) {
+        const uint32_t i = i0 + lane;
+        const bool used = s_key[i] != 0ull;
+        const uint32_t bal = __ballot_sync(0xffffffffu, used);
+        uint32_t pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&s_cnt, (uint32_t)__popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (used) s_list[pos + __popc(bal & ((1u << lane) - 1u))] = i;
+      }
       __syncthreads();
+      const uint32_t tot = s_cnt;
       for (uint32_t x = threadIdx.x; x < tot; x += blockDim.x) {
         const uint32_t i = s_list[x];
         s_gs[i] = small_claim(T, cap, s_key[i] - 1ull, a.seed, s_rep[i], s_info[i]);
@@ -284,6 +320,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
 #pragma unroll
     for (int j = 0; j < kSmallPer; ++j)
       if (stat[j]) slot[j] = (slot[j] & kGlobalSlot) ? (slot[j] & ~kGlobalSlot) : s_gs[slot[j]];
+    clear_shared();  // (the claims above read it before the last block barrier)
     g.sync();
     if (timing) a.tdbg[8 * it + 1] = small_now();
     // ---- B: resolve
@@ -298,8 +335,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
         const bool single = (sl.y & 0x7FFFFFFFu) == 1u;
         stat[j] |= (is_rep ? 2u : 0u) | (keeper ? 4u : 0u) | (single ? 8u : 0u);
         want += (is_rep && !keeper) ? 1u : 0u;
-        if (single) a.flag[q] = 0;
-        else ++survivors;
+        if (single) {
+          a.flag[q] = 0;
+          mys[j] &= ~1u;
+        } else {
+          ++survivors;
+        }
       }
     }
     {  // fresh ids and the survivor count: one atomic per CTA (16-bit fields, <= 8192 each)
@@ -319,6 +360,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
           const uint32_t q = base_q + j * kSmallThreads;
           a.block[q] = gid;
           a.lead[q] = 1;
+          myb[j] = gid;
+          mys[j] |= 2u;
           if (!(stat[j] & 8u)) st_relaxed_u64(&T[slot[j]].key, kPublished | gid);  // for the members
           ++gid;
         }
@@ -331,7 +374,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
       if ((stat[j] & 7u) == 1u) {  // active, not the rep, group without the old leader
         unsigned long long v = ld_relaxed_u64(&T[slot[j]].key);
         while (!(v & kPublished)) v = ld_relaxed_u64(&T[slot[j]].key);
-        a.block[base_q + j * kSmallThreads] = (uint32_t)v;
+        myb[j] = (uint32_t)v;
+        a.block[base_q + j * kSmallThreads] = myb[j];
       }
     }
     g.sync();
@@ -357,7 +401,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
       uint32_t run = 0;
 #pragma unroll
       for (int j = 0; j < kSmallPer; ++j) {
-        const uint32_t v = owned(j) ? (uint32_t)__ldcg(a.lead + base_q + j * kSmallThreads) : 0u;
+        const uint32_t v = (mys[j] >> 1) & 1u;
         uint32_t tot;
         const uint32_t e = prims::block_exclusive_sum<kSmallThreads>(v, s_warp, &tot);
         rank[j] = v ? run + e : kNoLeader;
@@ -372,12 +416,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
 #pragma unroll
       for (int j = 0; j < kSmallPer; ++j)
         if (rank[j] != kNoLeader)
-          a.cob[__ldcg(a.block + base_q + j * kSmallThreads)] = tot + rank[j];
+          a.cob[myb[j]] = tot + rank[j];
       g.sync();
 #pragma unroll
       for (int j = 0; j < kSmallPer; ++j) {
         const uint32_t q = base_q + j * kSmallThreads;
-        if (owned(j)) a.canon[q] = __ldcg(a.cob + __ldcg(a.block + q));
+        if (owned(j)) a.canon[q] = __ldcg(a.cob + myb[j]);
       }
     }
   }
