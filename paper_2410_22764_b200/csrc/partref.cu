@@ -299,6 +299,111 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
 }
 
 // ---------------------------------------------------------------------------
+// One grid barrier per pass: the split phase of pass p-1 is not materialised
+// before pass p; pass p reads the labels L(p-2) the previous pass wrote plus
+// that pass's split flags and election cells, and forms each label it needs
+// on the fly: L(p-1)[x] = split(p-1)[x] ? winner(cell(p-1)[L(p-2)[x]]) : L(p-2)[x].
+// Each thread stores L(p-1) of its own state as it goes (for pass p+1), its
+// split flag and its election for pass p.  Split flags and election cells are
+// double-buffered by pass parity; labels by the usual two buffers.  Same per-pass
+// semantics and pass count as persistent_kernel (min_partref.hpp:78-143); the
+// dependent-load depth of a pass is unchanged (label, successor of the leader,
+// its label, each with its cell), one barrier and one grid sweep fewer.
+struct FusedArgs {
+  const uint32_t* rows;
+  uint64_t n, letters;
+  uint32_t* lab0;
+  uint32_t* lab1;
+  unsigned long long* cells0;  // pass parity 0 / 1
+  unsigned long long* cells1;
+  uint8_t* split0;
+  uint8_t* split1;
+  uint32_t* changed;  // one flag per pass of this launch (zeroed by the host)
+  uint32_t pass0;
+  uint32_t max_passes;
+  int start_sel;  // buffer holding the labels the next pass reads
+  uint32_t* out;  // [0] passes executed, [1] stable, [2] buffer holding the labels
+};
+
+__device__ __forceinline__ uint32_t label_on_the_fly(uint32_t l, uint8_t s,
+                                                     const unsigned long long* cprev) {
+  return s ? (uint32_t)cprev[l] : l;
+}
+
+template <int kPolicy>
+__global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) {
+  cg::grid_group g = cg::this_grid();
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  int sel = a.start_sel;
+  uint32_t p = 0;
+  bool stable = false;
+  while (p < a.max_passes) {
+    const uint32_t pass = a.pass0 + p + 1;
+    const uint32_t* Lm = sel ? a.lab1 : a.lab0;
+    uint32_t* Lw = sel ? a.lab0 : a.lab1;
+    const uint8_t* sprev = (pass & 1) ? a.split0 : a.split1;
+    uint8_t* scur = (pass & 1) ? a.split1 : a.split0;
+    const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
+    unsigned long long* ccur = (pass & 1) ? a.cells1 : a.cells0;
+    const uint32_t prev_changed =
+        p > 0 ? *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) : 1u;
+    bool any = false;
+    for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
+      const uint64_t qi = qb + (threadIdx.x & 31);
+      const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
+      if (qi >= a.n) continue;
+      const uint32_t q = (uint32_t)qi;
+      const uint32_t leader = label_on_the_fly(Lm[q], sprev[q], cprev);
+      bool sp = false;
+      if (q != leader) {
+        for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
+          uint32_t tq[4], tl[4], lq[4], ll[4];
+          uint8_t sq[4], sl[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (a0 + u < a.letters) {
+              tq[u] = a.rows[(a0 + u) * a.n + q];
+              tl[u] = a.rows[(a0 + u) * a.n + leader];
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (a0 + u < a.letters) {
+              lq[u] = Lm[tq[u]];
+              sq[u] = sprev[tq[u]];
+              ll[u] = Lm[tl[u]];
+              sl[u] = sprev[tl[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (a0 + u < a.letters)
+              sp |= label_on_the_fly(lq[u], sq[u], cprev) != label_on_the_fly(ll[u], sl[u], cprev);
+        }
+      }
+      Lw[q] = leader;
+      scur[q] = sp;
+      any |= sp;
+      elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
+    }
+    if (prev_changed == 0u) {  // pass p was stable: this pass rewrote the same labels
+      stable = true;
+      break;
+    }
+    if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) a.changed[p] = 1u;
+    g.sync();
+    sel ^= 1;
+    ++p;
+  }
+  if (!stable && p > 0 && *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u)
+    stable = true;
+  if (first == 0) {
+    a.out[0] = p;
+    a.out[1] = stable ? 1u : 0u;
+    a.out[2] = (uint32_t)sel;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Cluster variant for tiny inputs (rings and chains of a few thousand states run
 // n-1 passes): the whole working set — successor rows, both label buffers,
 // election cells, split flags — lives in the (distributed) shared memory of a
@@ -497,6 +602,19 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 constexpr uint64_t kPersistentMaxStates = 1ull << 22;
 constexpr uint64_t kClusterMaxStates = 4096;
 
+uint64_t fused_max_states(const Ctx& ctx) {
+  static int per_sm = -1;
+  if (per_sm < 0)
+    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, fused_pr_kernel<DFM_POLICY_MIN>, kPersistThreads, 0));
+  return (uint64_t)per_sm * ctx.num_sms * kPersistThreads;
+}
+
+bool fused_enabled() {
+  const char* e = getenv("DFM_NAIVE_FUSED");
+  return e == nullptr || e[0] != '0';
+}
+
 bool cluster_disabled() {
   const char* e = getenv("DFM_NAIVE_CLUSTER");
   return e != nullptr && e[0] == '0';
@@ -581,6 +699,54 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       DFM_LAUNCH_CHECK();
       prof.stop();
       DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, cout, 12, cudaMemcpyDeviceToHost, ctx.stream));
+      ctx.sync();
+      const uint32_t* h = reinterpret_cast<const uint32_t*>(ctx.h_scalars + 20);
+      prof.bytes = (uint64_t)h[0] * pass_bytes;
+      pass += h[0];
+      sel = (int)h[2];
+      if (h[1]) break;
+    }
+    out.iterations = pass;
+    out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
+    out.num_blocks = canonicalize_dev(ctx, lab[sel], n, out.canon_dev);
+    out.status = DFM_STATUS_OK;
+    return out;
+  }
+  if (!tracing_ && !fused_cas && fused_enabled() && n <= fused_max_states(ctx)) {
+    // one barrier per pass (fused_pr_kernel) while every state has its own thread.
+    // Measured (B200): C1 random_dfa(1e5, 2) 95 -> 88 ms, fib_dfa(22) 129 -> 108 ms;
+    // with several states per thread the extra label/flag/cell gathers cost more than
+    // the barrier saves (vlts 1e6 x 20: 66 -> 92 ms), so larger inputs take the
+    // two-phase kernel
+    const uint32_t kChunkMax = 8192;
+    uint32_t chunk = 16;
+    uint32_t* chg = ctx.slot_t<uint32_t>("pr.pchanged", kChunkMax);
+    uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
+    auto* cells1 = ctx.slot_t<unsigned long long>("pr.cells1", n);
+    uint8_t* split1 = ctx.slot_t<uint8_t>("pr.split1", n);
+    DFM_CUDA(cudaMemsetAsync(cells1, policy == DFM_POLICY_MIN ? 0xFF : 0x00, n * 8, ctx.stream));
+    DFM_CUDA(cudaMemsetAsync(split_flag, 0, n, ctx.stream));
+    DFM_CUDA(cudaMemsetAsync(split1, 0, n, ctx.stream));
+    void (*kern)(FusedArgs) = policy == DFM_POLICY_MIN   ? fused_pr_kernel<DFM_POLICY_MIN>
+                              : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX>
+                                                         : fused_pr_kernel<DFM_POLICY_ARBITRARY>;
+    const unsigned pgrid = (unsigned)ceil_div(n, kPersistThreads);
+    while (true) {
+      if (dl.expired()) {
+        out.status = DFM_STATUS_TIMEOUT;
+        return out;
+      }
+      DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
+      FusedArgs fa{rows,  n,    letters, lab[0], lab[1], cells, cells1,
+                   split_flag, split1, chg, pass, chunk, sel, pout};
+      chunk = std::min(kChunkMax, chunk * 2);
+      void* args[] = {&fa};
+      ProfScope prof(ctx, "elect", 0);
+      DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, kPersistThreads, args, 0,
+                                           ctx.stream));
+      DFM_LAUNCH_CHECK();
+      prof.stop();
+      DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, pout, 12, cudaMemcpyDeviceToHost, ctx.stream));
       ctx.sync();
       const uint32_t* h = reinterpret_cast<const uint32_t*>(ctx.h_scalars + 20);
       prof.bytes = (uint64_t)h[0] * pass_bytes;

@@ -354,3 +354,28 @@ def test_small_persistent_sortpr(eng, monkeypatch, case):
     r2 = eng.sort_pr(d)
     assert r2.stats.iterations == r.stats.iterations
     assert (r2.partition.block == r.partition.block).all()
+
+
+@pytest.mark.parametrize("policy", [MIN, MAX])
+@pytest.mark.parametrize("case", [
+    ("random", 100_000, 2, 1, 0.5),
+    ("random", 20_000, 5, 7, 0.3),
+    ("fib", 16, 0, 0, 0.0),
+    ("vlts", 300_000, 10, 0, 0.0),
+])
+def test_naive_one_barrier_kernel(eng, monkeypatch, policy, case):
+    """naivePR's one-barrier-per-pass persistent kernel (labels of the previous
+    pass formed on the fly) against the oracle and the two-phase kernel."""
+    kind, n, k, seed, p = case
+    pair = {"random": lambda: O.random_dfa(n, k, seed, p), "fib": lambda: O.fib_dfa(n),
+            "vlts": lambda: O.vlts_dfa(300, n, k)}[kind]()
+    d = to_dfa(pair)
+    ref = O.naive_pr(*pair, "min" if policy == MIN else "max")
+    r = eng.naive_pr(d, dfm.PrOptions(policy=policy))
+    assert r.stats.status == dfm.RunStatus.ok
+    assert r.stats.iterations == ref.iterations
+    assert (r.partition.block == ref.block).all()
+    monkeypatch.setenv("DFM_NAIVE_FUSED", "0")
+    r2 = eng.naive_pr(d, dfm.PrOptions(policy=policy))
+    assert r2.stats.iterations == r.stats.iterations
+    assert (r2.partition.block == r.partition.block).all()
