@@ -151,13 +151,29 @@ void host_iota(uint32_t* out, uint64_t n) {
   for (auto& x : th) x.join();
 }
 
+// sortPR on a large automaton usually ends all singletons (random DFAs): the identity
+// labels are written into the caller's buffer by a host thread WHILE the GPU runs;
+// joined before anything else touches the buffer (a non-identity result overwrites it)
+struct SpeculativeIota {
+  std::thread th;
+  bool started = false;
+  void start(uint32_t* out, uint64_t n) {
+    th = std::thread([out, n] { host_iota(out, n); });
+    started = true;
+  }
+  void join() {
+    if (th.joinable()) th.join();
+  }
+  ~SpeculativeIota() { join(); }
+};
+
 void finish(Ctx& ctx, const AlgoOut& o, uint64_t n, const Deadline& dl, uint32_t* block_out,
-            uint32_t* nb_out, dfm_stats* st) {
+            uint32_t* nb_out, dfm_stats* st, bool iota_written = false) {
   const bool identity = o.status == DFM_STATUS_OK && block_out != nullptr && o.canon_identity;
   if (o.status == DFM_STATUS_OK && block_out != nullptr && !identity)
     DFM_CUDA(cudaMemcpyAsync(block_out, o.canon_dev, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
   ctx.sync();
-  if (identity) host_iota(block_out, n);
+  if (identity && !iota_written) host_iota(block_out, n);
   if (nb_out) *nb_out = o.status == DFM_STATUS_OK ? o.num_blocks : 0;
   if (st) {
     st->iterations = o.iterations;
@@ -174,9 +190,14 @@ int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const d
   return guarded(c, [&](Ctx& ctx) {
     const Deadline whole(0);
     const dfm_limits lim = limits_or_default(l);
+    SpeculativeIota spec;
+    if (algo == DFM_ALGO_SORT && block_out != nullptr && d != nullptr &&
+        d->num_states >= (1u << 22))
+      spec.start(block_out, d->num_states);
     const DevDfa dd = upload(ctx, d, "in", false);
     const AlgoOut o = dispatch(ctx, algo, dd, policy, lim, trace, apart, pops, pop_cap);
-    finish(ctx, o, dd.n, whole, block_out, nb_out, st);
+    spec.join();
+    finish(ctx, o, dd.n, whole, block_out, nb_out, st, spec.started);
   });
 }
 
