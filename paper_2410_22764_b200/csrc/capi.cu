@@ -105,6 +105,41 @@ DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_al
   return dd;
 }
 
+// sortPR from host buffers: accepting flags first, then the rows chunk by chunk on
+// the copy stream; sortPR's first pass and the layout build consume each chunk as
+// it lands (validation included), so only the tail of the copy is exposed
+DevDfa upload_progressive(Ctx& ctx, const dfm_dfa* d, uint64_t chunk) {
+  check_host_dfa(d);
+  DevDfa dd;
+  dd.n = d->num_states;
+  dd.k = d->alphabet_size;
+  dd.initial = d->initial;
+  const uint64_t n = dd.n, k = dd.k;
+  dd.delta = ctx.slot_t<uint32_t>("in.delta", std::max<uint64_t>(n * k, 1));
+  dd.acc = ctx.slot_t<uint8_t>("in.acc", n);
+  dd.owns = false;
+  DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+  const uint32_t nc = (uint32_t)ceil_div(n, chunk);
+  const cudaEvent_t* ev = ctx.chunk_event_pool(nc);
+  cudaStream_t cs = ctx.copy();
+  // the copy stream starts after everything queued so far (slot allocations)
+  DFM_CUDA(cudaEventRecord(ev[0], ctx.stream));
+  DFM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+  for (uint32_t c = 0; c < nc; ++c) {
+    const uint64_t q0 = c * chunk, len = std::min(n, q0 + chunk) - q0;
+    for (uint64_t a = 0; a < k; ++a)
+      DFM_CUDA(cudaMemcpyAsync(dd.delta + a * n + q0, d->delta[a] + q0, len * 4,
+                               cudaMemcpyHostToDevice, cs));
+    DFM_CUDA(cudaEventRecord(ev[c], cs));
+  }
+  dd.ready = ev;
+  dd.nready = nc;
+  dd.chunk_states = chunk;
+  dd.bad = reinterpret_cast<unsigned long long*>(ctx.d_scalars + 40);
+  DFM_CUDA(cudaMemsetAsync(dd.bad, 0, 8, ctx.stream));
+  return dd;
+}
+
 dfm_limits limits_or_default(const dfm_limits* l) {
   dfm_limits r;
   r.max_memory_bytes = l ? l->max_memory_bytes : (16ull << 30);
@@ -194,8 +229,20 @@ int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const d
     if (algo == DFM_ALGO_SORT && block_out != nullptr && d != nullptr &&
         d->num_states >= (1u << 22))
       spec.start(block_out, d->num_states);
-    const DevDfa dd = upload(ctx, d, "in", false);
-    const AlgoOut o = dispatch(ctx, algo, dd, policy, lim, trace, apart, pops, pop_cap);
+    const uint64_t chunk =
+        (algo == DFM_ALGO_SORT && ctx.sortpr_engine != DFM_SORTPR_RADIX && d != nullptr &&
+         !(trace && trace->on_pass))
+            ? sortpr_upload_chunk(d->num_states, d->alphabet_size)
+            : 0;
+    const DevDfa dd = chunk ? upload_progressive(ctx, d, chunk) : upload(ctx, d, "in", false);
+    AlgoOut o;
+    try {
+      o = dispatch(ctx, algo, dd, policy, lim, trace, apart, pops, pop_cap);
+    } catch (...) {
+      if (dd.nready) cudaStreamSynchronize(ctx.copy());
+      throw;
+    }
+    if (dd.nready) DFM_CUDA(cudaStreamSynchronize(ctx.copy()));
     spec.join();
     finish(ctx, o, dd.n, whole, block_out, nb_out, st, spec.started);
   });

@@ -108,6 +108,11 @@ struct Ctx {
   // small device scalars for host read-back (pinned host mirror)
   uint64_t* d_scalars = nullptr;  // device, 64 slots
   uint64_t* h_scalars = nullptr;  // pinned host, 64 slots
+  // second stream for pipelined host->device uploads, and its chunk events
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_events;
+  cudaStream_t copy();
+  const cudaEvent_t* chunk_event_pool(uint32_t count);
 
   explicit Ctx(int dev);
   ~Ctx();
@@ -145,6 +150,14 @@ struct DevDfa {
   uint32_t* delta = nullptr;  // k*n
   uint8_t* acc = nullptr;     // n
   bool owns = true;
+  // pipelined upload (sortPR from host buffers): the rows of states
+  // [c*chunk_states, (c+1)*chunk_states) are in HBM once ready[c] has fired on the
+  // copy stream; their targets are not yet validated (`bad` flags an out-of-range
+  // one, which the consumer zeroes).  acc is complete.  nready == 0: all resident.
+  const cudaEvent_t* ready = nullptr;
+  uint32_t nready = 0;
+  uint64_t chunk_states = 0;
+  unsigned long long* bad = nullptr;
 };
 
 struct AlgoOut {
@@ -158,6 +171,9 @@ struct AlgoOut {
 // ---- algorithm drivers (device-resident input, results on device) ----
 AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace);
 AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace);
+// states per chunk of a pipelined sortPR upload (whole layout windows, ~64 MB of
+// rows), or 0 when sortPR would not consume the rows chunk by chunk
+uint64_t sortpr_upload_chunk(uint64_t n, uint32_t k);
 AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uint64_t letters,
                             int policy, bool fused_cas, const Deadline& dl,
                             const dfm_trace* trace);

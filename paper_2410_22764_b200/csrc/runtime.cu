@@ -49,7 +49,26 @@ Ctx::~Ctx() {
   if (pinned) cudaFreeHost(pinned);
   if (d_scalars) cudaFree(d_scalars);
   if (h_scalars) cudaFreeHost(h_scalars);
+  if (copy_stream) {
+    cudaStreamSynchronize(copy_stream);
+    cudaStreamDestroy(copy_stream);
+  }
+  for (auto e : chunk_events) cudaEventDestroy(e);
   if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+cudaStream_t Ctx::copy() {
+  if (!copy_stream) DFM_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  return copy_stream;
+}
+
+const cudaEvent_t* Ctx::chunk_event_pool(uint32_t count) {
+  while (chunk_events.size() < count) {
+    cudaEvent_t e;
+    DFM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    chunk_events.push_back(e);
+  }
+  return chunk_events.data();
 }
 
 void* Ctx::slot(const std::string& name, size_t bytes) {

@@ -34,6 +34,10 @@ constexpr uint32_t kSliceBytes = 192u << 10;
 
 struct Layout {
   uint32_t R = 0, W = 0, nW = 0, E = 0;  // E = W*k
+  // bucket order is chunk-major: chunks of Wc windows (the first Wc*W states, ...)
+  // each hold their transitions range-major, so a chunk's layout can be built as
+  // soon as its rows are in HBM (pipelined upload); one chunk = plain range-major
+  uint32_t Wc = 0, nC = 0;
   uint64_t n = 0, T = 0;
   uint32_t k = 0;
   uint16_t* tgt = nullptr;
@@ -53,11 +57,12 @@ __device__ __forceinline__ uint32_t lanemask_lt_() {
 
 // ---- layout build: per-window range histogram (w-major) + in-window prefix
 __global__ void __launch_bounds__(512) lay_count_kernel(const uint32_t* __restrict__ delta, Layout L,
-                                                        uint32_t* __restrict__ cnt_w) {
+                                                        uint32_t* __restrict__ cnt_w,
+                                                        uint32_t w_begin, uint32_t w_end) {
   extern __shared__ uint32_t s_h[];  // [R]
   __shared__ uint32_t s_warp[512 / 32 + 1];
   const uint64_t pol = policy_evict_first();
-  for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
+  for (uint32_t w = w_begin + blockIdx.x; w < w_end; w += gridDim.x) {
     for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) s_h[j] = 0;
     __syncthreads();
     const uint64_t q0 = (uint64_t)w * L.W;
@@ -144,12 +149,17 @@ struct LayOffIn {
   const uint32_t* cnt;
   __device__ uint32_t operator()(uint64_t i) const { return cnt[i]; }
 };
+// one chunk's cells in (range j, window w0 + x) order, x < wc -> off(j, w), absolute
 struct LayOffOut {
   uint32_t* off;
-  uint64_t count;
+  uint32_t nW, wc, w0;
+  uint32_t base;     // transitions of the chunks before
+  uint64_t count;    // cells of this chunk (R * wc)
+  bool last;         // final chunk: off[R * nW] = T
   __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
-    off[i] = excl;
-    if (i + 1 == count) off[count] = excl + v;
+    const uint64_t j = i / wc, x = i - j * wc;
+    off[j * nW + w0 + x] = base + excl;
+    if (last && i + 1 == count) off[(count / wc) * nW] = base + excl + v;
   }
 };
 
@@ -168,7 +178,8 @@ __device__ __forceinline__ void lay_stage(uint32_t t, uint32_t a, uint32_t x, ui
 }
 
 __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __restrict__ delta,
-                                                           Layout L) {
+                                                           Layout L, uint32_t w_begin,
+                                                           uint32_t w_end) {
   // s_cur[R], s_off[R], s_pre[R+1], then u16 s_lsf[E], s_tgt[E], s_j[E]
   extern __shared__ uint32_t s_lay[];
   uint32_t* s_cur = s_lay;
@@ -185,14 +196,14 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
 #pragma unroll
     for (uint32_t u = 0; u < kPf; ++u) {
       const uint32_t j = threadIdx.x + u * blockDim.x;
-      if (w < L.nW && j < L.R) {
+      if (w < w_end && j < L.R) {
         pf_off[u] = L.off[(uint64_t)j * L.nW + w];
         pf_pre[u] = L.pre[(uint64_t)w * L.R + j];
       }
     }
   };
-  prefetch(blockIdx.x);
-  for (uint32_t w = blockIdx.x; w < L.nW; w += gridDim.x) {
+  prefetch(w_begin + blockIdx.x);
+  for (uint32_t w = w_begin + blockIdx.x; w < w_end; w += gridDim.x) {
     const uint64_t q0 = (uint64_t)w * L.W;
     const uint32_t wn = (uint32_t)(L.n - q0 < L.W ? L.n - q0 : L.W);
     const uint32_t ew = wn * L.k;
@@ -324,32 +335,40 @@ __global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32
     for (uint32_t i = threadIdx.x; i < nwords / 4; i += blockDim.x) s_slice4[i] = __ldg(src4 + i);
     for (uint32_t i = (nwords / 4) * 4 + threadIdx.x; i < nwords; i += blockDim.x)
       s_slice[i] = __ldg(ids + w0 + i);
-    if (threadIdx.x <= j1 - j0) s_bound[threadIdx.x] = L.off[(uint64_t)(j0 + threadIdx.x) * L.nW];
-    __syncthreads();
-    // range by range (no per-element range search); 8 targets per thread-step
-    for (uint32_t r = 0; r < j1 - j0; ++r) {
-      const uint32_t start = s_bound[r], end = s_bound[r + 1];
-      const uint32_t* sl = s_slice;
-      const uint32_t sb = r * kRs;
-      for (uint32_t e0 = start + threadIdx.x; e0 < end; e0 += 8 * blockDim.x) {
-        uint32_t t[8];
+    for (uint32_t ch = 0; ch < L.nC; ++ch) {
+      // bucket starts of ranges j0..j1 inside chunk ch (its end after the last range)
+      if (threadIdx.x <= j1 - j0) {
+        const uint32_t j = j0 + threadIdx.x;
+        s_bound[threadIdx.x] =
+            j < L.R ? L.off[(uint64_t)j * L.nW + (uint64_t)ch * L.Wc]
+                    : (ch + 1 < L.nC ? (ch + 1) * L.Wc * L.E : (uint32_t)L.T);
+      }
+      __syncthreads();
+      // range by range (no per-element range search); 8 targets per thread-step
+      for (uint32_t r = 0; r < j1 - j0; ++r) {
+        const uint32_t start = s_bound[r], end = s_bound[r + 1];
+        const uint32_t* sl = s_slice;
+        const uint32_t sb = r * kRs;
+        for (uint32_t e0 = start + threadIdx.x; e0 < end; e0 += 8 * blockDim.x) {
+          uint32_t t[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t e = e0 + u * blockDim.x;
-          uint32_t x = 0;
-          if (e < end)
-            asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
-                : "=r"(x) : "l"(L.tgt + e), "l"(pol));
-          t[u] = x;
-        }
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t e = e0 + u * blockDim.x;
+            uint32_t x = 0;
+            if (e < end)
+              asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                  : "=r"(x) : "l"(L.tgt + e), "l"(pol));
+            t[u] = x;
+          }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t e = e0 + u * blockDim.x;
-          if (e < end) vout[e] = (V)slice_id<kIdBits>(sl, sb + t[u]);
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t e = e0 + u * blockDim.x;
+            if (e < end) vout[e] = (V)slice_id<kIdBits>(sl, sb + t[u]);
+          }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 

@@ -75,6 +75,7 @@ struct InsertParams {
   const uint32_t* present;
   const uint32_t* present_pre;
   const uint32_t* cand;  // filtered passes: the states left for the table (m = their count)
+  uint64_t i0;           // first index (pipelined first pass: one chunk of states)
 };
 
 // L2 eviction policies: the delta stream is read once per pass (evict first) so
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_ids = policy_evict_last();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t start = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t start = p.i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t base = start - (threadIdx.x & 31); base < p.m; base += stride) {
     const uint64_t i = base + (threadIdx.x & 31);
     const bool valid = i < p.m;
@@ -892,17 +893,27 @@ bool layout_possible(uint64_t n, uint32_t k) {
          T >= kBlockedMinTransitions && !blocked_disabled();
 }
 
-void build_layout(Ctx& ctx, const DevDfa& d, Layout& L) {
+// source window of the layout: W*k ~ kWinElems transitions, and the scatter kernel
+// stages 6 bytes per window transition + 12 per range in shared memory
+uint32_t layout_window(uint64_t n, uint32_t k) {
+  const uint64_t R = ceil_div(n, kRs);
+  uint32_t W = std::max<uint32_t>(32, (kWinElems / k) & ~31u);
+  while (W > 32 && R * 12 + 4 + (uint64_t)W * k * 6 > (227u << 10))
+    W = std::max<uint32_t>(32, (W / 2) & ~31u);
+  return W;
+}
+
+// layout buffers and geometry; chunks of wc windows (0: one chunk)
+void layout_init(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t wc) {
   L.n = d.n;
   L.k = d.k;
   L.T = L.n * L.k;
   L.R = (uint32_t)ceil_div(L.n, kRs);
-  L.W = std::max<uint32_t>(32, (kWinElems / L.k) & ~31u);
-  // the scatter kernel stages 6 bytes per window transition + 12 per range in smem
-  while (L.W > 32 && (uint64_t)L.R * 12 + 4 + (uint64_t)L.W * L.k * 6 > (227u << 10))
-    L.W = std::max<uint32_t>(32, (L.W / 2) & ~31u);
+  L.W = layout_window(L.n, L.k);
   L.E = L.W * L.k;
   L.nW = (uint32_t)ceil_div(L.n, L.W);
+  L.Wc = wc == 0 ? L.nW : std::min(wc, L.nW);
+  L.nC = (uint32_t)ceil_div(L.nW, L.Wc);
   const uint64_t cells = (uint64_t)L.R * L.nW;
   L.tgt = ctx.slot_t<uint16_t>("ly.tgt", L.T);
   L.lsf = ctx.slot_t<uint16_t>("ly.lsf", (uint64_t)L.nW * L.E);
@@ -911,23 +922,72 @@ void build_layout(Ctx& ctx, const DevDfa& d, Layout& L) {
   L.pre = ctx.slot_t<uint16_t>("ly.pre", cells);
   L.wstart = ctx.slot_t<uint32_t>("ly.wstart", L.nW + 1);
   L.v = ctx.slot("ly.v", L.T * 4);
-  uint32_t* cnt_w = ctx.slot_t<uint32_t>("ly.cntw", cells);
-  uint32_t* cnt_j = ctx.slot_t<uint32_t>("ly.cntj", cells);
+}
+
+// chunk ch of the layout: its windows' range histograms, their bucket offsets
+// (chunk-major order: the chunk's base is the transitions before it) and the
+// scatter; needs only the chunk's rows of delta
+void layout_chunk(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t ch) {
+  const uint32_t w0 = ch * L.Wc, w1 = std::min(L.nW, w0 + L.Wc), wc = w1 - w0;
+  const uint64_t cells = (uint64_t)L.R * wc;
+  uint32_t* cnt_w = ctx.slot_t<uint32_t>("ly.cntw", (uint64_t)L.R * L.nW);
+  uint32_t* cnt_j = ctx.slot_t<uint32_t>("ly.cntj", (uint64_t)L.R * L.nW);
+  const uint64_t ct = std::min<uint64_t>((uint64_t)w1 * L.W, L.n) * L.k - (uint64_t)w0 * L.E;
   // delta read twice + tgt/lsf writes + the count/offset matrices
-  ProfScope ps(ctx, "layout", L.T * (4ull + 4 + 2 + 2 + 4) + cells * (4ull * 4 + 2 * 2));
-  const unsigned grid = (unsigned)std::min<uint64_t>(L.nW, (uint64_t)ctx.num_sms * 4);
-  lay_count_kernel<<<grid, 512, L.R * 4, ctx.stream>>>(d.delta, L, cnt_w);
+  ProfScope ps(ctx, "layout", ct * (4ull + 4 + 2 + 2 + 4) + cells * (4ull * 4 + 2 * 2));
+  const unsigned grid = (unsigned)std::min<uint64_t>(wc, (uint64_t)ctx.num_sms * 4);
+  lay_count_kernel<<<grid, 512, L.R * 4, ctx.stream>>>(d.delta, L, cnt_w, w0, w1);
   DFM_LAUNCH_CHECK();
-  lay_transpose_kernel<<<dim3((unsigned)ceil_div(L.R, 32), (unsigned)ceil_div(L.nW, 32)),
-                         dim3(32, 8), 0, ctx.stream>>>(cnt_w, cnt_j, L.nW, L.R);
+  lay_transpose_kernel<<<dim3((unsigned)ceil_div(L.R, 32), (unsigned)ceil_div(wc, 32)),
+                         dim3(32, 8), 0, ctx.stream>>>(cnt_w + (uint64_t)w0 * L.R,
+                                                       cnt_j + (uint64_t)w0 * L.R, wc, L.R);
   DFM_LAUNCH_CHECK();
-  prims::lookback_scan(ctx, "sc.lyoff", cells, LayOffIn{cnt_j}, LayOffOut{L.off, cells}, nullptr);
+  prims::lookback_scan(ctx, "sc.lyoff", cells, LayOffIn{cnt_j + (uint64_t)w0 * L.R},
+                       LayOffOut{L.off, L.nW, wc, w0, w0 * L.E, cells, ch + 1 == L.nC}, nullptr);
   const size_t smem = (size_t)L.R * 12 + 4 + (size_t)L.E * 6;
   DFM_CUDA(cudaFuncSetAttribute(lay_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
-  lay_scatter_kernel<<<(unsigned)std::min<uint64_t>(L.nW, (uint64_t)ctx.num_sms * 2), 1024, smem,
-                       ctx.stream>>>(d.delta, L);
+  lay_scatter_kernel<<<(unsigned)std::min<uint64_t>(wc, (uint64_t)ctx.num_sms * 2), 1024, smem,
+                       ctx.stream>>>(d.delta, L, w0, w1);
   DFM_LAUNCH_CHECK();
+}
+
+// pipelined upload: validate one chunk of rows as it lands (the reference rejects
+// out-of-range targets; a bad one is zeroed so no consumer gathers out of bounds,
+// and the run fails after the first pass)
+__global__ void sanitize_rows_kernel(uint32_t* __restrict__ delta, uint64_t n, uint32_t k,
+                                     uint64_t q0, uint64_t q1, unsigned long long* bad) {
+  const uint64_t len = q1 - q0, total = len * k;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool b = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const uint64_t a = i / len;
+    uint32_t* x = delta + a * n + q0 + (i - a * len);
+    if (*x >= n) {
+      *x = 0;
+      b = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1ull);
+}
+
+void wait_chunk(Ctx& ctx, const DevDfa& d, uint32_t c) {
+  DFM_CUDA(cudaStreamWaitEvent(ctx.stream, d.ready[c], 0));
+  const uint64_t q0 = c * d.chunk_states, q1 = std::min<uint64_t>(d.n, q0 + d.chunk_states);
+  ProfScope p(ctx, "init", (q1 - q0) * d.k * 4ull);
+  sanitize_rows_kernel<<<grid_for(ctx, (q1 - q0) * d.k), 256, 0, ctx.stream>>>(d.delta, d.n, d.k, q0,
+                                                                             q1, d.bad);
+  DFM_LAUNCH_CHECK();
+}
+
+uint32_t layout_chunk_windows() {  // DFM_LAYOUT_CHUNK_WINDOWS (tests): force chunking
+  const char* e = getenv("DFM_LAYOUT_CHUNK_WINDOWS");
+  return e ? (uint32_t)strtoul(e, nullptr, 10) : 0u;
+}
+
+void build_layout(Ctx& ctx, const DevDfa& d, Layout& L) {
+  layout_init(ctx, d, L, layout_chunk_windows());
+  for (uint32_t ch = 0; ch < L.nC; ++ch) layout_chunk(ctx, d, L, ch);
 }
 
 template <int kIdBits>
@@ -1057,6 +1117,14 @@ void group_partitioned(Ctx& ctx, uint64_t m, const uint32_t* act, unsigned long 
 
 }  // namespace
 
+uint64_t sortpr_upload_chunk(uint64_t n, uint32_t k) {
+  // the first pass consumes chunks only on its tiny direct table (2^(k+1) <= 4096 keys)
+  if (k == 0 || k + 1 > 12 || n * k * 4 < (256ull << 20)) return 0;
+  const uint32_t W = layout_window(n, k);
+  const uint64_t wc = std::max<uint64_t>(1, ((64ull << 20) / (4ull * k)) / W);
+  return wc * W;
+}
+
 AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {
   AlgoOut out;
   const uint64_t n = d.n;
@@ -1137,6 +1205,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint64_t m = n;
   uint64_t seed = 0x5EED0001ull;
   std::vector<uint32_t> trace_buf;
+  bool prog_pending = d.nready > 0;  // pipelined upload: rows still landing chunk by chunk
 
   while (true) {
     if (dl.expired()) {
@@ -1165,6 +1234,11 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       // blocked signature builder whenever most states are active (it streams all n*k
       // transitions); sparse late passes gather directly
       const bool blocked = lay_ok && m >= n / 4 && n * (uint64_t)mirror_bits / 8 > kBlockedMinMirror;
+      if (prog_pending && (blocked || act != nullptr || mirror_bits != 1 || !packed || !direct ||
+                           table > kSmallTable)) {
+        for (uint32_t c = 0; c < d.nready; ++c) wait_chunk(ctx, d, c);  // not chunkable
+        prog_pending = false;
+      }
       // partitioned grouping for the large passes (not the tiny direct tables)
       const bool part = blocked && part_on && !force_global && !(direct && table <= kSmallTable) &&
                         m >= kPartMinStates && m < (1ull << 31);
@@ -1249,6 +1323,26 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           case 4: launch_insert_keys<4>(ctx, ip, !packed, direct, table, filtered); break;
           default: launch_insert_keys<0>(ctx, ip, !packed, direct, table, filtered); break;
         }
+      } else if (prog_pending) {
+        // first pass over the pipelined upload: each chunk's keys (tiny direct table)
+        // and its share of the layout as soon as its rows land
+        const bool lay_early = lay_ok && n > kBlockedMinMirror && !lay_built;
+        if (lay_early) {
+          layout_init(ctx, d, lay, (uint32_t)(d.chunk_states / layout_window(n, k)));
+          lay_built = true;
+        }
+        for (uint32_t c = 0; c < d.nready; ++c) {
+          wait_chunk(ctx, d, c);
+          InsertParams ipc = ip;
+          ipc.i0 = c * d.chunk_states;
+          ipc.m = std::min<uint64_t>(n, ipc.i0 + d.chunk_states);
+          {
+            ProfScope p(ctx, "sig", (ipc.m - ipc.i0) * (4ull * k + k / 8 + 4 + 1 + 16 + 4));
+            launch_insert<1>(ctx, ipc, false, true, table);
+          }
+          if (lay_early) layout_chunk(ctx, d, lay, c);
+        }
+        prog_pending = false;
       } else {
         // delta 4k + gathered ids (mirror width) k + own id 4 + lead 1 + active id 4 +
         // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
@@ -1282,7 +1376,10 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 64, cudaMemcpyDeviceToHost, ctx.stream));
+    if (d.nready) DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 40, d.bad, 8, cudaMemcpyDeviceToHost,
+                                           ctx.stream));
     ctx.sync();
+    if (d.nready && ctx.h_scalars[40]) throw Error(DFM_ERR_INVALID, "transition target out of range");
     if (ctx.h_scalars[2] & kFlagOverflow) {  // partitioned grouping overflowed a bucket:
       force_global = true;                    // redo the pass with the global table
       continue;

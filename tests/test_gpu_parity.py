@@ -308,6 +308,20 @@ def test_blocked_signature_builder(eng, eng_radix, monkeypatch, n, k, seed):
     dd.free()
 
 
+@pytest.mark.parametrize("n,k,seed,wc", [(12_000_000, 4, 3, 97), (9_000_003, 5, 8, 1000),
+                                         (17_000_000, 2, 11, 31)])
+def test_chunked_layout(eng, monkeypatch, n, k, seed, wc):
+    """Chunk-major layout (the pipelined upload builds it chunk by chunk as the
+    rows arrive): forced chunking of wc windows gives the unchunked result."""
+    dd = eng.random_dfa_device(n, k, seed, 0.5)
+    nb, it, lab = _device_labels(eng, dd, n)
+    monkeypatch.setenv("DFM_LAYOUT_CHUNK_WINDOWS", str(wc))
+    nb1, it1, lab1 = _device_labels(eng, dd, n)
+    assert (nb, it) == (nb1, it1)
+    assert bool((lab == lab1).all())
+    dd.free()
+
+
 def test_blocked_builder_vs_oracle(eng):
     """One blocked-path size checked straight against the CPU oracle."""
     pair = O.random_dfa(17_000_000, 2, 11, 0.5)

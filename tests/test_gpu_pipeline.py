@@ -1,0 +1,54 @@
+"""Pipelined host upload for sortPR (capi.cu upload_progressive): the rows land
+chunk by chunk on a copy stream while the first pass and the layout build consume
+them.  Must give exactly the device-resident result (itself pinned against the
+oracle), and reject out-of-range targets like the one-shot upload does."""
+import numpy as np
+import pytest
+
+import paper_2410_22764_b200 as dfm
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_result(eng, dd, n):
+    import torch
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    nb, st = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
+    assert st.status == dfm.RunStatus.ok
+    return nb, st.iterations, out.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("n,k,seed", [(17_000_001, 4, 21), (40_000_000, 2, 22),
+                                      (9_000_000, 8, 23)])
+def test_pipelined_upload_matches_device_run(eng, n, k, seed):
+    dd = eng.random_dfa_device(n, k, seed, 0.5)
+    nb, it, lab = _device_result(eng, dd, n)
+    host = dd.download()
+    dd.free()
+    r = eng.sort_pr(host)
+    assert r.stats.status == dfm.RunStatus.ok
+    assert (r.partition.num_blocks, r.stats.iterations) == (nb, it)
+    assert (r.partition.block == lab).all()
+
+
+def test_pipelined_upload_non_identity_partition(eng):
+    delta, acc = O.vlts_dfa(1000, 20_000_000, 4)
+    d = dfm.Dfa(20_000_000, 4, delta, acc, 0)
+    r = eng.sort_pr(d)
+    dd = eng.upload(d)
+    nb, it, lab = _device_result(eng, dd, 20_000_000)
+    dd.free()
+    assert r.partition.num_blocks == nb < 20_000_000 and r.stats.iterations == it
+    assert (r.partition.block == lab).all()
+
+
+def test_pipelined_upload_rejects_bad_target(eng):
+    n, k = 17_000_000, 4
+    delta, acc = O.random_dfa(n, k, 5, 0.5)
+    delta[3, n - 1] = n  # last chunk, last row
+    with pytest.raises(dfm.EngineError):
+        eng.sort_pr(dfm.Dfa(n, k, delta, acc, 0))
+    delta[3, n - 1] = 0
+    r = eng.sort_pr(dfm.Dfa(n, k, delta, acc, 0))
+    assert r.stats.status == dfm.RunStatus.ok
