@@ -1399,6 +1399,12 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     }
     if (fresh == 0) break;  // fixpoint, min_sort.hpp:111-117
     B = B_next;
+    if (B == n && !(trace && trace->on_pass)) {
+      // every block a singleton: the next pass splits nothing and is the fixpoint
+      // pass the reference counts; no active state is left to run it on
+      ++out.iterations;
+      break;
+    }
     if (!act_scanned && m > 0 && ctx.h_scalars[8] != 0) {
       // some states became singletons: compact the active list (ascending q)
       ProfScope p(ctx, "scan", m * 9ull);

@@ -393,3 +393,19 @@ def test_naive_one_barrier_kernel(eng, monkeypatch, policy, case):
     r2 = eng.naive_pr(d, dfm.PrOptions(policy=policy))
     assert r2.stats.iterations == r.stats.iterations
     assert (r2.partition.block == r.partition.block).all()
+
+
+def test_hashed_blocked_pass_with_repeated_keys(eng, eng_radix, monkeypatch):
+    """vlts(1000, 2e7, 8): hashed (9 x 10-bit ids) blocked passes whose keys are
+    mostly repeated — the signature rows deferred to the filter's candidates are
+    then produced by a second window pass; same result as the direct path."""
+    delta, acc = O.vlts_dfa(1000, 20_000_000, 8)
+    dd = eng.upload(dfm.Dfa(20_000_000, 8, delta, acc, 0))
+    nb, it, lab = _device_labels(eng, dd, 20_000_000)
+    monkeypatch.setenv("DFM_SORTPR_BLOCKED", "0")
+    nb0, it0, lab0 = _device_labels(eng, dd, 20_000_000)
+    monkeypatch.delenv("DFM_SORTPR_BLOCKED")
+    nbr, itr, labr = _device_labels(eng_radix, dd, 20_000_000)
+    assert (nb, it) == (nb0, it0) == (nbr, itr) and nb <= 1000
+    assert bool((lab == lab0).all()) and bool((lab == labr).all())
+    dd.free()
