@@ -136,8 +136,17 @@ def int8_peak():
                     "profiles/int8_peak.json)"
 
 
-def ncu_traffic(family: str):
-    """dram bytes per launch for a kernel family from the committed ncu summary."""
+# the workloads profiles/ncu_traffic.json was captured on: (family, algo, n, k)
+TRAFFIC_WORKLOAD = {"gemm": ("fib", "trans", 12, 1)}
+TRAFFIC_DEFAULT = ("random", "sort", 100_000_000, 4)
+
+
+def ncu_traffic(family: str, args=None):
+    """dram bytes per step for a kernel family from the committed ncu summary, or
+    None when this run is not the workload that summary was captured on."""
+    if args is not None and (args.family, args.algo, args.n, args.k) != \
+            TRAFFIC_WORKLOAD.get(family, TRAFFIC_DEFAULT):
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
@@ -364,7 +373,7 @@ def run_ours(args, rank: int, world: int, local: int):
     if fam is not None:
         name, (scopes, fms, fbytes) = fam
         achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
-        traffic = ncu_traffic(name)
+        traffic = ncu_traffic(name, args)
         bound, unit = "hbm", "GB/s"
         if name == "gemm":  # tcgen05 kind::i8 squaring: the family counts 2*Vp^3 int8 ops
             bound, unit = "tensor", "TOP/s"
@@ -494,7 +503,7 @@ def run_sharded(args, rank: int, world: int, local: int):
         name, (scopes, fms, fbytes) = fam
         achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
         roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
-                    "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(name),
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
                     "peak_source": peak_src, "rank": 0,
                     "families_ms_per_step": {k: v[1] / args.steps for k, v in prof.items()}}
     cfg = config(args, world, r.iterations, r.num_blocks)
