@@ -76,6 +76,9 @@ struct InsertParams {
   const uint32_t* present_pre;
   const uint32_t* cand;  // filtered passes: the states left for the table (m = their count)
   uint64_t i0;           // first index (pipelined first pass: one chunk of states)
+  // relabel-in-place passes: the slot (key or key rank) + id_off becomes the new id
+  uint32_t* ids_out;
+  uint32_t id_off;
 };
 
 // L2 eviction policies: the delta stream is read once per pass (evict first) so
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       }
       if (kDirect && p.present) {  // many distinct keys: consecutive states rarely share one
         if (valid[u]) {
+          if (p.ids_out) p.ids_out[p.act ? p.act[i] : (uint32_t)i] = (uint32_t)s[u] + p.id_off;
           atomicMax(&p.slots[s[u]].rep, ~(uint32_t)i);
           atomicAdd(&p.slots[s[u]].info, 1u | (lead[u] ? 0x80000000u : 0u));
         }
@@ -352,6 +356,7 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
                                  : (uint32_t)make_key<kIdBits, false, kK>(p, i, q, b, pol_stream,
                                                                           pol_ids);
     p.slot_of[i] = s;
+    if (p.ids_out) p.ids_out[q] = s + p.id_off;
     // lanes are in ascending i: the lowest lane of each key group updates for all
     const uint32_t peers = __match_any_sync(vmask, s);
     const uint32_t leads = __ballot_sync(vmask, p.lead[q] != 0) & peers;
@@ -602,6 +607,42 @@ __global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* 
   }
 }
 
+// relabel-in-place passes (direct tables: the key, or its rank among the keys
+// present, is the new id — any numbering gives the same partition): one thread per
+// group marks its minimum member as the block leader (old leaders are the minimum
+// of their group too) and counts groups; *single: a one-member group exists
+__global__ void __launch_bounds__(256) rip_groups_kernel(const Slot* __restrict__ slots,
+                                                         uint64_t ntab,
+                                                         const uint32_t* __restrict__ act,
+                                                         uint8_t* __restrict__ lead,
+                                                         unsigned long long* groups,
+                                                         unsigned long long* single) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t mine = 0;
+  bool one = false;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntab; t += stride) {
+    const uint2 sl = *reinterpret_cast<const uint2*>(&slots[t].rep);
+    if ((sl.y & 0x7FFFFFFFu) == 0) continue;
+    const uint32_t i = ~sl.x;
+    lead[act ? act[i] : i] = 1;
+    ++mine;
+    one |= (sl.y & 0x7FFFFFFFu) == 1u;
+  }
+  mine = __reduce_add_sync(0xffffffffu, mine);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(groups, (unsigned long long)mine);
+  if (__any_sync(0xffffffffu, one) && (threadIdx.x & 31) == 0) atomicOr(single, 1ull);
+}
+
+// states of one-member groups leave the active list
+__global__ void __launch_bounds__(256) rip_flag_kernel(uint64_t m, const uint32_t* __restrict__ act,
+                                                       const uint32_t* __restrict__ slot_of,
+                                                       const Slot* __restrict__ slots,
+                                                       uint8_t* __restrict__ flag) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+    flag[act ? act[i] : (uint32_t)i] = (slots[slot_of[i]].info & 0x7FFFFFFFu) >= 2 ? 1 : 0;
+}
+
 struct PresentIn {
   const uint32_t* present;
   __device__ uint32_t operator()(uint64_t w) const { return __popc(present[w]); }
@@ -783,6 +824,11 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   else
     insert_kernel<32, false, false, kK, true><<<grid, 256, 0, ctx.stream>>>(p);
   DFM_LAUNCH_CHECK();
+}
+
+bool rip_enabled() {  // DFM_SORTPR_RIP=0: resolve/apply on every pass (tests)
+  const char* e = getenv("DFM_SORTPR_RIP");
+  return e == nullptr || e[0] != '0';
 }
 
 bool small_enabled() {
@@ -1195,6 +1241,11 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     DFM_LAUNCH_CHECK();
   };
   build_mirror(B);
+  // B bounds the ids (key packing, mirror width, fresh ids start there); nb counts the
+  // blocks.  They differ after a relabel-in-place pass, whose ids are direct-table
+  // slots (the key, not all of which occur)
+  uint32_t nb = B;
+  const bool rip_on = rip_enabled();
   Layout lay;
   bool lay_built = false;
   bool force_global = false;
@@ -1222,6 +1273,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     DFM_CUDA(cudaMemsetAsync(sc + 1, 0, 24, ctx.stream));
     DFM_CUDA(cudaMemsetAsync(sc + 8, 0, 8, ctx.stream));
     uint32_t* act_next = act_buf[act_sel ^ 1];
+    bool rip = false;        // this pass relabels in place (no resolve / apply)
+    uint64_t rip_bound = 0;  // its id bound: the direct table's size
+    const Slot* rip_slots = nullptr;
     bool act_scanned = false;  // the partitioned path compacts inside the pass
     if (m > 0) {
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
@@ -1316,6 +1370,17 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       InsertParams ip{d.delta, n, k, block, ids, act, lead, filtered ? ncand : m, w, seed, cap,
                       slots, slot_of, packed ? nullptr : sig, row, keys, present,
                       present ? present_pre : nullptr, filtered ? cand : nullptr};
+      // direct tables whose slot can become the id at once: the tiny smem-aggregated
+      // ones (the ids are gathered from a mirror or were gathered by the layout) and
+      // the rank-compacted ones (slot = rank of the key: dense ids)
+      // States off the active list keep their ids (< B): the new ids then start at B.
+      rip = rip_on && packed && direct && !filtered &&
+            (present != nullptr || (table <= kSmallTable && (blocked || mirror_bits < 32))) &&
+            (act == nullptr || (uint64_t)B + cap < (1ull << 32));
+      const uint32_t rip_off = act ? B : 0u;
+      rip_bound = rip_off + cap;
+      ip.ids_out = rip ? block : nullptr;
+      ip.id_off = rip_off;
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
         switch (k) {
@@ -1357,6 +1422,13 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           default: launch_insert<32>(ctx, ip, !packed, direct, table); break;
         }
       }
+      if (rip) {
+        ProfScope p(ctx, "scan", cap * 8ull);
+        rip_groups_kernel<<<grid_for(ctx, cap), 256, 0, ctx.stream>>>(
+            slots, cap, act, lead, reinterpret_cast<unsigned long long*>(sc + 1),
+            reinterpret_cast<unsigned long long*>(sc + 8));
+        DFM_LAUNCH_CHECK();
+      } else {
       {
         ProfScope p(ctx, "scan", m * (4ull + 16 + 4 + 4 + 1));  // slot_of, slot, own id, res, st
         resolve_kernel<<<grid_for(ctx, ceil_div(m, kResolveItems)), 256, 0, ctx.stream>>>(
@@ -1374,6 +1446,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         DFM_LAUNCH_CHECK();
       }
       }
+      rip_slots = slots;
+      }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 64, cudaMemcpyDeviceToHost, ctx.stream));
     if (d.nready) DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 40, d.bad, 8, cudaMemcpyDeviceToHost,
@@ -1388,18 +1462,31 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       seed = seed * kGolden + 0x632BE59BD9B4E019ull;
       continue;
     }
-    const uint64_t fresh = ctx.h_scalars[1];
+    // regular pass: [1] = fresh ids; relabel-in-place pass: [1] = groups of the active
+    // states (the others are singleton blocks)
+    const uint32_t nb_next =
+        rip ? (uint32_t)(n - m + ctx.h_scalars[1]) : nb + (uint32_t)ctx.h_scalars[1];
+    const uint64_t fresh = nb_next - nb;
     ++out.iterations;
-    const uint32_t B_next = B + (uint32_t)fresh;
+    const uint32_t B_next = rip ? (uint32_t)rip_bound : B + (uint32_t)fresh;
     if (trace && trace->on_pass) {
       trace_buf.resize(n);
       DFM_CUDA(cudaMemcpyAsync(trace_buf.data(), block, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
       ctx.sync();
-      trace->on_pass(trace->user, out.iterations, trace_buf.data(), (uint32_t)n, B_next);
+      trace->on_pass(trace->user, out.iterations, trace_buf.data(), (uint32_t)n, nb_next);
     }
-    if (fresh == 0) break;  // fixpoint, min_sort.hpp:111-117
+    if (fresh == 0) {  // fixpoint, min_sort.hpp:111-117 (a relabelled pass renamed the ids)
+      B = B_next;
+      break;
+    }
     B = B_next;
-    if (B == n && !(trace && trace->on_pass)) {
+    nb = nb_next;
+    if (rip && m > 0 && ctx.h_scalars[8] != 0) {  // one-member groups: flags for the compaction
+      ProfScope p(ctx, "relabel", m * 9ull);
+      rip_flag_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, act, slot_of, rip_slots, flag);
+      DFM_LAUNCH_CHECK();
+    }
+    if (nb == n && !(trace && trace->on_pass)) {
       // every block a singleton: the next pass splits nothing and is the fixpoint
       // pass the reference counts; no active state is left to run it on
       ++out.iterations;
@@ -1421,19 +1508,19 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     build_mirror(B);  // id mirror for the next pass's gathers
   }
   out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
-  if (B == n) {  // every block a singleton: first-occurrence labels are the identity
+  if (nb == n) {  // every block a singleton: first-occurrence labels are the identity
     ProfScope p(ctx, "canon", n * 4);
     iota_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(out.canon_dev, n);
     DFM_LAUNCH_CHECK();
-    out.num_blocks = B;
+    out.num_blocks = nb;
     out.canon_identity = true;
   } else {
-    uint32_t* cob = ctx.slot_t<uint32_t>("sh.cob", n);
+    uint32_t* cob = ctx.slot_t<uint32_t>("sh.cob", std::max<uint64_t>(n, B));
     ProfScope p(ctx, "canon", n * 13ull);
     prims::lookback_scan(ctx, "sc.canon", n, LeadIn{lead}, LeadOut{block, cob}, sc + 5);
     canon_gather_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, cob, out.canon_dev);
     DFM_LAUNCH_CHECK();
-    out.num_blocks = B;  // one leader per block
+    out.num_blocks = nb;  // one leader per block
   }
   out.status = DFM_STATUS_OK;
   return out;

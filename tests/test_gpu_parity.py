@@ -409,3 +409,29 @@ def test_hashed_blocked_pass_with_repeated_keys(eng, eng_radix, monkeypatch):
     assert (nb, it) == (nb0, it0) == (nbr, itr) and nb <= 1000
     assert bool((lab == lab0).all()) and bool((lab == labr).all())
     dd.free()
+
+
+def test_host_loop_relabel_in_place_vs_oracle(eng, monkeypatch):
+    """The host-driven pass loop (small-n kernel off) with relabel-in-place direct
+    passes (slot = new id) against the oracle, and against resolve/apply passes."""
+    monkeypatch.setenv("DFM_SORTPR_SMALL", "0")
+    rng = np.random.default_rng(4242)
+    for rnd in range(120):
+        n = int(rng.integers(1, 3000))
+        k = int(rng.integers(0, 6))
+        pair = O.random_dfa(n, k, int(rng.integers(1, 2 ** 62)), [0.0, 0.1, 0.5, 1.0][rnd % 4])
+        d = to_dfa(pair)
+        ref = O.sort_pr(*pair)
+        r = eng.sort_pr(d)
+        assert (r.partition.num_blocks, r.stats.iterations) == (ref.num_blocks, ref.iterations), rnd
+        assert (r.partition.block == ref.block).all(), rnd
+    for pair in (O.fib_dfa(14), O.bit_splitter(9), O.comb_dfa(300, 3), O.random_dfa(200_000, 3, 9)):
+        d = to_dfa(pair)
+        ref = O.sort_pr(*pair)
+        r = eng.sort_pr(d)
+        monkeypatch.setenv("DFM_SORTPR_RIP", "0")
+        r0 = eng.sort_pr(d)
+        monkeypatch.delenv("DFM_SORTPR_RIP")
+        for x in (r, r0):
+            assert (x.partition.num_blocks, x.stats.iterations) == (ref.num_blocks, ref.iterations)
+            assert (x.partition.block == ref.block).all()
