@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(Si
           row[a + 1] = s;
           h = mix64(h + kGolden + s);
         }
-        p.keys[i] = h;
+        p.keys[i] = weak(h, p.seed);
       }
       if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
       {

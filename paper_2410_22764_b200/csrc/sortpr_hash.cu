@@ -40,6 +40,15 @@ namespace {
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 constexpr int kSmallTable = 4096;  // direct tables up to this size aggregate in smem
 
+// first seed of every run; DFM_SORTPR_WEAK_HASH=<bits> (tests) truncates the hashed
+// keys of passes under this seed so that distinct signatures collide and the
+// void-and-retry path runs
+constexpr uint64_t kSeed0 = 0x5EED0001ull;
+__device__ unsigned long long g_weak_mask = ~0ull;
+__device__ __forceinline__ unsigned long long weak(unsigned long long h, uint64_t seed) {
+  return seed == kSeed0 ? (h & g_weak_mask) : h;
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -175,7 +184,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
       row[a + 1] = s[a];
       h = mix64(h + kGolden + s[a]);
     }
-    return h;
+    return weak(h, p.seed);
   }
   if (!kHashed) {
     unsigned long long key = b;
@@ -194,7 +203,7 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
     row[a + 1] = s;
     h = mix64(h + kGolden + s);
   }
-  return h;
+  return weak(h, p.seed);
 }
 
 // K1, hash or large direct table; warp-level aggregation of equal slots
@@ -631,6 +640,43 @@ __global__ void __launch_bounds__(256) rip_groups_kernel(const Slot* __restrict_
   mine = __reduce_add_sync(0xffffffffu, mine);
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(groups, (unsigned long long)mine);
   if (__any_sync(0xffffffffu, one) && (threadIdx.x & 31) == 0) atomicOr(single, 1ull);
+}
+
+// relabel-in-place for filtered (hash-table) passes over ALL states: a state the
+// filter found unique is a singleton block (its own leader) with id B + i; a table
+// state takes B + m + slot, members verified against the group's minimum (a hash
+// collision voids the pass: the ids go to `ids` — swapped in for the block array
+// only after the check — and every leader flag set here is right regardless)
+__global__ void __launch_bounds__(256) rip_hashed_kernel(uint64_t m,
+                                                         const uint32_t* __restrict__ slot_of,
+                                                         const Slot* __restrict__ slots,
+                                                         const uint32_t* __restrict__ sig,
+                                                         uint32_t words, uint32_t row,
+                                                         unsigned long long* collision,
+                                                         uint32_t B, uint32_t* __restrict__ ids,
+                                                         uint8_t* __restrict__ lead,
+                                                         uint8_t* __restrict__ flag) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint32_t s = slot_of[i];
+    if (s == kUnique) {
+      ids[i] = B + (uint32_t)i;
+      lead[i] = 1;
+      flag[i] = 0;
+      continue;
+    }
+    const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
+    const uint32_t rep_i = ~sl.x;
+    if (rep_i != (uint32_t)i && sig != nullptr) {
+      const uint32_t* a = sig + i * (uint64_t)row;
+      const uint32_t* b = sig + (uint64_t)rep_i * row;
+      uint32_t diff = 0;
+      for (uint32_t x = 0; x < words; ++x) diff |= a[x] ^ b[x];
+      if (diff) atomicOr(collision, 1ull);
+    }
+    ids[i] = B + (uint32_t)m + s;
+    flag[i] = (sl.y & 0x7FFFFFFFu) >= 2 ? 1 : 0;
+  }
 }
 
 // states of one-member groups leave the active list
@@ -1254,7 +1300,17 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   const uint32_t* act = nullptr;  // identity at pass 1
   int act_sel = 0;
   uint64_t m = n;
-  uint64_t seed = 0x5EED0001ull;
+  uint64_t seed = kSeed0;
+  {
+    static unsigned long long mask_set = ~0ull;
+    const char* e = getenv("DFM_SORTPR_WEAK_HASH");
+    const unsigned long long mask =
+        e ? ((1ull << std::min(63ul, strtoul(e, nullptr, 10))) - 1) : ~0ull;
+    if (mask != mask_set) {
+      DFM_CUDA(cudaMemcpyToSymbol(g_weak_mask, &mask, sizeof(mask)));
+      mask_set = mask;
+    }
+  }
   std::vector<uint32_t> trace_buf;
   bool prog_pending = d.nready > 0;  // pipelined upload: rows still landing chunk by chunk
 
@@ -1276,6 +1332,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     bool rip = false;        // this pass relabels in place (no resolve / apply)
     uint64_t rip_bound = 0;  // its id bound: the direct table's size
     const Slot* rip_slots = nullptr;
+    bool hrip = false;        // filtered pass relabelled in place (ids into res, swapped in)
+    uint64_t hrip_table = 0;  // states that reached its table
     bool act_scanned = false;  // the partitioned path compacts inside the pass
     if (m > 0) {
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sh.sig", n * (uint64_t)row);
@@ -1381,6 +1439,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       rip_bound = rip_off + cap;
       ip.ids_out = rip ? block : nullptr;
       ip.id_off = rip_off;
+      hrip = rip_on && filtered && act == nullptr && (uint64_t)B + m + cap < (1ull << 32);
+      hrip_table = ncand;
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
         switch (k) {
@@ -1422,7 +1482,22 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           default: launch_insert<32>(ctx, ip, !packed, direct, table); break;
         }
       }
-      if (rip) {
+      if (hrip) {
+        {
+          // slot_of 4 + id 4 + flag 1 (+ lead 1 for unique states) + slot 8 for table states
+          ProfScope p(ctx, "scan", m * 10ull + ncand * 8ull);
+          rip_hashed_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+              m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
+              reinterpret_cast<unsigned long long*>(sc + 2), B, res, lead, flag);
+          DFM_LAUNCH_CHECK();
+        }
+        ProfScope p(ctx, "scan", cap * 8ull);
+        rip_groups_kernel<<<grid_for(ctx, cap), 256, 0, ctx.stream>>>(
+            slots, cap, nullptr, lead, reinterpret_cast<unsigned long long*>(sc + 1),
+            reinterpret_cast<unsigned long long*>(sc + 8));
+        DFM_LAUNCH_CHECK();
+        rip_bound = (uint64_t)B + m + cap;
+      } else if (rip) {
         ProfScope p(ctx, "scan", cap * 8ull);
         rip_groups_kernel<<<grid_for(ctx, cap), 256, 0, ctx.stream>>>(
             slots, cap, act, lead, reinterpret_cast<unsigned long long*>(sc + 1),
@@ -1465,10 +1540,16 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     // regular pass: [1] = fresh ids; relabel-in-place pass: [1] = groups of the active
     // states (the others are singleton blocks)
     const uint32_t nb_next =
-        rip ? (uint32_t)(n - m + ctx.h_scalars[1]) : nb + (uint32_t)ctx.h_scalars[1];
+        rip    ? (uint32_t)(n - m + ctx.h_scalars[1])
+        : hrip ? (uint32_t)(m - hrip_table + ctx.h_scalars[1])  // unique states + groups
+               : nb + (uint32_t)ctx.h_scalars[1];
     const uint64_t fresh = nb_next - nb;
     ++out.iterations;
-    const uint32_t B_next = rip ? (uint32_t)rip_bound : B + (uint32_t)fresh;
+    const uint32_t B_next = (rip || hrip) ? (uint32_t)rip_bound : B + (uint32_t)fresh;
+    if (hrip) {
+      std::swap(block, res);  // verified: the new ids become the block array
+      if (m > hrip_table) ctx.h_scalars[8] = 1;  // unique states leave the active list
+    }
     if (trace && trace->on_pass) {
       trace_buf.resize(n);
       DFM_CUDA(cudaMemcpyAsync(trace_buf.data(), block, n * 4, cudaMemcpyDeviceToHost, ctx.stream));

@@ -435,3 +435,20 @@ def test_host_loop_relabel_in_place_vs_oracle(eng, monkeypatch):
         for x in (r, r0):
             assert (x.partition.num_blocks, x.stats.iterations) == (ref.num_blocks, ref.iterations)
             assert (x.partition.block == ref.block).all()
+
+
+@pytest.mark.parametrize("n,k,seed", [(200_000, 4, 3), (12_000_000, 4, 3)])
+def test_forced_hash_collisions_retry_exactly(eng, monkeypatch, n, k, seed):
+    """DFM_SORTPR_WEAK_HASH truncates the first seed's hashed keys to 10 bits: every
+    hashed pass collides, is voided and redone under the next seed (direct passes,
+    the filtered relabel-in-place pass included) — same result as without."""
+    monkeypatch.setenv("DFM_SORTPR_SMALL", "0")
+    dd = eng.random_dfa_device(n, k, seed, 0.5)
+    nb, it, lab = _device_labels(eng, dd, n)
+    monkeypatch.setenv("DFM_SORTPR_WEAK_HASH", "10")
+    nb1, it1, lab1 = _device_labels(eng, dd, n)
+    monkeypatch.delenv("DFM_SORTPR_WEAK_HASH")
+    _device_labels(eng, dd, n)  # mask restored
+    assert (nb, it) == (nb1, it1)
+    assert bool((lab == lab1).all())
+    dd.free()
