@@ -711,35 +711,63 @@ struct ActOut {
   }
 };
 
-// split: both an accepting and a rejecting state exist (min_sort.hpp:80-88)
+// split: both an accepting and a rejecting state exist (min_sort.hpp:80-88).  Also
+// writes pass 1's 1-bit id mirror.  Four consecutive states per thread (vector
+// accesses); the 8 lanes covering 32 states OR their nibbles into one mirror word.
 __global__ void init_kernel(const uint8_t* __restrict__ acc, uint64_t n,
                             const uint32_t* __restrict__ first2, uint32_t* __restrict__ block,
-                            uint8_t* __restrict__ lead) {
-  const bool split = first2[0] != kNoLeader && first2[1] != kNoLeader;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
-    const uint32_t b = (split && acc[q] == 0) ? 1u : 0u;
-    block[q] = b;
-    // block leaders = minimum state of each initial block (min_partref.hpp:53-63 analogue)
-    lead[q] = ((uint32_t)q == first2[0] || (uint32_t)q == first2[1] ||
-               (!split && (uint32_t)q == 0))
-                  ? 1
-                  : 0;
+                            uint8_t* __restrict__ lead, uint32_t* __restrict__ mirror1) {
+  const uint32_t fa = first2[0], fr = first2[1];
+  const bool split = fa != kNoLeader && fr != kNoLeader;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 4;  // a multiple of 128
+  for (uint64_t q0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+       q0 - 4 * lane < n; q0 += stride) {
+    uint32_t nib = 0;
+    if (q0 + 4 <= n) {
+      const uchar4 a4 = *reinterpret_cast<const uchar4*>(acc + q0);
+      const uint32_t b0 = (split && a4.x == 0), b1 = (split && a4.y == 0),
+                     b2 = (split && a4.z == 0), b3 = (split && a4.w == 0);
+      *reinterpret_cast<uint4*>(block + q0) = make_uint4(b0, b1, b2, b3);
+      uchar4 l4;
+      l4.x = (q0 == fa || q0 == fr || (!split && q0 == 0)) ? 1 : 0;
+      l4.y = (q0 + 1 == fa || q0 + 1 == fr) ? 1 : 0;
+      l4.z = (q0 + 2 == fa || q0 + 2 == fr) ? 1 : 0;
+      l4.w = (q0 + 3 == fa || q0 + 3 == fr) ? 1 : 0;
+      *reinterpret_cast<uchar4*>(lead + q0) = l4;
+      nib = b0 | b1 << 1 | b2 << 2 | b3 << 3;
+    } else {
+      for (uint64_t q = q0; q < n; ++q) {
+        const uint32_t b = (split && acc[q] == 0) ? 1u : 0u;
+        block[q] = b;
+        // block leaders = minimum state of each initial block (min_partref.hpp:53-63 analogue)
+        lead[q] = ((uint32_t)q == fa || (uint32_t)q == fr || (!split && q == 0)) ? 1 : 0;
+        nib |= b << (q - q0);
+      }
+    }
+    uint32_t word = nib << (4 * (lane & 7));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    if ((lane & 7) == 0 && q0 < n) mirror1[q0 >> 5] = word;
   }
 }
 
-__global__ void first_states_kernel(const uint8_t* __restrict__ acc, uint64_t n, uint32_t* out2) {
+// first accepting / rejecting state among [lo, hi); a second launch over the rest
+// of the states returns at once when the first (a prefix) found both
+__global__ void first_states_kernel(const uint8_t* __restrict__ acc, uint64_t lo, uint64_t hi,
+                                    uint32_t* out2) {
+  if (lo > 0 && *reinterpret_cast<volatile uint32_t*>(&out2[0]) != kNoLeader &&
+      *reinterpret_cast<volatile uint32_t*>(&out2[1]) != kNoLeader)
+    return;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint32_t fa = kNoLeader, fr = kNoLeader;
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+  for (uint64_t q = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += stride) {
     if (acc[q]) fa = min(fa, (uint32_t)q);
     else fr = min(fr, (uint32_t)q);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
-    fr = min(fr, __shfl_xor_sync(0xffffffffu, fr, o));
-  }
+  fa = __reduce_min_sync(0xffffffffu, fa);
+  fr = __reduce_min_sync(0xffffffffu, fr);
   if ((threadIdx.x & 31) == 0) {
     if (fa != kNoLeader) atomicMin(&out2[0], fa);
     if (fr != kNoLeader) atomicMin(&out2[1], fr);
@@ -1259,12 +1287,17 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   } else {
     {
       ProfScope p(ctx, "init", n * 2);
-      first_states_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2);
+      const uint64_t pre = std::min<uint64_t>(n, 1u << 20);
+      first_states_kernel<<<grid_for(ctx, pre), 256, 0, ctx.stream>>>(d.acc, 0, pre, first2);
+      DFM_LAUNCH_CHECK();
+      if (pre < n)
+        first_states_kernel<<<grid_for(ctx, n - pre), 256, 0, ctx.stream>>>(d.acc, pre, n, first2);
       DFM_LAUNCH_CHECK();
     }
     {
       ProfScope p(ctx, "init", n * 10);
-      init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, first2, block, lead);
+      init_kernel<<<grid_for(ctx, ceil_div(n, 4)), 256, 0, ctx.stream>>>(d.acc, n, first2, block,
+                                                                       lead, mirror);
       DFM_LAUNCH_CHECK();
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 16, first2, 8, cudaMemcpyDeviceToHost, ctx.stream));
@@ -1286,7 +1319,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     else mirror_kernel<16><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
     DFM_LAUNCH_CHECK();
   };
-  build_mirror(B);
+  if (sgrid) build_mirror(B);  // (else init_kernel wrote the 1-bit mirror of pass 1)
+  else mirror_bits = 1;
   // B bounds the ids (key packing, mirror width, fresh ids start there); nb counts the
   // blocks.  They differ after a relabel-in-place pass, whose ids are direct-table
   // slots (the key, not all of which occur)
