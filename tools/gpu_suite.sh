@@ -39,7 +39,7 @@ fi
 if [[ " $WHAT " == *" ncu "* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches_default.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"insert_kernel|insert_small|resolve_kernel|apply_kernel|filt_|lay_" -c 40 \
+  timeout 900 ncu --set full --clock-control none --import-source on -c 60 \
       -o $OUT/prof_default python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"square_kernel" -c 2 \
       -o $OUT/prof_trans python bench.py --algo trans --family fib --n 12 --k 1 --steps 1 --warmup 0 --no-e2e > $OUT/ncu_trans.log 2>&1
