@@ -46,7 +46,7 @@ for r in rows[2:]:
     short = re.sub(r"\(.*", "", name.replace("(anonymous namespace)::", "").replace("dfm::", ""))
     detail.setdefault(f, []).append(f"{short[:60]} {b / 1e9:.2f} GB")
 old = json.load(open(out)) if out else {}
-res = {"_doc": old.get("_doc", ""), **{k: round(v, -7) for k, v in fam.items()}}
+res = {"_doc": old.get("_doc", "") if out else "", **{k: round(v, -7) for k, v in fam.items()}}
 if "gemm" in old:
     res["gemm"] = old["gemm"]
 res["_detail"] = {k: "; ".join(v) for k, v in detail.items()}
