@@ -391,11 +391,30 @@ struct SigParams {
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
 // narrow tiles (<= 64 KB) fit two CTAs per SM: cap registers at 32 for that
-template <int kIdBits, int kK, bool kHashed>
-__global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(SigParams p) {
+// kTile24: 32-bit ids below 2^24 kept as 3 bytes per tile entry (96 KB instead of
+// 128 KB: two CTAs per SM, so one window's loads overlap the other's key phase)
+template <int kIdBits, int kK, bool kHashed, bool kTile24 = false>
+__global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
+    lay_sig_kernel(SigParams p) {
   using V = typename IdT<kIdBits>::type;
   extern __shared__ uint4 s_tile4[];
   V* s_tile = reinterpret_cast<V*>(s_tile4);  // [k][W]
+  uint8_t* s_t8 = reinterpret_cast<uint8_t*>(s_tile4);
+  auto tput = [&](uint32_t slot, V x) {
+    if (kTile24) {
+      s_t8[3 * slot] = (uint8_t)x;
+      s_t8[3 * slot + 1] = (uint8_t)(x >> 8);
+      s_t8[3 * slot + 2] = (uint8_t)(x >> 16);
+    } else {
+      s_tile[slot] = x;
+    }
+  };
+  auto tget = [&](uint32_t slot) -> uint32_t {
+    if (kTile24)
+      return (uint32_t)s_t8[3 * slot] | (uint32_t)s_t8[3 * slot + 1] << 8 |
+             (uint32_t)s_t8[3 * slot + 2] << 16;
+    return (uint32_t)s_tile[slot];
+  };
   const Layout& L = p.L;
   const uint32_t k = kK > 0 ? (uint32_t)kK : L.k;
   const V* __restrict__ vin = static_cast<const V*>(L.v);
@@ -408,7 +427,7 @@ __global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(Si
     // lane-consecutive transitions (coalesced slot / position loads; the ids come
     // in runs of ~16 per sub-run), U in flight per thread (fewer under the 32-register
     // cap of the two-CTA narrow tiles)
-    constexpr int U = kIdBits <= 16 ? 4 : 8;
+    constexpr int U = (kIdBits <= 16 || kTile24) ? 4 : 8;
     for (uint32_t f0 = threadIdx.x; f0 < ew; f0 += U * blockDim.x) {
       uint32_t sl[U], ee[U];
 #pragma unroll
@@ -428,7 +447,7 @@ __global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(Si
       for (int u = 0; u < U; ++u) x[u] = (f0 + u * blockDim.x < ew) ? vin[ee[u]] : (V)0;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (f0 + u * blockDim.x < ew) s_tile[sl[u]] = x[u];
+        if (f0 + u * blockDim.x < ew) tput(sl[u], x[u]);
     }
     __syncthreads();
     const uint64_t i0 = p.wstart ? p.wstart[w] : q0;
@@ -441,7 +460,7 @@ __global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(Si
         unsigned long long key = b;
 #pragma unroll
         for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
-          key = (key << p.w) | (uint32_t)s_tile[a * L.W + x];
+          key = (key << p.w) | tget(a * L.W + x);
         p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
         if (p.present) {  // test before set: most keys of a dense pass are repeats
           const uint32_t bit = 1u << (key & 31);
@@ -454,7 +473,7 @@ __global__ void __launch_bounds__(1024, kIdBits <= 16 ? 2 : 1) lay_sig_kernel(Si
         unsigned long long h = mix64(p.seed * kGolden + b);
 #pragma unroll
         for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a) {
-          const uint32_t s = s_tile[a * L.W + x];
+          const uint32_t s = tget(a * L.W + x);
           row[a + 1] = s;
           h = mix64(h + kGolden + s);
         }

@@ -900,6 +900,11 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   DFM_LAUNCH_CHECK();
 }
 
+bool tile24_enabled() {  // DFM_SORTPR_TILE24=0: 4-byte tiles for all 32-bit passes (tests)
+  const char* e = getenv("DFM_SORTPR_TILE24");
+  return e == nullptr || e[0] != '0';
+}
+
 bool rip_enabled() {  // DFM_SORTPR_RIP=0: resolve/apply on every pass (tests)
   const char* e = getenv("DFM_SORTPR_RIP");
   return e == nullptr || e[0] != '0';
@@ -1123,26 +1128,31 @@ void launch_layout_gather(Ctx& ctx, const Layout& L, const uint32_t* ids) {
 }
 
 template <int kIdBits, int kK>
-void launch_layout_sig(Ctx& ctx, const SigParams& sp, bool hashed) {
+void launch_layout_sig(Ctx& ctx, const SigParams& sp, bool hashed, bool tile24) {
   using V = typename IdT<kIdBits>::type;
-  const size_t smem = (size_t)sp.L.E * sizeof(V);
+  const size_t smem = (size_t)sp.L.E * (tile24 ? 3 : sizeof(V));
   auto go = [&](auto kern) {
     DFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<sp.L.nW, 1024, smem, ctx.stream>>>(sp);
     DFM_LAUNCH_CHECK();
   };
-  if (hashed) go(lay_sig_kernel<kIdBits, kK, true>);
-  else go(lay_sig_kernel<kIdBits, kK, false>);
+  if (kIdBits == 32 && tile24) {
+    if (hashed) go(lay_sig_kernel<kIdBits, kK, true, true>);
+    else go(lay_sig_kernel<kIdBits, kK, false, true>);
+  } else {
+    if (hashed) go(lay_sig_kernel<kIdBits, kK, true>);
+    else go(lay_sig_kernel<kIdBits, kK, false>);
+  }
 }
 
 template <int kIdBits>
 void layout_keys_bits(Ctx& ctx, const Layout& L, const uint32_t* ids, const SigParams& sp,
-                      bool hashed) {
+                      bool hashed, bool tile24) {
   launch_layout_gather<kIdBits>(ctx, L, ids);
   switch (L.k) {
-    case 2: return launch_layout_sig<kIdBits, 2>(ctx, sp, hashed);
-    case 4: return launch_layout_sig<kIdBits, 4>(ctx, sp, hashed);
-    default: return launch_layout_sig<kIdBits, 0>(ctx, sp, hashed);
+    case 2: return launch_layout_sig<kIdBits, 2>(ctx, sp, hashed, tile24);
+    case 4: return launch_layout_sig<kIdBits, 4>(ctx, sp, hashed, tile24);
+    default: return launch_layout_sig<kIdBits, 0>(ctx, sp, hashed, tile24);
   }
 }
 
@@ -1164,12 +1174,13 @@ void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const ui
   ProfScope ps(ctx, "sig", L.T * (8 + 2 * idb) + L.n * (uint64_t)mirror_bits / 8 +
                                m * (4ull + 4 + 8 + (vals ? 5 : 0) + (hashed ? 4ull * row : 0)));
   const uint32_t* ids32 = static_cast<const uint32_t*>(ids);
+  const bool t24 = w <= 24 && tile24_enabled();  // 32-bit ids below 2^24: 3-byte tiles
   switch (mirror_bits) {
-    case 1: return layout_keys_bits<1>(ctx, L, ids32, sp, hashed);
-    case 4: return layout_keys_bits<4>(ctx, L, ids32, sp, hashed);
-    case 8: return layout_keys_bits<8>(ctx, L, ids32, sp, hashed);
-    case 16: return layout_keys_bits<16>(ctx, L, ids32, sp, hashed);
-    default: return layout_keys_bits<32>(ctx, L, ids32, sp, hashed);
+    case 1: return layout_keys_bits<1>(ctx, L, ids32, sp, hashed, t24);
+    case 4: return layout_keys_bits<4>(ctx, L, ids32, sp, hashed, t24);
+    case 8: return layout_keys_bits<8>(ctx, L, ids32, sp, hashed, t24);
+    case 16: return layout_keys_bits<16>(ctx, L, ids32, sp, hashed, t24);
+    default: return layout_keys_bits<32>(ctx, L, ids32, sp, hashed, t24);
   }
 }
 // partitioned grouping of one pass (sortpr_group.cuh); keys/vals from layout_keys

@@ -317,8 +317,11 @@ def test_chunked_layout(eng, monkeypatch, n, k, seed, wc):
     nb, it, lab = _device_labels(eng, dd, n)
     monkeypatch.setenv("DFM_LAYOUT_CHUNK_WINDOWS", str(wc))
     nb1, it1, lab1 = _device_labels(eng, dd, n)
-    assert (nb, it) == (nb1, it1)
-    assert bool((lab == lab1).all())
+    monkeypatch.delenv("DFM_LAYOUT_CHUNK_WINDOWS")
+    monkeypatch.setenv("DFM_SORTPR_TILE24", "0")  # 4-byte window tiles throughout
+    nb2, it2, lab2 = _device_labels(eng, dd, n)
+    assert (nb, it) == (nb1, it1) == (nb2, it2)
+    assert bool((lab == lab1).all()) and bool((lab == lab2).all())
     dd.free()
 
 
