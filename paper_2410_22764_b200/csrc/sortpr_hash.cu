@@ -290,9 +290,11 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       }
       if (kDirect && p.present) {  // many distinct keys: consecutive states rarely share one
         if (valid[u]) {
-          if (p.ids_out) p.ids_out[p.act ? p.act[i] : (uint32_t)i] = (uint32_t)s[u] + p.id_off;
           atomicMax(&p.slots[s[u]].rep, ~(uint32_t)i);
-          atomicAdd(&p.slots[s[u]].info, 1u | (lead[u] ? 0x80000000u : 0u));
+          if (p.ids_out)  // relabel in place: the rank is the id; no group size or leader bit
+            p.ids_out[p.act ? p.act[i] : (uint32_t)i] = (uint32_t)s[u] + p.id_off;
+          else
+            atomicAdd(&p.slots[s[u]].info, 1u | (lead[u] ? 0x80000000u : 0u));
         }
         continue;
       }
@@ -619,7 +621,9 @@ __global__ void __launch_bounds__(256) apply_kernel(uint64_t m, const uint32_t* 
 // relabel-in-place passes (direct tables: the key, or its rank among the keys
 // present, is the new id — any numbering gives the same partition): one thread per
 // group marks its minimum member as the block leader (old leaders are the minimum
-// of their group too) and counts groups; *single: a one-member group exists
+// of their group too) and counts groups; *single: a one-member group exists (only
+// known where the slots keep group sizes; the rank-compacted passes do not, and
+// their one-member groups simply stay on the active list)
 __global__ void __launch_bounds__(256) rip_groups_kernel(const Slot* __restrict__ slots,
                                                          uint64_t ntab,
                                                          const uint32_t* __restrict__ act,
@@ -631,11 +635,11 @@ __global__ void __launch_bounds__(256) rip_groups_kernel(const Slot* __restrict_
   bool one = false;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntab; t += stride) {
     const uint2 sl = *reinterpret_cast<const uint2*>(&slots[t].rep);
-    if ((sl.y & 0x7FFFFFFFu) == 0) continue;
+    if (sl.x == 0) continue;  // no member (rep holds ~min member)
     const uint32_t i = ~sl.x;
     lead[act ? act[i] : i] = 1;
     ++mine;
-    one |= (sl.y & 0x7FFFFFFFu) == 1u;
+    one |= (sl.y & 0x7FFFFFFFu) == 1u;  // (rank-compacted passes keep no sizes: never)
   }
   mine = __reduce_add_sync(0xffffffffu, mine);
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(groups, (unsigned long long)mine);
