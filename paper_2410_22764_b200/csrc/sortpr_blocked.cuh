@@ -43,7 +43,8 @@ struct Layout {
   uint16_t* tgt = nullptr;
   uint16_t* lsf = nullptr;
   uint32_t* eidx = nullptr;    // [T] bucket position of each window-flattened transition
-  uint32_t* off = nullptr;
+  uint32_t* off = nullptr;     // [nW][R] (+1): bucket start of sub-run (window w, range j)
+  uint32_t* gb = nullptr;      // [nC][R]: bucket start of range j inside chunk c
   uint16_t* pre = nullptr;
   uint32_t* wstart = nullptr;  // [nW + 1] first active index of each window
   void* v = nullptr;           // [T] ids in window-flattened order (id bytes)
@@ -149,24 +150,28 @@ struct LayOffIn {
   const uint32_t* cnt;
   __device__ uint32_t operator()(uint64_t i) const { return cnt[i]; }
 };
-// one chunk's cells in (range j, window w0 + x) order, x < wc -> off(j, w), absolute
+// one chunk's cells in (range j, window w0 + x) order, x < wc -> off(w, j), absolute
+// (window-major, so the per-window kernels read a window's R starts coalesced), and
+// the chunk's range starts for the gather kernel
 struct LayOffOut {
   uint32_t* off;
-  uint32_t nW, wc, w0;
+  uint32_t* gb;
+  uint32_t R, wc, w0, ch;
   uint32_t base;     // transitions of the chunks before
   uint64_t count;    // cells of this chunk (R * wc)
-  bool last;         // final chunk: off[R * nW] = T
+  uint64_t total;    // final chunk: off[nW * R] = T (else ~0)
   __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
     const uint64_t j = i / wc, x = i - j * wc;
-    off[j * nW + w0 + x] = base + excl;
-    if (last && i + 1 == count) off[(count / wc) * nW] = base + excl + v;
+    off[(w0 + x) * (uint64_t)R + j] = base + excl;
+    if (x == 0) gb[(uint64_t)ch * R + j] = base + excl;
+    if (total != ~0ull && i + 1 == count) off[total] = base + excl + v;
   }
 };
 
 // ---- layout build: bucket every transition (tgt) and its tile slot (lsf).
 // Both are staged in shared memory in the window's flattened order (sub-run j
-// at pre(w, j)); lsf leaves as one coalesced chunk, and one warp per sub-run
-// writes its tgt run at the bucket position off(j, w) and the positions (eidx).
+// at pre(w, j)); lsf and the bucket positions (eidx) leave as coalesced chunks and
+// every tgt goes to its bucket position off(w, j) + rank.
 __device__ __forceinline__ void lay_stage(uint32_t t, uint32_t a, uint32_t x, uint32_t W,
                                           uint32_t* s_cur, const uint32_t* s_pre,
                                           uint16_t* s_tgt, uint16_t* s_lsf, uint16_t* s_j) {
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
     for (uint32_t u = 0; u < kPf; ++u) {
       const uint32_t j = threadIdx.x + u * blockDim.x;
       if (w < w_end && j < L.R) {
-        pf_off[u] = L.off[(uint64_t)j * L.nW + w];
+        pf_off[u] = L.off[(uint64_t)w * L.R + j];
         pf_pre[u] = L.pre[(uint64_t)w * L.R + j];
       }
     }
@@ -271,8 +276,8 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
     for (uint32_t f = threadIdx.x; f < ew; f += blockDim.x) {
       const uint32_t e = s_off[s_j[f]] + f;
       L.lsf[fb + f] = s_lsf[f];
-      L.tgt[e] = s_tgt[f];
       L.eidx[fb + f] = e;
+      L.tgt[e] = s_tgt[f];
     }
     __syncthreads();
   }
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32
       if (threadIdx.x <= j1 - j0) {
         const uint32_t j = j0 + threadIdx.x;
         s_bound[threadIdx.x] =
-            j < L.R ? L.off[(uint64_t)j * L.nW + (uint64_t)ch * L.Wc]
+            j < L.R ? L.gb[(uint64_t)ch * L.R + j]
                     : (ch + 1 < L.nC ? (ch + 1) * L.Wc * L.E : (uint32_t)L.T);
       }
       __syncthreads();
@@ -387,6 +392,7 @@ struct SigParams {
   uint32_t* vals;
   const uint8_t* lead;
   uint32_t* present;  // direct keys: bitmap of the keys present (rank-compacted table)
+  uint32_t tile_bytes;  // shared tile size (16-byte multiple)
 };
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys

@@ -1048,6 +1048,7 @@ void layout_init(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t wc) {
   L.lsf = ctx.slot_t<uint16_t>("ly.lsf", (uint64_t)L.nW * L.E);
   L.eidx = ctx.slot_t<uint32_t>("ly.eidx", (uint64_t)L.nW * L.E);
   L.off = ctx.slot_t<uint32_t>("ly.off", cells + 1);
+  L.gb = ctx.slot_t<uint32_t>("ly.gb", (uint64_t)L.nC * L.R);
   L.pre = ctx.slot_t<uint16_t>("ly.pre", cells);
   L.wstart = ctx.slot_t<uint32_t>("ly.wstart", L.nW + 1);
   L.v = ctx.slot("ly.v", L.T * 4);
@@ -1062,7 +1063,7 @@ void layout_chunk(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t ch) {
   uint32_t* cnt_w = ctx.slot_t<uint32_t>("ly.cntw", (uint64_t)L.R * L.nW);
   uint32_t* cnt_j = ctx.slot_t<uint32_t>("ly.cntj", (uint64_t)L.R * L.nW);
   const uint64_t ct = std::min<uint64_t>((uint64_t)w1 * L.W, L.n) * L.k - (uint64_t)w0 * L.E;
-  // delta read twice + tgt/lsf writes + the count/offset matrices
+  // delta read twice + tgt/lsf/eidx writes + the count/offset matrices
   ProfScope ps(ctx, "layout", ct * (4ull + 4 + 2 + 2 + 4) + cells * (4ull * 4 + 2 * 2));
   const unsigned grid = (unsigned)std::min<uint64_t>(wc, (uint64_t)ctx.num_sms * 4);
   lay_count_kernel<<<grid, 512, L.R * 4, ctx.stream>>>(d.delta, L, cnt_w, w0, w1);
@@ -1072,7 +1073,9 @@ void layout_chunk(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t ch) {
                                                        cnt_j + (uint64_t)w0 * L.R, wc, L.R);
   DFM_LAUNCH_CHECK();
   prims::lookback_scan(ctx, "sc.lyoff", cells, LayOffIn{cnt_j + (uint64_t)w0 * L.R},
-                       LayOffOut{L.off, L.nW, wc, w0, w0 * L.E, cells, ch + 1 == L.nC}, nullptr);
+                       LayOffOut{L.off, L.gb, L.R, wc, w0, ch, w0 * L.E, cells,
+                                 ch + 1 == L.nC ? (uint64_t)L.nW * L.R : ~0ull},
+                       nullptr);
   const size_t smem = (size_t)L.R * 12 + 4 + (size_t)L.E * 6;
   DFM_CUDA(cudaFuncSetAttribute(lay_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
@@ -1132,9 +1135,11 @@ void launch_layout_gather(Ctx& ctx, const Layout& L, const uint32_t* ids) {
 }
 
 template <int kIdBits, int kK>
-void launch_layout_sig(Ctx& ctx, const SigParams& sp, bool hashed, bool tile24) {
+void launch_layout_sig(Ctx& ctx, const SigParams& sp0, bool hashed, bool tile24) {
   using V = typename IdT<kIdBits>::type;
-  const size_t smem = (size_t)sp.L.E * (tile24 ? 3 : sizeof(V));
+  SigParams sp = sp0;
+  sp.tile_bytes = (uint32_t)(((size_t)sp.L.E * (tile24 ? 3 : sizeof(V)) + 15) & ~size_t(15));
+  const size_t smem = sp.tile_bytes;
   auto go = [&](auto kern) {
     DFM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<sp.L.nW, 1024, smem, ctx.stream>>>(sp);
