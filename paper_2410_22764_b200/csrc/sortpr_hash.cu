@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
           }
           s[u] = t;
         }
-        p.slot_of[i] = (uint32_t)s[u];
+        // (relabel-in-place rank passes read no slot index back)
+        if (!(kDirect && p.present && p.ids_out)) p.slot_of[i] = (uint32_t)s[u];
       }
       if (kDirect && p.present) {  // many distinct keys: consecutive states rarely share one
         if (valid[u]) {

@@ -52,3 +52,15 @@ def test_pipelined_upload_rejects_bad_target(eng):
     delta[3, n - 1] = 0
     r = eng.sort_pr(dfm.Dfa(n, k, delta, acc, 0))
     assert r.stats.status == dfm.RunStatus.ok
+
+
+def test_pipelined_upload_timeout_then_reuse(eng):
+    """A deadline that expires while the rows are still landing: timeout status,
+    empty partition, and the engine (its copy stream drained) stays usable."""
+    n, k = 40_000_000, 4
+    delta, acc = O.random_dfa(n, k, 6, 0.5)
+    d = dfm.Dfa(n, k, delta, acc, 0)
+    r = eng.sort_pr(d, 1)
+    assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
+    r = eng.sort_pr(d)
+    assert r.stats.status == dfm.RunStatus.ok and r.partition.num_blocks > 0
