@@ -905,6 +905,11 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   DFM_LAUNCH_CHECK();
 }
 
+bool layout_overlap_enabled() {  // DFM_SORTPR_LAYOUT_OVERLAP=0: build it at pass 2 (tests)
+  const char* e = getenv("DFM_SORTPR_LAYOUT_OVERLAP");
+  return e == nullptr || e[0] != '0';
+}
+
 bool tile24_enabled() {  // DFM_SORTPR_TILE24=0: 4-byte tiles for all 32-bit passes (tests)
   const char* e = getenv("DFM_SORTPR_TILE24");
   return e == nullptr || e[0] != '0';
@@ -1352,6 +1357,35 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   bool force_global = false;
   const bool part_on = partition_enabled();
   const bool lay_ok = layout_possible(n, k);
+  // Device-resident input whose later passes will want the blocked layout: build it
+  // on the side stream while pass 1 (gather-rate bound) runs on the main one.
+  bool lay_pending = false;
+  cudaEvent_t lay_ready = nullptr;
+  struct JoinSide {  // every exit joins the side stream into the main one
+    Ctx& ctx;
+    bool& pending;
+    cudaEvent_t& ev;
+    ~JoinSide() {
+      if (pending) cudaStreamWaitEvent(ctx.stream, ev, 0);
+    }
+  } join_side{ctx, lay_pending, lay_ready};
+  if (lay_ok && d.nready == 0 && n > kBlockedMinMirror && layout_overlap_enabled()) {
+    cudaStream_t main = ctx.stream, side = ctx.copy();
+    lay_ready = ctx.chunk_event_pool(1)[0];
+    DFM_CUDA(cudaEventRecord(lay_ready, main));
+    DFM_CUDA(cudaStreamWaitEvent(side, lay_ready, 0));
+    ctx.stream = side;  // the build's kernels, scans and scratch follow ctx.stream
+    try {
+      build_layout(ctx, d, lay);
+    } catch (...) {
+      ctx.stream = main;
+      throw;
+    }
+    ctx.stream = main;
+    DFM_CUDA(cudaEventRecord(lay_ready, side));
+    lay_built = true;
+    lay_pending = true;
+  }
   const uint32_t* act = nullptr;  // identity at pass 1
   int act_sel = 0;
   uint64_t m = n;
@@ -1411,6 +1445,10 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
                         m >= kPartMinStates && m < (1ull << 31);
       force_global = false;
       if (blocked) {
+        if (lay_pending) {  // built on the side stream during pass 1
+          DFM_CUDA(cudaStreamWaitEvent(ctx.stream, lay_ready, 0));
+          lay_pending = false;
+        }
         if (!lay_built) {
           build_layout(ctx, d, lay);
           lay_built = true;

@@ -455,3 +455,15 @@ def test_forced_hash_collisions_retry_exactly(eng, monkeypatch, n, k, seed):
     assert (nb, it) == (nb1, it1)
     assert bool((lab == lab1).all())
     dd.free()
+
+
+def test_layout_built_beside_pass_one(eng, monkeypatch):
+    """The blocked layout built on the side stream during pass 1 (device-resident
+    input) gives the result of building it at pass 2."""
+    n, k = 40_000_000, 4
+    dd = eng.random_dfa_device(n, k, 12, 0.5)
+    nb, it, lab = _device_labels(eng, dd, n)
+    monkeypatch.setenv("DFM_SORTPR_LAYOUT_OVERLAP", "0")
+    nb0, it0, lab0 = _device_labels(eng, dd, n)
+    assert (nb, it) == (nb0, it0) and bool((lab == lab0).all())
+    dd.free()

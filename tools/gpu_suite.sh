@@ -14,6 +14,7 @@ fi
 if [[ " $WHAT " == *" bench "* ]]; then
   python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; tail -c 600 $OUT/bench_default.json
   python bench.py --sortpr-engine radix --no-e2e --no-cpu-baseline > $OUT/bench_radix.json 2>&1
+  python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2>&1
   python bench.py --algo naive --n 100000 --k 2 --steps 5 --warmup 2 --no-e2e > $OUT/bench_c1_naive.json 2>&1
   python bench.py --algo sort --n 100000 --k 2 --steps 10 --warmup 3 --no-e2e > $OUT/bench_c1_sort.json 2>&1
   python bench.py --algo sort --family vlts --n 10000000 --k 100 --steps 5 --warmup 2 --no-e2e > $OUT/bench_c2_sort.json 2>&1
