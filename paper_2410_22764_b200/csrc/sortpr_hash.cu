@@ -206,12 +206,57 @@ __device__ __forceinline__ unsigned long long make_key(const InsertParams& p, ui
   return weak(h, p.seed);
 }
 
+// Hashed keys for a runtime (large) alphabet, one call per warp for 32 consecutive
+// active positions i0 + lane: each lane hashes its own signature, and the rows are
+// written 8 words at a time through a per-warp shared buffer so that every store
+// fills whole 32-byte sectors (row stride a multiple of 8 words) instead of 32
+// lanes touching 32 rows per store.
+template <int kIdBits>
+__device__ __forceinline__ unsigned long long make_key_rows_warp(
+    const InsertParams& p, uint64_t i0, bool valid, uint32_t q, uint32_t b, uint64_t pol_stream,
+    uint64_t pol_ids, uint32_t* s_buf /* [32][9] */) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t k = p.k, words = k + 1;
+  const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+  unsigned long long h = mix64(p.seed * kGolden + b);
+  for (uint32_t w0 = 0; w0 < words; w0 += 8) {
+    uint32_t t[8], v[8];
+#pragma unroll
+    for (uint32_t c = 0; c < 8; ++c) {
+      const uint32_t wd = w0 + c;
+      t[c] = (valid && wd >= 1 && wd < words)
+                 ? ld_stream(p.delta + (uint64_t)(wd - 1) * p.n + q, pol_stream)
+                 : 0u;
+    }
+#pragma unroll
+    for (uint32_t c = 0; c < 8; ++c) {
+      const uint32_t wd = w0 + c;
+      v[c] = wd == 0 ? b : (valid && wd < words) ? load_id<kIdBits>(p.ids, t[c], pol_ids) : 0u;
+      if (wd >= 1 && wd < words) h = mix64(h + kGolden + v[c]);
+      s_buf[lane * 9 + c] = v[c];
+    }
+    __syncwarp();
+    // lane L writes word L % 8 of row (4 r + L / 8): one full sector per 8 lanes
+#pragma unroll
+    for (uint32_t r = 0; r < 8; ++r) {
+      const uint32_t row_lane = 4 * r + (lane >> 3), c = lane & 7;
+      if (((vmask >> row_lane) & 1u) && w0 + c < words)
+        p.sig[(i0 + row_lane) * (uint64_t)p.row + w0 + c] = s_buf[row_lane * 9 + c];
+    }
+    __syncwarp();
+  }
+  return weak(h, p.seed);
+}
+
 // K1, hash or large direct table; warp-level aggregation of equal slots
 constexpr uint32_t kUnique = 0xFFFFFFFFu;  // slot_of mark: key seen once (filtered)
 
 template <int kIdBits, bool kHashed, bool kDirect, int kK, bool kFromKeys = false,
           bool kFilter = false>
 __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
+  // large runtime alphabets with hashed keys: warp-cooperative coalesced row writes
+  constexpr bool kRowsWarp = kHashed && kK == 0 && !kFromKeys && !kFilter;
+  __shared__ uint32_t s_rows[kRowsWarp ? 8 * 32 * 9 : 1];
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_ids = policy_evict_last();
   // each warp takes 64 consecutive active states per step (two per lane) so two
@@ -235,7 +280,13 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
       valid[u] = j < p.m;
       idx[u] = kFilter ? (valid[u] ? p.cand[j] : 0) : j;
       const uint64_t i = idx[u];
-      if (valid[u]) {
+      if (kRowsWarp) {  // whole warp: coalesced signature rows (see make_key_rows_warp)
+        const uint32_t q = valid[u] ? (p.act ? p.act[i] : (uint32_t)i) : 0u;
+        const uint32_t b = valid[u] ? p.block[q] : 0u;
+        if (valid[u]) lead[u] = p.lead[q];
+        key[u] = make_key_rows_warp<kIdBits>(p, base + u * 32, valid[u], q, b, pol_stream,
+                                             pol_ids, s_rows + (threadIdx.x >> 5) * (32 * 9));
+      } else if (valid[u]) {
         const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
         lead[u] = p.lead[q];
         key[u] = kFromKeys ? p.keys[i]
@@ -466,6 +517,41 @@ struct CandOut {
   }
 };
 
+// two signature rows differ?  Rows of large alphabets are padded to 8-word strides:
+// 16-byte loads, 16 words of each row in flight per step (words past `words` are
+// padding and masked)
+__device__ __forceinline__ bool rows_differ(const uint32_t* __restrict__ sig, uint32_t row,
+                                            uint32_t words, uint64_t i, uint64_t j) {
+  const uint32_t* a = sig + i * (uint64_t)row;
+  const uint32_t* b = sig + j * (uint64_t)row;
+  if ((row & 7) == 0) {
+    const uint4* a4 = reinterpret_cast<const uint4*>(a);
+    const uint4* b4 = reinterpret_cast<const uint4*>(b);
+    for (uint32_t x = 0; x < words; x += 16) {
+      uint32_t diff = 0;
+#pragma unroll
+      for (uint32_t y = 0; y < 4; ++y) {
+        const uint32_t w = x + 4 * y;
+        if (w < words) {
+          const uint4 u = a4[w / 4], v = b4[w / 4];
+          diff |= (u.x ^ v.x) | (w + 1 < words ? u.y ^ v.y : 0u) |
+                  (w + 2 < words ? u.z ^ v.z : 0u) | (w + 3 < words ? u.w ^ v.w : 0u);
+        }
+      }
+      if (diff) return true;
+    }
+    return false;
+  }
+  uint32_t diff = 0;
+  for (uint32_t x = 0; x < words; x += 4) {  // 4 independent words in flight
+#pragma unroll
+    for (uint32_t y = 0; y < 4; ++y)
+      if (x + y < words) diff |= a[x + y] ^ b[x + y];
+    if (diff) return true;
+  }
+  return false;
+}
+
 struct ResolveItem {
   uint32_t v;      // 1 = minimum member of a group that gets a fresh id
   uint32_t slot;
@@ -496,16 +582,7 @@ struct ResolveIn {
     const bool keeper = (sl.y >> 31) != 0;
     const bool is_rep = rep_i == (uint32_t)i;
     if (!is_rep && sig != nullptr) {  // equal hash: verify the full signature
-      const uint32_t* a = sig + i * (uint64_t)row;
-      const uint32_t* b = sig + (uint64_t)rep_i * row;
-      uint32_t diff = 0;
-      for (uint32_t x = 0; x < words; x += 4) {  // 4 independent words in flight
-#pragma unroll
-        for (uint32_t y = 0; y < 4; ++y)
-          if (x + y < words) diff |= a[x + y] ^ b[x + y];
-        if (diff) break;
-      }
-      if (diff) atomicOr(collision, 1ull);
+      if (rows_differ(sig, row, words, i, rep_i)) atomicOr(collision, 1ull);
     }
     ResolveItem it;
     it.v = (is_rep && !keeper) ? 1u : 0u;
@@ -672,13 +749,8 @@ __global__ void __launch_bounds__(256) rip_hashed_kernel(uint64_t m,
     }
     const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
     const uint32_t rep_i = ~sl.x;
-    if (rep_i != (uint32_t)i && sig != nullptr) {
-      const uint32_t* a = sig + i * (uint64_t)row;
-      const uint32_t* b = sig + (uint64_t)rep_i * row;
-      uint32_t diff = 0;
-      for (uint32_t x = 0; x < words; ++x) diff |= a[x] ^ b[x];
-      if (diff) atomicOr(collision, 1ull);
-    }
+    if (rep_i != (uint32_t)i && sig != nullptr && rows_differ(sig, row, words, i, rep_i))
+      atomicOr(collision, 1ull);
     ids[i] = B + (uint32_t)m + s;
     flag[i] = (sl.y & 0x7FFFFFFFu) >= 2 ? 1 : 0;
   }
@@ -1287,7 +1359,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   uint8_t* st = ctx.slot_t<uint8_t>("sh.st", n);
   uint32_t* sig = nullptr;
   // signature rows packed back to back: a warp's consecutive rows cover whole sectors
-  const uint32_t row = k + 1;
+  // (rows of large alphabets padded to whole 32-byte sectors: coalesced row writes)
+  const uint32_t row = k + 1 > 8 ? ((k + 1 + 7) & ~7u) : k + 1;
   uint64_t* sc = ctx.d_scalars;  // [1] fresh [2] collision [3] next active [4] accepting
   uint32_t* first2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
   DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
