@@ -64,3 +64,15 @@ def test_pipelined_upload_timeout_then_reuse(eng):
     assert r.stats.status == dfm.RunStatus.timeout and r.partition.block.size == 0
     r = eng.sort_pr(d)
     assert r.stats.status == dfm.RunStatus.ok and r.partition.num_blocks > 0
+
+
+@pytest.mark.parametrize("p", [0.0, 1.0])
+def test_pipelined_upload_single_initial_block(eng, p):
+    """All states accepting (or none): one block after one pass, through the
+    pipelined path as well."""
+    n, k = 17_000_000, 4
+    delta, acc = O.random_dfa(n, k, 7, p)
+    r = eng.sort_pr(dfm.Dfa(n, k, delta, acc, 0))
+    assert r.stats.status == dfm.RunStatus.ok
+    assert (r.partition.num_blocks, r.stats.iterations) == (1, 1)
+    assert not r.partition.block.any()
