@@ -224,19 +224,6 @@ struct PersistentArgs {
   uint32_t max_passes;
   int start_sel;
   uint32_t* out;      // [0] passes executed, [1] stable, [2] buffer holding the labels
-  // dirty-set pruning (nullptr: off).  A state that did not split keeps its label
-  // and leader; if neither its successors' labels nor its leader's successors'
-  // labels changed in the previous pass, its comparisons give the same result and
-  // it cannot split now.  So pass p only evaluates q with dq[q] (q split, or one of
-  // its successors changed label, in pass p-1) or dl[cur[q]] (its leader's
-  // successors changed); the flags are double-buffered by pass parity and marked
-  // through the predecessor lists (CSR) of the changed states.
-  const uint32_t* pred_off;
-  const uint32_t* pred;
-  uint8_t* dq0;
-  uint8_t* dq1;
-  uint8_t* dl0;
-  uint8_t* dl1;
 };
 
 template <int kPolicy, bool kCas>
@@ -278,10 +265,7 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
         if (qi >= a.n) continue;
         const uint32_t q = (uint32_t)qi;
         const uint32_t leader = cur[q];
-        bool sp = false;
-        if (a.pred_off == nullptr || ((pass & 1) ? a.dq1 : a.dq0)[q] ||
-            ((pass & 1) ? a.dl1 : a.dl0)[leader])
-          sp = splits(a.rows, a.n, a.letters, cur, q, leader);
+        const bool sp = splits(a.rows, a.n, a.letters, cur, q, leader);
         a.split[q] = sp;
         elect_cell<kPolicy>(a.cells, leader, q, pass, sp, vmask);
       }
@@ -290,30 +274,13 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
         break;
       }
       g.sync();
-      uint8_t* dq_now = (pass & 1) ? a.dq1 : a.dq0;
-      uint8_t* dl_now = (pass & 1) ? a.dl1 : a.dl0;
-      uint8_t* dq_nxt = (pass & 1) ? a.dq0 : a.dq1;
-      uint8_t* dl_nxt = (pass & 1) ? a.dl0 : a.dl1;
       for (uint64_t qi = first; qi < a.n; qi += nth) {
         const uint32_t c = cur[qi];
         if (a.split[qi]) {
           nxt[qi] = (uint32_t)a.cells[c];
           any = true;
-          if (a.pred_off) {  // q and the predecessors of q are dirty next pass
-            dq_nxt[qi] = 1;
-            const uint32_t e1 = a.pred_off[qi + 1];
-            for (uint32_t e = a.pred_off[qi]; e < e1; ++e) {
-              const uint32_t x = a.pred[e];
-              dq_nxt[x] = 1;
-              dl_nxt[x] = 1;
-            }
-          }
         } else {
           nxt[qi] = c;
-        }
-        if (a.pred_off) {  // this pass's flags are spent (re-marked two passes on)
-          dq_now[qi] = 0;
-          dl_now[qi] = 0;
         }
       }
     }
@@ -625,35 +592,6 @@ __global__ void __launch_bounds__(1024, 1) cluster_pr_kernel(ClusterArgs a) {
   cl.sync();  // no CTA leaves while others may still read its shared memory
 }
 
-// predecessor lists (CSR over all letters' rows) for the dirty-set pruning
-__global__ void pred_count_kernel(const uint32_t* __restrict__ rows, uint64_t total,
-                                  uint32_t* __restrict__ cnt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride)
-    atomicAdd(&cnt[rows[e]], 1u);
-}
-struct PredIn {
-  const uint32_t* cnt;
-  __device__ uint32_t operator()(uint64_t i) const { return cnt[i]; }
-};
-struct PredOut {
-  uint32_t* off;
-  uint64_t n;
-  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t v) const {
-    off[i] = excl;
-    if (i + 1 == n) off[n] = excl + v;
-  }
-};
-__global__ void pred_fill_kernel(const uint32_t* __restrict__ rows, uint64_t n, uint64_t total,
-                                 const uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
-                                 uint32_t* __restrict__ pred) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const uint32_t t = rows[e];
-    pred[off[t] + atomicAdd(&fill[t], 1u)] = (uint32_t)(e % n);
-  }
-}
-
 unsigned grid_for(const Ctx& ctx, uint64_t items) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
                                       (uint64_t)ctx.num_sms * 16);
@@ -670,11 +608,6 @@ uint64_t fused_max_states(const Ctx& ctx) {
     DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, fused_pr_kernel<DFM_POLICY_MIN>, kPersistThreads, 0));
   return (uint64_t)per_sm * ctx.num_sms * kPersistThreads;
-}
-
-bool dirty_enabled() {  // DFM_NAIVE_DIRTY=0: evaluate every state every pass (tests)
-  const char* e = getenv("DFM_NAIVE_DIRTY");
-  return e == nullptr || e[0] != '0';
 }
 
 bool fused_enabled() {
@@ -828,37 +761,6 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     return out;
   }
   if (!tracing_ && n <= kPersistentMaxStates) {
-    // dirty-set pruning for the two-phase kernel (PersistentArgs): predecessor lists
-    // once, then every pass evaluates only the states a change can reach
-    const uint32_t* pred_off = nullptr;
-    const uint32_t* pred = nullptr;
-    uint8_t* dq[2] = {nullptr, nullptr};
-    uint8_t* dlf[2] = {nullptr, nullptr};
-    const uint64_t edges = n * letters;
-    if (!fused_cas && edges > 0 && edges <= (1ull << 27) && dirty_enabled()) {
-      ProfScope p(ctx, "init", edges * 16 + n * 16);
-      uint32_t* cnt = ctx.slot_t<uint32_t>("pr.predcnt", n + 1);
-      uint32_t* off = ctx.slot_t<uint32_t>("pr.predoff", n + 1);
-      uint32_t* lst = ctx.slot_t<uint32_t>("pr.pred", edges);
-      DFM_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * 4, ctx.stream));
-      pred_count_kernel<<<grid_for(ctx, edges), 256, 0, ctx.stream>>>(rows, edges, cnt);
-      DFM_LAUNCH_CHECK();
-      prims::lookback_scan(ctx, "sc.pred", n, PredIn{cnt}, PredOut{off, n}, nullptr);
-      DFM_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * 4, ctx.stream));
-      pred_fill_kernel<<<grid_for(ctx, edges), 256, 0, ctx.stream>>>(rows, n, edges, off, cnt, lst);
-      DFM_LAUNCH_CHECK();
-      for (int b = 0; b < 2; ++b) {
-        dq[b] = ctx.slot_t<uint8_t>(b ? "pr.dq1" : "pr.dq0", n);
-        dlf[b] = ctx.slot_t<uint8_t>(b ? "pr.dl1" : "pr.dl0", n);
-      }
-      // the first pass (odd) evaluates everything
-      DFM_CUDA(cudaMemsetAsync(dq[1], 1, n, ctx.stream));
-      DFM_CUDA(cudaMemsetAsync(dlf[1], 1, n, ctx.stream));
-      DFM_CUDA(cudaMemsetAsync(dq[0], 0, n, ctx.stream));
-      DFM_CUDA(cudaMemsetAsync(dlf[0], 0, n, ctx.stream));
-      pred_off = off;
-      pred = lst;
-    }
     // one cooperative launch per chunk of passes; the deadline is checked between
     // chunks (the reference checks it before every pass, min_partref.hpp:78-83), so
     // chunks start small and double: a run that overruns its deadline is reported as
@@ -883,7 +785,7 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       }
       DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
       PersistentArgs pa{rows, n, letters, lab[0], lab[1], cells, split_flag, chg, pass, chunk,
-                        sel, pout, pred_off, pred, dq[0], dq[1], dlf[0], dlf[1]};
+                        sel, pout};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&pa};
       ProfScope prof(ctx, "elect", 0);

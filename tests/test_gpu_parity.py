@@ -468,21 +468,3 @@ def test_layout_built_beside_pass_one(eng, monkeypatch):
     assert (nb, it) == (nb0, it0) and bool((lab == lab0).all())
     dd.free()
 
-
-@pytest.mark.parametrize("policy", [MIN, MAX, ARB])
-def test_naive_dirty_set_pruning(eng, monkeypatch, policy):
-    """The two-phase persistent kernel evaluates only states a change can reach
-    (predecessor lists): same partition and pass count as evaluating all states."""
-    # > 150K states: the two-phase kernel (smaller inputs take the one-barrier kernel)
-    for pair in (O.vlts_dfa(1000, 200_000, 20), O.random_dfa(300_000, 3, 13, 0.5)):
-        d = to_dfa(pair)
-        r = eng.naive_pr(d, dfm.PrOptions(policy=policy))
-        monkeypatch.setenv("DFM_NAIVE_DIRTY", "0")
-        r0 = eng.naive_pr(d, dfm.PrOptions(policy=policy))
-        monkeypatch.delenv("DFM_NAIVE_DIRTY")
-        assert (r.partition.block == r0.partition.block).all()
-        if policy != ARB:
-            assert r.stats.iterations == r0.stats.iterations
-        if policy == MIN and pair[0].shape[1] == 200_000:
-            ref = O.naive_pr(*pair, "min")
-            assert r.stats.iterations == ref.iterations and (r.partition.block == ref.block).all()
