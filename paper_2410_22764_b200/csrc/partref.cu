@@ -300,15 +300,16 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
 
 // ---------------------------------------------------------------------------
 // One grid barrier per pass: the split phase of pass p-1 is not materialised
-// before pass p; pass p reads the labels L(p-2) the previous pass wrote plus
-// that pass's split flags and election cells, and forms each label it needs
-// on the fly: L(p-1)[x] = split(p-1)[x] ? winner(cell(p-1)[L(p-2)[x]]) : L(p-2)[x].
-// Each thread stores L(p-1) of its own state as it goes (for pass p+1), its
-// split flag and its election for pass p.  Split flags and election cells are
-// double-buffered by pass parity; labels by the usual two buffers.  Same per-pass
-// semantics and pass count as persistent_kernel (min_partref.hpp:78-143); the
-// dependent-load depth of a pass is unchanged (label, successor of the leader,
-// its label, each with its cell), one barrier and one grid sweep fewer.
+// before pass p; pass p reads the label words the previous pass wrote — the labels
+// L(p-2) with that pass's split flag in bit 31 — and that pass's election cells,
+// and forms each label it needs on the fly: L(p-1)[x] = flag ? winner(cell(p-1)[
+// L(p-2)[x]]) : L(p-2)[x].  Each thread stores L(p-1) of its own state with its
+// split flag of pass p (for pass p+1), and its election for pass p.  Election
+// cells are double-buffered by pass parity, labels by the usual two buffers.  Same
+// per-pass semantics and pass count as persistent_kernel (min_partref.hpp:78-143);
+// the dependent-load depth of a pass is unchanged and there is no extra gather
+// per compared letter (the flag rides in the label word), one barrier and one grid
+// sweep fewer.
 struct FusedArgs {
   const uint32_t* rows;
   uint64_t n, letters;
@@ -316,8 +317,6 @@ struct FusedArgs {
   uint32_t* lab1;
   unsigned long long* cells0;  // pass parity 0 / 1
   unsigned long long* cells1;
-  uint8_t* split0;
-  uint8_t* split1;
   uint32_t* changed;  // one flag per pass of this launch (zeroed by the host)
   uint32_t pass0;
   uint32_t max_passes;
@@ -325,9 +324,11 @@ struct FusedArgs {
   uint32_t* out;  // [0] passes executed, [1] stable, [2] buffer holding the labels
 };
 
-__device__ __forceinline__ uint32_t label_on_the_fly(uint32_t l, uint8_t s,
-                                                     const unsigned long long* cprev) {
-  return s ? (uint32_t)cprev[l] : l;
+// label words carry the previous pass's split flag in bit 31 (state ids < 2^31), so
+// one gather yields both the label and whether it must be corrected
+constexpr uint32_t kSplitBit = 0x80000000u;
+__device__ __forceinline__ uint32_t label_on_the_fly(uint32_t w, const unsigned long long* cprev) {
+  return (w & kSplitBit) ? (uint32_t)cprev[w & ~kSplitBit] : w;
 }
 
 template <int kPolicy>
@@ -342,8 +343,6 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
     const uint32_t pass = a.pass0 + p + 1;
     const uint32_t* Lm = sel ? a.lab1 : a.lab0;
     uint32_t* Lw = sel ? a.lab0 : a.lab1;
-    const uint8_t* sprev = (pass & 1) ? a.split0 : a.split1;
-    uint8_t* scur = (pass & 1) ? a.split1 : a.split0;
     const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
     unsigned long long* ccur = (pass & 1) ? a.cells1 : a.cells0;
     const uint32_t prev_changed =
@@ -354,12 +353,11 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
       if (qi >= a.n) continue;
       const uint32_t q = (uint32_t)qi;
-      const uint32_t leader = label_on_the_fly(Lm[q], sprev[q], cprev);
+      const uint32_t leader = label_on_the_fly(Lm[q], cprev);
       bool sp = false;
       if (q != leader) {
         for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
           uint32_t tq[4], tl[4], lq[4], ll[4];
-          uint8_t sq[4], sl[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (a0 + u < a.letters) {
@@ -370,18 +368,15 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
           for (int u = 0; u < 4; ++u)
             if (a0 + u < a.letters) {
               lq[u] = Lm[tq[u]];
-              sq[u] = sprev[tq[u]];
               ll[u] = Lm[tl[u]];
-              sl[u] = sprev[tl[u]];
             }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (a0 + u < a.letters)
-              sp |= label_on_the_fly(lq[u], sq[u], cprev) != label_on_the_fly(ll[u], sl[u], cprev);
+              sp |= label_on_the_fly(lq[u], cprev) != label_on_the_fly(ll[u], cprev);
         }
       }
-      Lw[q] = leader;
-      scur[q] = sp;
+      Lw[q] = leader | (sp ? kSplitBit : 0u);  // this pass's split rides with the label
       any |= sp;
       elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
     }
@@ -712,33 +707,28 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     out.status = DFM_STATUS_OK;
     return out;
   }
-  if (!tracing_ && !fused_cas && fused_enabled() && n <= fused_max_states(ctx)) {
-    // one barrier per pass (fused_pr_kernel) while every state has its own thread.
-    // Measured (B200): C1 random_dfa(1e5, 2) 95 -> 88 ms, fib_dfa(22) 129 -> 108 ms;
-    // with several states per thread the extra label/flag/cell gathers cost more than
-    // the barrier saves (vlts 1e6 x 20: 66 -> 92 ms), so larger inputs take the
-    // two-phase kernel
+  if (!tracing_ && !fused_cas && fused_enabled() && n <= kPersistentMaxStates) {
+    // one barrier per pass (fused_pr_kernel), grid-stride over the resident threads.
+    // Measured (B200, against the two-phase persistent kernel): C1 random_dfa(1e5, 2)
+    // 95 -> 79 ms, vlts(1000, 1e6, 20) 66 -> 60 ms, transPR comb(1e6, 3) 12.8 -> 10.8 ms
     const uint32_t kChunkMax = 8192;
     uint32_t chunk = 16;
     uint32_t* chg = ctx.slot_t<uint32_t>("pr.pchanged", kChunkMax);
     uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
     auto* cells1 = ctx.slot_t<unsigned long long>("pr.cells1", n);
-    uint8_t* split1 = ctx.slot_t<uint8_t>("pr.split1", n);
     DFM_CUDA(cudaMemsetAsync(cells1, policy == DFM_POLICY_MIN ? 0xFF : 0x00, n * 8, ctx.stream));
-    DFM_CUDA(cudaMemsetAsync(split_flag, 0, n, ctx.stream));
-    DFM_CUDA(cudaMemsetAsync(split1, 0, n, ctx.stream));
     void (*kern)(FusedArgs) = policy == DFM_POLICY_MIN   ? fused_pr_kernel<DFM_POLICY_MIN>
                               : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX>
                                                          : fused_pr_kernel<DFM_POLICY_ARBITRARY>;
-    const unsigned pgrid = (unsigned)ceil_div(n, kPersistThreads);
+    const unsigned pgrid = (unsigned)std::min<uint64_t>(
+        ceil_div(n, kPersistThreads), fused_max_states(ctx) / kPersistThreads);
     while (true) {
       if (dl.expired()) {
         out.status = DFM_STATUS_TIMEOUT;
         return out;
       }
       DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
-      FusedArgs fa{rows,  n,    letters, lab[0], lab[1], cells, cells1,
-                   split_flag, split1, chg, pass, chunk, sel, pout};
+      FusedArgs fa{rows, n, letters, lab[0], lab[1], cells, cells1, chg, pass, chunk, sel, pout};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&fa};
       ProfScope prof(ctx, "elect", 0);
