@@ -44,5 +44,12 @@ if [[ " $WHAT " == *" ncu "* ]]; then
       -o $OUT/prof_default python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"square_kernel" -c 2 \
       -o $OUT/prof_trans python bench.py --algo trans --family fib --n 12 --k 1 --steps 1 --warmup 0 --no-e2e > $OUT/ncu_trans.log 2>&1
+  # the reports themselves can exceed gpurun's 64 MiB copy-back: keep their raw pages
+  for r in default trans; do
+    if [ -f $OUT/prof_$r.ncu-rep ]; then
+      ncu -i $OUT/prof_$r.ncu-rep --page raw --csv > $OUT/prof_${r}_raw.csv 2>/dev/null
+      rm -f $OUT/prof_$r.ncu-rep
+    fi
+  done
   ls -la $OUT
 fi

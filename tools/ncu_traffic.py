@@ -1,7 +1,7 @@
 """Per-family DRAM bytes of one sortPR step from an ncu --set full report of
 `python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline` (all kernels):
 writes the summary bench.py reports as roofline.traffic.
-usage: python tools/ncu_traffic.py report.ncu-rep out.json"""
+usage: python tools/ncu_traffic.py report.ncu-rep|raw.csv out.json"""
 import csv
 import io
 import json
@@ -21,8 +21,11 @@ FAMILY = [  # kernel-name regex -> bench.py ProfScope family
 ]
 
 rep, out = sys.argv[1], sys.argv[2]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+if rep.endswith(".csv"):  # the raw page saved next to the run (tools/gpu_suite.sh)
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
 ki = h.index("Kernel Name")
