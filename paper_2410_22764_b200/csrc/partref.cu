@@ -594,7 +594,17 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 
 }  // namespace
 
-constexpr uint64_t kPersistentMaxStates = 1ull << 22;
+// Persistent kernels (all passes in one launch; grid barriers) up to 2M states;
+// larger inputs launch each pass at full occupancy.  Measured (B200, persistent vs
+// per-pass launches): transPR chain 1e6 1.70 vs 1.92 ms, chain 4e6 7.5 vs 4.7 ms,
+// comb 4e6 10.8 vs 8.9 ms; naive vlts 1e6 (602 passes) 59.8 vs 69.4 ms, random 3e5
+// (50,291 passes) 477 vs 1421 ms.
+constexpr uint64_t kPersistentMaxStates = 1ull << 21;
+
+uint64_t persistent_max_states() {  // DFM_NAIVE_PERSIST_MAX (experiments)
+  const char* e = getenv("DFM_NAIVE_PERSIST_MAX");
+  return e ? strtoull(e, nullptr, 10) : kPersistentMaxStates;
+}
 constexpr uint64_t kClusterMaxStates = 4096;
 
 uint64_t fused_max_states(const Ctx& ctx) {
@@ -707,7 +717,8 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     out.status = DFM_STATUS_OK;
     return out;
   }
-  if (!tracing_ && !fused_cas && fused_enabled() && n <= kPersistentMaxStates) {
+  const uint64_t persist_max = persistent_max_states();
+  if (!tracing_ && !fused_cas && fused_enabled() && n <= persist_max) {
     // one barrier per pass (fused_pr_kernel), grid-stride over the resident threads.
     // Measured (B200, against the two-phase persistent kernel): C1 random_dfa(1e5, 2)
     // 95 -> 79 ms, vlts(1000, 1e6, 20) 66 -> 60 ms, transPR comb(1e6, 3) 12.8 -> 10.8 ms
@@ -750,7 +761,7 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     out.status = DFM_STATUS_OK;
     return out;
   }
-  if (!tracing_ && n <= kPersistentMaxStates) {
+  if (!tracing_ && n <= persist_max) {
     // one cooperative launch per chunk of passes; the deadline is checked between
     // chunks (the reference checks it before every pass, min_partref.hpp:78-83), so
     // chunks start small and double: a run that overruns its deadline is reported as
