@@ -36,6 +36,7 @@ constexpr int kStageBytes = kStageA + kStageB;     // 48 KB
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int kThreads = 256;
 constexpr int kGroupM = 16;  // rasterisation: 16 M-tiles share the concurrent wave
+constexpr uint32_t kMaxKBlocks = 1024;  // Vp <= 131072 (|V| = n^2 <= 65,536 here)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -114,10 +115,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tile occupancy bit of the 128x128 tile (mt, ct)
+__device__ __forceinline__ bool tile_nz(const uint32_t* nz, uint32_t T, uint32_t mt, uint32_t ct) {
+  const uint32_t b = mt * T + ct;
+  return (nz[b >> 5] >> (b & 31)) & 1u;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     square_kernel(const __grid_constant__ CUtensorMap map, const int8_t* __restrict__ reach,
                   int8_t* __restrict__ next, const unsigned long long* __restrict__ apart,
-                  unsigned long long* apart_next, uint32_t Vp, uint32_t W) {
+                  unsigned long long* apart_next, uint32_t Vp, uint32_t W,
+                  const uint32_t* __restrict__ nz, uint32_t* __restrict__ nz_next,
+                  unsigned long long* live_blocks) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -137,6 +146,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t m0 = (first_m + in_group % gm) * kBM;
   const uint32_t n0 = (in_group / gm) * kBN;
   const uint32_t kblocks = Vp / kBK;
+  // K block kb contributes only if the A tile (m0, kb) and one of the B tiles
+  // (kb, n0) / (kb, n0 + 128) hold a one (producer and MMA warp skip the same ones)
+  const uint32_t T = Vp / 128, mt = m0 / 128, nt = n0 / 128;
+  __shared__ uint32_t s_live[kMaxKBlocks / 32];  // live K blocks of this tile, one bit each
+  for (uint32_t w = threadIdx.x; w < kMaxKBlocks / 32; w += blockDim.x) s_live[w] = 0;
+  __syncthreads();
+  for (uint32_t kb = threadIdx.x; kb < kblocks; kb += blockDim.x)
+    if (tile_nz(nz, T, mt, kb) && (tile_nz(nz, T, kb, nt) || tile_nz(nz, T, kb, nt + 1)))
+      atomicOr(&s_live[kb >> 5], 1u << (kb & 31));
+  auto live = [&](uint32_t kb) { return (s_live[kb >> 5] >> (kb & 31)) & 1u; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -160,10 +179,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
+      uint32_t j = 0;  // live blocks so far
       for (uint32_t kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t round = kb / kStages;
-        if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], (round - 1) & 1);
+        if (!live(kb)) continue;
+        const int s = j % kStages;
+        const uint32_t round = j / kStages;
+        if (j >= (uint32_t)kStages) mbar_wait(&empty[s], (round - 1) & 1);
+        ++j;
         uint8_t* a = smem + s * kStageBytes;
         uint8_t* b = a + kStageA;
         mbar_expect_tx(&full[s], kStageBytes);
@@ -174,9 +196,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
+      uint32_t j = 0;
       for (uint32_t kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+        if (!live(kb)) continue;
+        const int s = j % kStages;
+        mbar_wait(&full[s], (j / kStages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t a = smem_u32(smem + s * kStageBytes);
         const uint32_t b = a + kStageA;
@@ -185,15 +209,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           // A K-major: +32 bytes along K; B MN-major: +32 rows of 128 bytes
           const uint64_t da = smem_desc(a + kk * 32, 16, 1024);
           const uint64_t db = smem_desc(b + kk * 32 * 128, kStageB / 2, 1024);
-          umma_i8(tmem, da, db, (kb | kk) != 0 ? 1u : 0u);
+          umma_i8(tmem, da, db, (j | kk) != 0 ? 1u : 0u);
         }
         umma_commit(&empty[s]);  // frees the stage once these MMAs retire
+        ++j;
       }
+      if (j) atomicAdd(live_blocks, (unsigned long long)j);  // (the executed ops, for the roofline)
       umma_commit(acc_full);
     }
   } else if (warp >= 4) {  // epilogue: one accumulator row per thread
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    bool any_mma = false;  // no live K block: the accumulator was never written (zero)
+    for (uint32_t kb = 0; kb < kblocks && !any_mma; ++kb) any_mma = live(kb);
     const uint32_t quarter = warp - 4;  // TMEM lanes [32*quarter, 32*quarter+32)
     const uint32_t row = m0 + quarter * 32 + lane;
     const int8_t* rrow = reach + (uint64_t)row * Vp;
@@ -202,7 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int c = 0; c < kBN / 32; ++c) {
       uint32_t v[32];
-      tmem_ld32(tmem + ((quarter * 32) << 16) + c * 32, v);
+      if (any_mma) {
+        tmem_ld32(tmem + ((quarter * 32) << 16) + c * 32, v);
+      } else {
+#pragma unroll
+        for (int b = 0; b < 32; ++b) v[b] = 0;
+      }
       const uint32_t j0 = n0 + c * 32;
       const uint4* rp = reinterpret_cast<const uint4*>(rrow + j0);
       const uint4 r0 = rp[0], r1 = rp[1];
@@ -225,6 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       op[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
       const uint32_t abits = (j0 >> 6) < W ? (uint32_t)(apart[j0 >> 6] >> (j0 & 63)) : 0u;
       hit |= (mask & abits) != 0u;
+      // occupancy of next for the following pass: tile (mt, j0 / 128)
+      if (__any_sync(0xffffffffu, mask != 0u) && lane == 0) {
+        const uint32_t b = mt * T + j0 / 128;
+        atomicOr(&nz_next[b >> 5], 1u << (b & 31));
+      }
     }
     if (hit) atomicOr(&apart_next[row >> 6], 1ull << (row & 63));
   }
@@ -238,12 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // 0/1 byte matrix init: row s = (q,r) gets 1 at (delta_a(q), delta_a(r)) for every a
 __global__ void init_bytes_kernel(const uint32_t* __restrict__ delta, uint64_t n, uint32_t k,
-                                  uint64_t V, uint64_t Vp, int8_t* __restrict__ R) {
+                                  uint64_t V, uint64_t Vp, int8_t* __restrict__ R,
+                                  uint32_t* __restrict__ nz) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < V; s += stride) {
     const uint64_t q = s / n, r = s % n;
-    for (uint32_t a = 0; a < k; ++a)
-      R[s * Vp + (uint64_t)delta[a * n + q] * n + delta[a * n + r]] = 1;
+    for (uint32_t a = 0; a < k; ++a) {
+      const uint64_t c = (uint64_t)delta[a * n + q] * n + delta[a * n + r];
+      R[s * Vp + c] = 1;
+      const uint64_t b = (s / 128) * (Vp / 128) + c / 128;
+      atomicOr(&nz[b >> 5], 1u << (b & 31));
+    }
   }
 }
 
@@ -308,9 +351,15 @@ TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V) {
   st.reach = ctx.slot_t<int8_t>("tc.R0", bytes);
   st.next = ctx.slot_t<int8_t>("tc.R1", bytes);
   DFM_CUDA(cudaMemsetAsync(st.reach, 0, bytes, ctx.stream));
+  const uint64_t T = st.Vp / 128, nzw = ceil_div(T * T, 32);
+  st.nz = ctx.slot_t<uint32_t>("tc.nz0", nzw);
+  st.nz_next = ctx.slot_t<uint32_t>("tc.nz1", nzw);
+  // DFM_TRANS_DENSE=1: every tile treated as occupied (the dense squaring; tests)
+  const char* dense = getenv("DFM_TRANS_DENSE");
+  DFM_CUDA(cudaMemsetAsync(st.nz, (dense && dense[0] == '1') ? 0xFF : 0x00, nzw * 4, ctx.stream));
   const unsigned grid =
       (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(V, 1), 256), ctx.num_sms * 16ull);
-  init_bytes_kernel<<<grid, 256, 0, ctx.stream>>>(d.delta, d.n, d.k, V, st.Vp, st.reach);
+  init_bytes_kernel<<<grid, 256, 0, ctx.stream>>>(d.delta, d.n, d.k, V, st.Vp, st.reach, st.nz);
   DFM_LAUNCH_CHECK();
   return st;
 }
@@ -322,14 +371,28 @@ void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* 
   DFM_LAUNCH_CHECK();
   const CUtensorMap map = make_map(st.reach, st.Vp);
   const uint64_t tiles = (st.Vp / kBM) * (st.Vp / kBN);
+  const uint64_t T = st.Vp / 128, nzw = ceil_div(T * T, 32);
+  const char* dense = getenv("DFM_TRANS_DENSE");
+  DFM_CUDA(cudaMemsetAsync(st.nz_next, (dense && dense[0] == '1') ? 0xFF : 0x00, nzw * 4,
+                           ctx.stream));
   {
-    // 2*Vp^3 int8 multiply-adds (as ops) per pass; bytes: algorithmic tensor-bound figure
-    ProfScope p(ctx, "gemm", 2ull * st.Vp * st.Vp * st.Vp);
+    // int8 ops executed: 2 * 128 * 256 * 128 per live (output tile, K block) — the
+    // dense pass would be 2 * Vp^3; K blocks of all-zero tiles are skipped
+    auto* live = reinterpret_cast<unsigned long long*>(ctx.d_scalars + 56);
+    DFM_CUDA(cudaMemsetAsync(live, 0, 8, ctx.stream));
+    ProfScope p(ctx, "gemm", 0);
     square_kernel<<<(unsigned)tiles, kThreads, kSmemBytes, ctx.stream>>>(
-        map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W);
+        map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W, st.nz,
+        st.nz_next, live);
     DFM_LAUNCH_CHECK();
+    p.stop();
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 56, live, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    p.bytes = ctx.h_scalars[56] * 2ull * kBM * kBN * kBK;
+    st.skipped_blocks += tiles * (st.Vp / kBK) - ctx.h_scalars[56];
   }
   std::swap(st.reach, st.next);
+  std::swap(st.nz, st.nz_next);
 }
 
 }  // namespace trans_tc

@@ -12,6 +12,11 @@ struct TransTcState {
   uint64_t Vp = 0;    // padded to the GEMM tile
   int8_t* reach = nullptr;   // Vp x Vp 0/1 bytes, row-major (A K-major, B MN-major)
   int8_t* next = nullptr;
+  // 128x128-tile occupancy of reach / next (bit mt*T + kt, T = Vp/128): the squaring
+  // skips the K blocks whose A or B tile is all zero
+  uint32_t* nz = nullptr;
+  uint32_t* nz_next = nullptr;
+  uint64_t skipped_blocks = 0;  // (diagnostics)
 };
 
 namespace trans_tc {

@@ -56,3 +56,20 @@ def test_tensor_engine_matches_bit_engine_large(tc, bit):
         assert a.stats.iterations == b.stats.iterations
         assert ti.apart_popcounts == bi.apart_popcounts
         assert (ti.apart == bi.apart).all()
+
+
+def test_tile_skipping_matches_dense(tc, monkeypatch):
+    """The tensor squaring skips K blocks whose 128x128 tiles are all zero; forcing
+    every tile occupied (DFM_TRANS_DENSE=1) gives the same partition, passes and
+    apartness trace."""
+    for pair in (O.fib_dfa(10), O.random_dfa(100, 2, 3, 0.5)):
+        d = to_dfa(pair)
+        ins = dfm.TransInspect()
+        r = tc.trans_minimize(d, inspect=ins)
+        monkeypatch.setenv("DFM_TRANS_DENSE", "1")
+        ins0 = dfm.TransInspect()
+        r0 = tc.trans_minimize(d, inspect=ins0)
+        monkeypatch.delenv("DFM_TRANS_DENSE")
+        assert (r.partition.block == r0.partition.block).all()
+        assert r.stats.iterations == r0.stats.iterations
+        assert ins.apart_popcounts == ins0.apart_popcounts
