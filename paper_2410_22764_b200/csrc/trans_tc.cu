@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   int8_t* __restrict__ next, const unsigned long long* __restrict__ apart,
                   unsigned long long* apart_next, uint32_t Vp, uint32_t W,
                   const uint32_t* __restrict__ nz, uint32_t* __restrict__ nz_next,
-                  unsigned long long* live_blocks) {
+                  unsigned long long* live_blocks, const uint32_t* __restrict__ tile_list) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // rasterised tile order: groups of kGroupM M-tiles sweep all N-tiles together
   const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN;
-  const uint32_t tid = blockIdx.x;
+  const uint32_t tid = tile_list ? tile_list[blockIdx.x] : blockIdx.x;
   const uint32_t group = tid / (kGroupM * tiles_n);
   const uint32_t first_m = group * kGroupM;
   const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
@@ -308,6 +308,82 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Output tiles (in square_kernel's rasterised order) with / without a live K block;
+// the live ones go to the tensor kernel, the others to the copy kernel below, so
+// the 197 KB-smem tensor CTAs run only where there is something to multiply
+__global__ void tile_classify_kernel(const uint32_t* __restrict__ nz, uint32_t Vp,
+                                     uint32_t* __restrict__ live_list,
+                                     uint32_t* __restrict__ dead_list, uint32_t* counts) {
+  const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN, T = Vp / 128;
+  const uint32_t tiles = tiles_m * tiles_n;
+  for (uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x; tid - (threadIdx.x & 31) < tiles;
+       tid += gridDim.x * blockDim.x) {
+    bool live = false;
+    if (tid < tiles) {
+      const uint32_t group = tid / (kGroupM * tiles_n);
+      const uint32_t first_m = group * kGroupM;
+      const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
+      const uint32_t in_group = tid - group * kGroupM * tiles_n;
+      const uint32_t mt = first_m + in_group % gm, nt = (in_group / gm) * 2;
+      for (uint32_t kb = 0; kb < T && !live; ++kb)
+        live = tile_nz(nz, T, mt, kb) && (tile_nz(nz, T, kb, nt) || tile_nz(nz, T, kb, nt + 1));
+    }
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t vm = __ballot_sync(0xffffffffu, tid < tiles && live);
+    const uint32_t dm = __ballot_sync(0xffffffffu, tid < tiles && !live);
+    uint32_t lb = 0, db = 0;
+    if (lane == 0) {
+      if (vm) lb = atomicAdd(&counts[0], (uint32_t)__popc(vm));
+      if (dm) db = atomicAdd(&counts[1], (uint32_t)__popc(dm));
+    }
+    lb = __shfl_sync(0xffffffffu, lb, 0);
+    db = __shfl_sync(0xffffffffu, db, 0);
+    const uint32_t below = (1u << lane) - 1u;
+    if ((vm >> lane) & 1u) live_list[lb + __popc(vm & below)] = tid;
+    if ((dm >> lane) & 1u) dead_list[db + __popc(dm & below)] = tid;
+  }
+}
+
+// next = R on a tile without live K blocks, with the apartness propagation and the
+// occupancy bits (one 256-thread CTA per tile, small footprint: many CTAs per SM)
+__global__ void __launch_bounds__(256) dead_copy_kernel(const int8_t* __restrict__ reach,
+                                                        int8_t* __restrict__ next, uint32_t Vp,
+                                                        const uint32_t* __restrict__ dead_list,
+                                                        const unsigned long long* __restrict__ apart,
+                                                        unsigned long long* apart_next, uint32_t W,
+                                                        uint32_t* __restrict__ nz_next) {
+  __shared__ uint32_t s_occ[2];
+  const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN, T = Vp / 128;
+  const uint32_t tid = dead_list[blockIdx.x];
+  const uint32_t group = tid / (kGroupM * tiles_n);
+  const uint32_t first_m = group * kGroupM;
+  const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
+  const uint32_t in_group = tid - group * kGroupM * tiles_n;
+  const uint32_t m0 = (first_m + in_group % gm) * kBM;
+  const uint32_t n0 = (in_group / gm) * kBN;
+  if (threadIdx.x < 2) s_occ[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t idx = threadIdx.x; idx < kBM * (kBN / 16); idx += blockDim.x) {
+    const uint32_t r = idx / (kBN / 16), c = (idx % (kBN / 16)) * 16;
+    const uint64_t off = (uint64_t)(m0 + r) * Vp + n0 + c;
+    const uint4 v = *reinterpret_cast<const uint4*>(reach + off);
+    *reinterpret_cast<uint4*>(next + off) = v;
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+    uint32_t mask = 0;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) mask |= (((w4[b >> 2] >> ((b & 3) * 8)) & 0xFFu) ? 1u : 0u) << b;
+    const uint32_t j0 = n0 + c;
+    const uint32_t abits = (j0 >> 6) < W ? (uint32_t)(apart[j0 >> 6] >> (j0 & 63)) & 0xFFFFu : 0u;
+    if (mask & abits) atomicOr(&apart_next[(m0 + r) >> 6], 1ull << ((m0 + r) & 63));
+    if (mask) atomicOr(&s_occ[c >> 7], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 && s_occ[threadIdx.x]) {
+    const uint32_t b = (m0 / 128) * T + n0 / 128 + threadIdx.x;
+    atomicOr(&nz_next[b >> 5], 1u << (b & 31));
+  }
+}
+
 // 0/1 byte matrix init: row s = (q,r) gets 1 at (delta_a(q), delta_a(r)) for every a
 __global__ void init_bytes_kernel(const uint32_t* __restrict__ delta, uint64_t n, uint32_t k,
                                   uint64_t V, uint64_t Vp, int8_t* __restrict__ R,
@@ -413,11 +489,28 @@ void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* 
     // int8 ops executed: 2 * 128 * 256 * 128 per live (output tile, K block) — the
     // dense pass would be 2 * Vp^3; K blocks of all-zero tiles are skipped
     auto* live = reinterpret_cast<unsigned long long*>(ctx.d_scalars + 56);
-    DFM_CUDA(cudaMemsetAsync(live, 0, 8, ctx.stream));
+    uint32_t* counts = reinterpret_cast<uint32_t*>(ctx.d_scalars + 57);
+    uint32_t* live_list = ctx.slot_t<uint32_t>("tc.live", tiles);
+    uint32_t* dead_list = ctx.slot_t<uint32_t>("tc.dead", tiles);
+    DFM_CUDA(cudaMemsetAsync(live, 0, 16, ctx.stream));  // live blocks + the two counts
     ProfScope p(ctx, "gemm", 0);
-    square_kernel<<<(unsigned)tiles, kThreads, kSmemBytes, ctx.stream>>>(
-        map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W, st.nz,
-        st.nz_next, live);
+    tile_classify_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(tiles, 256), ctx.num_sms * 8ull),
+                           256, 0, ctx.stream>>>(st.nz, (uint32_t)st.Vp, live_list, dead_list,
+                                                 counts);
+    DFM_LAUNCH_CHECK();
+    DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 57, counts, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    const uint32_t n_live = (uint32_t)(ctx.h_scalars[57] & 0xFFFFFFFFu);
+    const uint32_t n_dead = (uint32_t)(ctx.h_scalars[57] >> 32);
+    if (n_dead)
+      dead_copy_kernel<<<n_dead, 256, 0, ctx.stream>>>(st.reach, st.next, (uint32_t)st.Vp,
+                                                      dead_list, apart, apart_next, (uint32_t)W,
+                                                      st.nz_next);
+    DFM_LAUNCH_CHECK();
+    if (n_live)
+      square_kernel<<<n_live, kThreads, kSmemBytes, ctx.stream>>>(
+          map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W, st.nz,
+          st.nz_next, live, live_list);
     DFM_LAUNCH_CHECK();
     p.stop();
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 56, live, 8, cudaMemcpyDeviceToHost, ctx.stream));
