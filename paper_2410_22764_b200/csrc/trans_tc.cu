@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // rasterised tile order: groups of kGroupM M-tiles sweep all N-tiles together
   const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN;
-  const uint32_t tid = tile_list ? tile_list[blockIdx.x] : blockIdx.x;
+  const uint32_t tid = tile_list[blockIdx.x];  // a tile with live K blocks
   const uint32_t group = tid / (kGroupM * tiles_n);
   const uint32_t first_m = group * kGroupM;
   const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
@@ -156,40 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tile_nz(nz, T, mt, kb) && (tile_nz(nz, T, kb, nt) || tile_nz(nz, T, kb, nt + 1)))
       atomicOr(&s_live[kb >> 5], 1u << (kb & 31));
   auto live = [&](uint32_t kb) { return (s_live[kb >> 5] >> (kb & 31)) & 1u; };
-  __syncthreads();
-  {
-    // no live K block: next = R on this tile.  All 256 threads copy it with 16-byte
-    // accesses (16 threads per 256-byte row), fold in the apartness propagation and
-    // the occupancy bits, and the CTA leaves without barriers or TMEM.
-    uint32_t any = 0;
-    for (uint32_t w = 0; w < (kblocks + 31) / 32; ++w) any |= s_live[w];
-    if (any == 0) {
-      __shared__ uint32_t s_occ[2];
-      if (threadIdx.x < 2) s_occ[threadIdx.x] = 0;
-      __syncthreads();
-      for (uint32_t idx = threadIdx.x; idx < kBM * (kBN / 16); idx += blockDim.x) {
-        const uint32_t r = idx / (kBN / 16), c = (idx % (kBN / 16)) * 16;
-        const uint64_t off = (uint64_t)(m0 + r) * Vp + n0 + c;
-        const uint4 v = *reinterpret_cast<const uint4*>(reach + off);
-        *reinterpret_cast<uint4*>(next + off) = v;
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
-        uint32_t mask = 0;  // non-zero bytes of these 16 columns
-#pragma unroll
-        for (int b = 0; b < 16; ++b) mask |= (((w4[b >> 2] >> ((b & 3) * 8)) & 0xFFu) ? 1u : 0u) << b;
-        const uint32_t j0 = n0 + c;
-        const uint32_t abits =
-            (j0 >> 6) < W ? (uint32_t)(apart[j0 >> 6] >> (j0 & 63)) & 0xFFFFu : 0u;
-        if (mask & abits) atomicOr(&apart_next[(m0 + r) >> 6], 1ull << ((m0 + r) & 63));
-        if (mask) atomicOr(&s_occ[c >> 7], 1u);
-      }
-      __syncthreads();
-      if (threadIdx.x < 2 && s_occ[threadIdx.x]) {
-        const uint32_t b = mt * T + nt + threadIdx.x;
-        atomicOr(&nz_next[b >> 5], 1u << (b & 31));
-      }
-      return;
-    }
-  }
+  // (tiles without a live K block never get here: dead_copy_kernel handles them;
+  // the __syncthreads below — after the TMEM allocation — publishes s_live)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -516,7 +484,6 @@ void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* 
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 56, live, 8, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();
     p.bytes = ctx.h_scalars[56] * 2ull * kBM * kBN * kBK;
-    st.skipped_blocks += tiles * (st.Vp / kBK) - ctx.h_scalars[56];
   }
   std::swap(st.reach, st.next);
   std::swap(st.nz, st.nz_next);

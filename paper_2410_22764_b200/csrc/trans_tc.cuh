@@ -16,7 +16,6 @@ struct TransTcState {
   // skips the K blocks whose A or B tile is all zero
   uint32_t* nz = nullptr;
   uint32_t* nz_next = nullptr;
-  uint64_t skipped_blocks = 0;  // (diagnostics)
 };
 
 namespace trans_tc {
