@@ -20,7 +20,7 @@ def _device_result(eng, dd, n):
 
 
 @pytest.mark.parametrize("n,k,seed", [(17_000_001, 4, 21), (40_000_000, 2, 22),
-                                      (9_000_000, 8, 23)])
+                                      (9_000_000, 8, 23), (70_000_003, 1, 24)])
 def test_pipelined_upload_matches_device_run(eng, n, k, seed):
     dd = eng.random_dfa_device(n, k, seed, 0.5)
     nb, it, lab = _device_result(eng, dd, n)
