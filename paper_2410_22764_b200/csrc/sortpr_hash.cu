@@ -462,6 +462,11 @@ __device__ __forceinline__ uint32_t atom_or_keep(uint32_t* a, uint32_t v, uint64
                : "=r"(old) : "l"(a), "r"(v), "l"(pol) : "memory");
   return old;
 }
+// (no result needed: a fire-and-forget reduction, no round trip)
+__device__ __forceinline__ void red_or_keep(uint32_t* a, uint32_t v, uint64_t pol) {
+  asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol)
+               : "memory");
+}
 
 // level 0 uses hash bits [36, 64), level 1 bits [8, 36) of the same 64-bit table hash;
 // level 1 only sees the candidates level 0 left (slot_of != kUnique)
@@ -479,7 +484,7 @@ __global__ void __launch_bounds__(256) filt_set_kernel(const unsigned long long*
                        ((1ull << kFilterCellBits) - 1);
     const uint32_t b = (uint32_t)(c & 15) * 2;
     const uint32_t old = atom_or_keep(&F[c >> 4], 1u << b, pol_keep);
-    if ((old >> b) & 1u) atom_or_keep(&F[c >> 4], 2u << b, pol_keep);
+    if (((old >> b) & 3u) == 1u) red_or_keep(&F[c >> 4], 2u << b, pol_keep);
   }
 }
 
