@@ -331,7 +331,7 @@ __device__ __forceinline__ uint32_t label_on_the_fly(uint32_t w, const unsigned 
   return (w & kSplitBit) ? (uint32_t)cprev[w & ~kSplitBit] : w;
 }
 
-template <int kPolicy>
+template <int kPolicy, bool kOne>
 __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) {
   cg::grid_group g = cg::this_grid();
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -339,6 +339,16 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
   int sel = a.start_sel;
   uint32_t p = 0;
   bool stable = false;
+  // one state per thread (n <= resident threads): the first four successors of the
+  // state and of its leader stay in registers — the leader changes only when the
+  // state splits — taking the leader-row load off the pass's dependent chain
+  constexpr bool one = kOne;  // the host launches kOne only when n <= resident threads
+  uint32_t cl = 0xFFFFFFFFu, crow[4] = {0, 0, 0, 0}, qrow[4] = {0, 0, 0, 0};
+  if (one && first < a.n) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if ((uint64_t)u < a.letters) qrow[u] = a.rows[(uint64_t)u * a.n + first];
+  }
   while (p < a.max_passes) {
     const uint32_t pass = a.pass0 + p + 1;
     const uint32_t* Lm = sel ? a.lab1 : a.lab0;
@@ -355,14 +365,20 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       const uint32_t q = (uint32_t)qi;
       const uint32_t leader = label_on_the_fly(Lm[q], cprev);
       bool sp = false;
+      if (one && leader != cl && q != leader) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if ((uint64_t)u < a.letters) crow[u] = a.rows[(uint64_t)u * a.n + leader];
+        cl = leader;
+      }
       if (q != leader) {
         for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
           uint32_t tq[4], tl[4], lq[4], ll[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (a0 + u < a.letters) {
-              tq[u] = a.rows[(a0 + u) * a.n + q];
-              tl[u] = a.rows[(a0 + u) * a.n + leader];
+              tq[u] = (one && a0 == 0) ? qrow[u] : a.rows[(a0 + u) * a.n + q];
+              tl[u] = (one && a0 == 0) ? crow[u] : a.rows[(a0 + u) * a.n + leader];
             }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -611,7 +627,7 @@ uint64_t fused_max_states(const Ctx& ctx) {
   static int per_sm = -1;
   if (per_sm < 0)
     DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, fused_pr_kernel<DFM_POLICY_MIN>, kPersistThreads, 0));
+        &per_sm, fused_pr_kernel<DFM_POLICY_MIN, false>, kPersistThreads, 0));
   return (uint64_t)per_sm * ctx.num_sms * kPersistThreads;
 }
 
@@ -728,9 +744,14 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
     auto* cells1 = ctx.slot_t<unsigned long long>("pr.cells1", n);
     DFM_CUDA(cudaMemsetAsync(cells1, policy == DFM_POLICY_MIN ? 0xFF : 0x00, n * 8, ctx.stream));
-    void (*kern)(FusedArgs) = policy == DFM_POLICY_MIN   ? fused_pr_kernel<DFM_POLICY_MIN>
-                              : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX>
-                                                         : fused_pr_kernel<DFM_POLICY_ARBITRARY>;
+    const bool one = n <= fused_max_states(ctx);  // a thread per state
+    void (*kern)(FusedArgs) =
+        policy == DFM_POLICY_MIN
+            ? (one ? fused_pr_kernel<DFM_POLICY_MIN, true> : fused_pr_kernel<DFM_POLICY_MIN, false>)
+        : policy == DFM_POLICY_MAX
+            ? (one ? fused_pr_kernel<DFM_POLICY_MAX, true> : fused_pr_kernel<DFM_POLICY_MAX, false>)
+            : (one ? fused_pr_kernel<DFM_POLICY_ARBITRARY, true>
+                   : fused_pr_kernel<DFM_POLICY_ARBITRARY, false>);
     const unsigned pgrid = (unsigned)std::min<uint64_t>(
         ceil_div(n, kPersistThreads), fused_max_states(ctx) / kPersistThreads);
     while (true) {
