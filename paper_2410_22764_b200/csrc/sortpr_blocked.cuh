@@ -391,7 +391,8 @@ struct SigParams {
   // and vals[i] = i | lead << 31
   uint32_t* vals;
   const uint8_t* lead;
-  uint32_t* present;  // direct keys: bitmap of the keys present (rank-compacted table)
+  uint32_t* present;  // direct keys: bitmap of the keys present, words interleaved with
+                      // their exclusive popcounts (rank-compacted table)
   uint32_t tile_bytes;  // shared tile size (16-byte multiple)
 };
 
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
         p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
         if (p.present) {  // test before set: most keys of a dense pass are repeats
           const uint32_t bit = 1u << (key & 31);
-          uint32_t* word = p.present + (key >> 5);
+          uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
           if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
         }
       } else {

@@ -81,8 +81,7 @@ struct InsertParams {
   unsigned long long* keys;  // precomputed exact keys (swept passes), else unused
   // rank-compacted direct table: slot = rank of the key among the keys present
   // (bitmap + per-word exclusive popcount); no same-slot warp aggregation
-  const uint32_t* present;
-  const uint32_t* present_pre;
+  const uint32_t* present;  // {bitmap word, exclusive popcount} pairs
   const uint32_t* cand;  // filtered passes: the states left for the table (m = their count)
   uint64_t i0;           // first index (pipelined first pass: one chunk of states)
   // relabel-in-place passes: the slot (key or key rank) + id_off becomes the new id
@@ -301,7 +300,9 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
         if (kDirect) {
           if (p.present) {
             const uint32_t w = (uint32_t)(key[u] >> 5);
-            s[u] = p.present_pre[w] + __popc(p.present[w] & ((1u << (key[u] & 31)) - 1u));
+            // {bitmap word, exclusive popcount} pairs: one 8-byte gather per key
+            const uint2 pw = *reinterpret_cast<const uint2*>(p.present + 2ull * w);
+            s[u] = pw.y + __popc(pw.x & ((1u << (key[u] & 31)) - 1u));
           } else {
             s[u] = key[u];
           }
@@ -772,12 +773,12 @@ __global__ void __launch_bounds__(256) rip_flag_kernel(uint64_t m, const uint32_
 }
 
 struct PresentIn {
-  const uint32_t* present;
-  __device__ uint32_t operator()(uint64_t w) const { return __popc(present[w]); }
+  const uint32_t* present;  // interleaved {bitmap word, prefix}
+  __device__ uint32_t operator()(uint64_t w) const { return __popc(present[2 * w]); }
 };
 struct PresentOut {
-  uint32_t* pre;
-  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { pre[w] = excl; }
+  uint32_t* present;  // the prefix goes next to its bitmap word
+  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { present[2 * w + 1] = excl; }
 };
 
 struct ActIn {
@@ -1507,7 +1508,6 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       const void* ids = mirror_bits == 32 ? (const void*)block : (const void*)mirror;
       unsigned long long* keys = nullptr;
       uint32_t* present = nullptr;  // rank-compacted direct table (blocked passes)
-      uint32_t* present_pre = nullptr;
       if (packed && (mirror_bits == 8 || mirror_bits == 16))
         keys = ctx.slot_t<unsigned long long>("sh.keys", m);
       // blocked signature builder whenever most states are active (it streams all n*k
@@ -1535,9 +1535,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         uint32_t* vals = part ? ctx.slot_t<uint32_t>("gp.v", m) : nullptr;
         if (!part && direct && table > kSmallTable) {
           const uint64_t words = ceil_div(table, 32);
-          present = ctx.slot_t<uint32_t>("sh.present", words);
-          present_pre = ctx.slot_t<uint32_t>("sh.presentpre", words);
-          DFM_CUDA(cudaMemsetAsync(present, 0, words * 4, ctx.stream));
+          // interleaved {bitmap word, exclusive popcount}: the rank is one 8-byte read
+          present = ctx.slot_t<uint32_t>("sh.present", 2 * words);
+          DFM_CUDA(cudaMemsetAsync(present, 0, 2 * words * 4, ctx.stream));
         }
         layout_keys(ctx, lay, mirror_bits, ids, act, m, block, w, !packed, seed, keys, sig, row,
                     vals, lead, present);
@@ -1560,7 +1560,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         const uint64_t words = ceil_div(table, 32);
         ProfScope p(ctx, "insert", words * 8);
         prims::lookback_scan(ctx, "sc.present", words, PresentIn{present},
-                             PresentOut{present_pre}, sc + 9);
+                             PresentOut{present}, sc + 9);
         DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 9, sc + 9, 8, cudaMemcpyDeviceToHost, ctx.stream));
         ctx.sync();
         cap = std::max<uint64_t>(1, ctx.h_scalars[9]);
@@ -1598,7 +1598,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(Slot), ctx.stream));
       InsertParams ip{d.delta, n, k, block, ids, act, lead, filtered ? ncand : m, w, seed, cap,
                       slots, slot_of, packed ? nullptr : sig, row, keys, present,
-                      present ? present_pre : nullptr, filtered ? cand : nullptr};
+                      filtered ? cand : nullptr};
       // direct tables whose slot can become the id at once: the tiny smem-aggregated
       // ones (the ids are gathered from a mirror or were gathered by the layout) and
       // the rank-compacted ones (slot = rank of the key: dense ids)
