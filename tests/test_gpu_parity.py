@@ -468,3 +468,20 @@ def test_layout_built_beside_pass_one(eng, monkeypatch):
     assert (nb, it) == (nb0, it0) and bool((lab == lab0).all())
     dd.free()
 
+
+
+def test_one_barrier_kernel_all_policies_partition(eng):
+    """Every election policy through the one-barrier kernel (a thread per state and
+    grid-stride sizes) reaches the reference partition; det-min/max pass counts
+    match the oracle's."""
+    for pair in (O.random_dfa(50_000, 3, 31, 0.5), O.random_dfa(400_000, 2, 32, 0.5)):
+        d = to_dfa(pair)
+        ref = O.sort_pr(*pair)
+        for pol in (MIN, MAX, ARB):
+            r = eng.naive_pr(d, dfm.PrOptions(policy=pol))
+            assert r.stats.status == dfm.RunStatus.ok
+            assert (r.partition.block == ref.block).all(), pol
+        if pair[0].shape[1] == 50_000:
+            for pol, name in ((MIN, "min"), (MAX, "max")):
+                assert eng.naive_pr(d, dfm.PrOptions(policy=pol)).stats.iterations == \
+                    O.naive_pr(*pair, name).iterations
