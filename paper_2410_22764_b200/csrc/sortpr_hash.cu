@@ -1029,7 +1029,7 @@ bool small_timing() {
 constexpr uint64_t kSmallSeed = 0x5EED5A11ull;
 
 int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint32_t* block,
-              uint8_t* lead, uint8_t* flag, uint32_t* first2, uint32_t* canon, uint32_t& B,
+              uint8_t* lead, uint8_t* flag, uint32_t* canon, uint32_t& B,
               uint64_t& iterations) {
   const uint32_t n = d.n;
   const uint64_t cap0 = small_cap(n);
@@ -1039,6 +1039,7 @@ int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint
   auto* st = ctx.slot_t<uint32_t>("ss.state", 4);
   uint32_t* cob = ctx.slot_t<uint32_t>("ss.cob", n);
   uint32_t* cta_cnt = ctx.slot_t<uint32_t>("ss.ctacnt", grid);
+  uint32_t* cta_first = ctx.slot_t<uint32_t>("ss.ctafirst", 2ull * grid);
   uint32_t* h = reinterpret_cast<uint32_t*>(ctx.h_scalars + 24);
   h[1] = 0;
   const bool timing = small_timing();
@@ -1056,7 +1057,7 @@ int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint
     if (dl.expired()) return -1;
     SmallArgs a{d.delta, n,          d.k,     block,    lead,  flag,   t0,
                 t1,      ctr,        st,      chunk,    kSmallSeed,     per_cta,
-                tab - 1, d.acc,      first2,  first_launch, canon, cob, cta_cnt, tdbg};
+                tab - 1, d.acc,      cta_first, first_launch, canon, cob, cta_cnt, tdbg};
     first_launch = false;
     chunk = std::min<uint32_t>(4096, chunk * 2);
     void* args[] = {&a};
@@ -1369,15 +1370,17 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   const uint32_t row = k + 1 > 8 ? ((k + 1 + 7) & ~7u) : k + 1;
   uint64_t* sc = ctx.d_scalars;  // [1] fresh [2] collision [3] next active [4] accepting
   uint32_t* first2 = reinterpret_cast<uint32_t*>(ctx.d_scalars + 16);
-  DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
-  DFM_CUDA(cudaMemsetAsync(first2, 0xFF, 8, ctx.stream));
   const unsigned sgrid =
       (n <= kSmallMaxStates && !(trace && trace->on_pass) && small_enabled()) ? small_grid(ctx, n)
                                                                               : 0u;
+  if (!sgrid) {  // (the single-kernel path initialises its own state)
+    DFM_CUDA(cudaMemsetAsync(sc, 0, 40, ctx.stream));
+    DFM_CUDA(cudaMemsetAsync(first2, 0xFF, 8, ctx.stream));
+  }
   uint32_t B = 0;
   if (sgrid) {
     out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
-    const int r = run_small(ctx, d, dl, sgrid, block, lead, flag, first2, out.canon_dev, B,
+    const int r = run_small(ctx, d, dl, sgrid, block, lead, flag, out.canon_dev, B,
                             out.iterations);
     if (r < 0) {
       out.status = DFM_STATUS_TIMEOUT;

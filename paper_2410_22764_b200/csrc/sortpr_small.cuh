@@ -41,7 +41,7 @@ struct SmallArgs {
   uint32_t tab_mask;  // shared table slots - 1 (power of two >= 2 * per_cta, <= kSmallTab)
   // first launch: initial partition in the prologue (first_states/init of the host loop)
   const uint8_t* acc;
-  uint32_t* first2;  // [0] first accepting, [1] first rejecting (host-set to kNoLeader)
+  uint32_t* first2;  // [2 * grid]: each CTA's first accepting / rejecting state
   bool init;
   // fixpoint: canonical labels in the epilogue (rank of each block's leader)
   uint32_t* canon;
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
   // CTA c owns states [c * per_cta, (c + 1) * per_cta): every SM gets a share
   const uint32_t base_q = blockIdx.x * a.per_cta + threadIdx.x;
   __shared__ uint32_t s_warp[kSmallThreads / 32 + 1];
+  __shared__ uint32_t s_warp2[kSmallThreads / 32];
   __shared__ uint32_t s_base;
   __shared__ uint32_t s_cnt;  // occupied shared slots (flush list length)
   auto owned = [&](int j) { return threadIdx.x + j * kSmallThreads < a.per_cta &&
@@ -162,11 +163,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
         else fr = min(fr, q);
       }
     }
+    // per-CTA minima (no pre-initialised global cell needed), reduced after the barrier
     fa = __reduce_min_sync(0xffffffffu, fa);
     fr = __reduce_min_sync(0xffffffffu, fr);
     if (lane == 0) {
-      if (fa != kNoLeader) atomicMin(&a.first2[0], fa);
-      if (fr != kNoLeader) atomicMin(&a.first2[1], fr);
+      s_warp[threadIdx.x >> 5] = fa;
+      s_warp2[threadIdx.x >> 5] = fr;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t x = threadIdx.x < kSmallThreads / 32 ? s_warp[threadIdx.x] : kNoLeader;
+      uint32_t y = threadIdx.x < kSmallThreads / 32 ? s_warp2[threadIdx.x] : kNoLeader;
+      x = __reduce_min_sync(0xffffffffu, x);
+      y = __reduce_min_sync(0xffffffffu, y);
+      if (threadIdx.x == 0) {
+        a.first2[2 * blockIdx.x] = x;
+        a.first2[2 * blockIdx.x + 1] = y;
+      }
     }
     {
       const uint32_t cap0 = small_cap(a.n);
@@ -175,8 +188,14 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sortpr_kernel(SmallArg
       if (first < 6) a.ctr[first] = 0;
     }
     g.sync();
-    fa = __ldcg(&a.first2[0]);
-    fr = __ldcg(&a.first2[1]);
+    fa = kNoLeader;
+    fr = kNoLeader;
+    for (uint32_t c = lane; c < gridDim.x; c += 32) {
+      fa = min(fa, __ldcg(&a.first2[2 * c]));
+      fr = min(fr, __ldcg(&a.first2[2 * c + 1]));
+    }
+    fa = __reduce_min_sync(0xffffffffu, fa);
+    fr = __reduce_min_sync(0xffffffffu, fr);
     const bool split = fa != kNoLeader && fr != kNoLeader;
 #pragma unroll
     for (int j = 0; j < kSmallPer; ++j) {
