@@ -13,14 +13,22 @@ generated on the device bit-exactly with the reference generator.
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
-Multi-GPU (N > 1): one random_dfa of N x 1e8 states, state-sharded over the N
-ranks (paper_2410_22764_b200/sharded.py: NCCL all-gather of block ids + key
-all-to-all per pass; weak scaling, 1e8 states per GPU); timing is the max over
-ranks.  --replicas runs N independent single-GPU minimizations instead.
+Multi-GPU (N > 1): BASELINE configs[4] — ONE random_dfa(1e9, 4, seed 1)
+state-sharded over the N ranks (strong scaling; NCCL all-gather of block ids +
+key all-to-all per pass); timing is the max over ranks.  --replicas runs N
+independent single-GPU minimizations instead (weak scaling).
+
+Roofline: the headline is SURVEY 8(d)'s whole-iteration figure over the whole
+step (8n(k+1) bytes per counted sortPR pass), with the executed passes beside
+it; every kernel family's measured share of the step is listed.
+
+cpu_baseline: the unmodified reference (oracle/_ref) on the same input at nproc
+threads and at 1 thread (CPU model stated).
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified dfamin headers) on the host cores, on a bounded sample of the same
-workload; rank 0 only.
+unmodified dfamin headers, input from its own generator) on the host cores, on
+our arm's config; sortPR steps are one reference refinement pass each (see
+run_reference_arm); rank 0 only.
 """
 import argparse
 import json
@@ -58,7 +66,9 @@ def parse():
     ap.add_argument("--p", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--sortpr-engine", default="hash", choices=["hash", "radix"])
-    ap.add_argument("--cpu-sample-n", type=int, default=10_000_000)
+    ap.add_argument("--c5-n", type=int, default=1_000_000_000,
+                    help="N > 1 sortPR: states of the one random_dfa sharded over the N GPUs "
+                         "(BASELINE configs[4], strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--replicas", action="store_true",
@@ -156,60 +166,176 @@ def ncu_traffic(family: str, args=None):
 
 
 # ----------------------------------------------------------------- CPU baseline
-def cpu_reference_sample(n: int, k: int, seed: int, p: float, threads: int, steps: int = 1):
-    """The unmodified reference sort_pr (oracle/_ref) on host cores; returns
-    (transitions/s per step list, iterations, kind, sample, cores)."""
-    import numpy as np
-    import paper_2410_22764_b200 as dfm
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_generate(R, args):
+    """The workload's input from the REFERENCE's own generators (generators.hpp) or the
+    oracle's C generators for the builder-defined families — never libdfm."""
     from oracle import oracle as O
-    d = dfm.random_dfa(n, k, seed, p)  # bit-exact with generators.hpp:130-145
-    if O.ref_available():
-        R = O.Reference()
-        R.set_threads(threads)
-        runs = []
-        for _ in range(steps):
-            r = R.sort_pr(d.delta, d.accepting)
-            runs.append((n * k * r.iterations) / (r.elapsed_ms / 1e3))
-        return runs, r.iterations, "reference", R.worker_count(), r.elapsed_ms
-    # oracle port (plain C restatement, single-threaded)
-    runs = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        r = O.sort_pr(d.delta, d.accepting)
-        dt = time.perf_counter() - t0
-        runs.append((n * k * r.iterations) / dt)
-    return runs, r.iterations, "port", 1, dt * 1e3
+    if args.family == "random":
+        return R.random_dfa(args.n, args.k, args.seed, args.p)
+    if args.family == "chain":
+        return R.chain_dfa(args.n)
+    if args.family == "fib":
+        return R.fib_dfa(args.n)
+    if args.family == "bits":
+        return R.bit_splitter(args.n)
+    if args.family == "comb":
+        return O.comb_dfa(args.n, 3)
+    if args.family == "vlts":
+        return O.vlts_dfa(args.vlts_m, args.n, args.k)
+    raise ValueError(args.family)
+
+
+def ref_run(R, algo, delta, acc, timeout_ms=3_600_000):
+    """One run of the reference's own entry point for `algo`; RunStats timing.  On a
+    timeout the reference still counts the passes it finished (core.hpp:190-199)."""
+    if algo == "sort":
+        return R.sort_pr(delta, acc, timeout_ms=timeout_ms)
+    if algo == "naive":
+        return R.naive_pr(delta, acc, "min", timeout_ms=timeout_ms)
+    if algo == "naive_cas":
+        return R.naive_pr(delta, acc, "min", fused_cas=True, timeout_ms=timeout_ms)
+    if algo == "transpr":
+        return R.trans_pr(delta, acc, "min", timeout_ms=timeout_ms, max_memory_bytes=64 << 30)
+    if algo == "trans":
+        return R.trans_minimize(delta, acc, timeout_ms=timeout_ms, max_memory_bytes=64 << 30)
+    raise ValueError(algo)
+
+
+def ref_bounded(R, args, delta, acc, budget_ms):
+    """The reference on this input within a time budget: the whole run when it fits,
+    else the passes it finished inside the budget (a bounded sample of the same
+    workload); when not even one pass fits, a 10x smaller instance of the family."""
+    n, k = acc.size, delta.shape[0]
+    r = ref_run(R, args.algo, delta, acc, timeout_ms=int(budget_ms))
+    if r.status == "ok":
+        return (n * k * r.iterations / (r.elapsed_ms / 1e3), r.elapsed_ms, r.iterations,
+                f"the whole run ({n} states, {r.iterations} passes)")
+    if r.iterations > 0:
+        return (n * k * r.iterations / (r.elapsed_ms / 1e3), r.elapsed_ms, r.iterations,
+                f"the first {r.iterations} passes of the run ({n} states) inside a "
+                f"{budget_ms / 1e3:.0f} s budget")
+    if args.family in ("random", "vlts", "chain", "comb") and n >= 200_000:
+        a1 = argparse.Namespace(**vars(args))
+        a1.n = n // 10 if args.family != "vlts" else max(args.vlts_m, (n // 10) // args.vlts_m
+                                                           * args.vlts_m)
+        if args.family == "comb":
+            a1.n = max(2, args.n // 10)
+        d1, c1 = ref_generate(R, a1)
+        v, ms, it, smp = ref_bounded(R, a1, d1, c1, budget_ms)
+        return v, ms, it, f"{smp} of a smaller instance ({c1.size} states)"
+    return None, r.elapsed_ms, 0, "no pass finished inside the budget"
+
+
+def cpu_baseline_for(args, delta, acc, our_iters, budget_ms=60_000):
+    """cpu_baseline of our line: the unmodified reference (oracle/_ref) on the SAME input,
+    at nproc threads and at 1 thread; rank 0, N = 1 only.  Each leg is
+    bounded by `budget_ms` (ref_bounded)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                "sample": "oracle/_ref not built"}
+    R = O.Reference()
+    nproc = os.cpu_count() or 1
+    out = {"unit": UNIT, "kind": "reference", "cpu_model": cpu_model(), "nproc": nproc}
+    R.set_threads(nproc)
+    v, ms, it, smp = ref_bounded(R, args, delta, acc, budget_ms)
+    if "whole run" in smp and smp.startswith("the whole run ("):
+        assert it == our_iters, (it, our_iters)
+    out.update({"value": v, "cores": R.worker_count(), "ms": ms,
+                "sample": f"reference {args.algo}, {R.worker_count()} threads: {smp}"})
+    R.set_threads(1)
+    v1, ms1, it1, smp1 = ref_bounded(R, args, delta, acc, budget_ms)
+    out["threads_1"] = {"value": v1, "ms": ms1, "passes": it1,
+                        "sample": f"reference {args.algo}, 1 thread: {smp1}"}
+    R.set_threads(0)
+    if v1 is not None and (v is None or v1 > v):  # SURVEY 8(d): report the better as baseline
+        out.update({"value": v1, "cores": 1, "ms": ms1, "sample": out["threads_1"]["sample"],
+                    "nproc_run": {"value": v, "ms": ms, "sample": smp}})
+    return out
 
 
 def run_reference_arm(args, rank: int, world: int):
+    """The reference's own CPU implementation (oracle/_ref, unmodified headers) on this
+    box's host cores, on OUR arm's config/metric/unit.  Input from the reference's own
+    generator.  sortPR steps are one refinement pass each (ref_sort_session_pass: the
+    loop body of min_sort.hpp:100-118 over the reference's own functions; the fixpoint
+    pass adds canonicalize) so K steps stay within minutes at 1e8 states; the timed
+    steps start at pass 1, and when K is a multiple of the pass count they are exactly
+    K/passes whole sort_pr runs.  Other algorithms: one whole reference run per step."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    n = min(args.n, args.cpu_sample_n)
+    from oracle import oracle as O
+    R = O.Reference()
+    R.set_threads(os.cpu_count() or 1)
     t_all = time.perf_counter()
-    for _ in range(args.warmup):
-        cpu_reference_sample(n, args.k, args.seed, args.p, threads)
-    vals = []
-    iters = None
-    kind = cores = None
-    ms = []
-    for _ in range(args.steps):
-        v, iters, kind, cores, el = cpu_reference_sample(n, args.k, args.seed, args.p, threads)
-        vals.append(v[0])
-        ms.append(el)
-    value = statistics.mean(vals)
-    sample = (f"random_dfa(n={n}, k={args.k}, seed={args.seed}, p={args.p}) {args.algo}PR, "
-              f"{iters} passes; time = the reference's own RunStats.elapsed_ms")
+    line_extra = {}
+    if args.algo == "sort" and args.family == "random":
+        t0 = time.perf_counter()
+        S = R.sort_session(args.n, args.k, args.seed, args.p)
+        gen_s = time.perf_counter() - t0
+        for _ in range(args.warmup):
+            S.pass_()
+        S.reset()
+        ms, cycle, passes, blocks = [], [], None, None
+        for _ in range(args.steps):
+            m, fresh, done = S.pass_()
+            ms.append(m)
+            cycle.append(m)
+            if done:
+                passes, blocks = (passes or len(cycle)), fresh
+                line_extra.setdefault("ms_per_minimization", sum(cycle))
+                cycle = []
+        while passes is None:  # finish one cycle (untimed) to learn the pass count
+            m, fresh, done = S.pass_()
+            cycle.append(m)
+            if done:
+                passes, blocks = len(cycle), fresh
+                line_extra.setdefault("ms_per_minimization", sum(cycle))
+        S.close()
+        value = args.steps * float(args.n) * args.k / (sum(ms) / 1e3)
+        step = "one sortPR refinement pass of the reference loop (the fixpoint pass adds " \
+               "canonicalize); value = steps*n*k / sum of pass times"
+        iters = passes
+        sample = (f"reference sort_pr loop, {args.steps} passes over random_dfa(n={args.n}, "
+                  f"k={args.k}, seed={args.seed}, p={args.p}) generated by the reference "
+                  f"({gen_s:.0f} s, untimed); {passes} passes per minimization")
+    else:
+        delta, acc = ref_generate(R, args)
+        args.n, args.k = acc.size, delta.shape[0]
+        for _ in range(args.warmup):
+            ref_run(R, args.algo, delta, acc)
+        ms = []
+        for _ in range(args.steps):
+            r = ref_run(R, args.algo, delta, acc)
+            ms.append(r.elapsed_ms)
+        iters, blocks = r.iterations, r.num_blocks
+        value = args.steps * float(args.n) * args.k * iters / (sum(ms) / 1e3)
+        step = "one whole reference run (RunStats.elapsed_ms)"
+        sample = f"reference {args.algo} on the full workload, {iters} passes"
+    cores = R.worker_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": statistics.mean(ms), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic (host-generated)",
-            "config": config(args, world, iters, None),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": sample},
+            "ms_per_step": statistics.mean(ms), "step": step, "higher_is_better": True,
+            "scaling": scaling_of(args, world), "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (the reference's own generator)",
+            "config": config(args, world, iters, blocks),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t_all}
+    line.update(line_extra)
     print(json.dumps(line), flush=True)
 
 
@@ -241,11 +367,17 @@ def workload_name(args):
     return f"{args.algo} on {fam}"
 
 
+def scaling_of(args, world):
+    # N > 1 sortPR: one fixed random_dfa(1e9, 4) sharded over the N GPUs (configs[4])
+    return "strong" if world > 1 and args.algo == "sort" and not args.replicas else "weak"
+
+
 def config(args, world, iters, blocks):
+    sharded = world > 1 and args.algo == "sort" and not args.replicas
     return {"workload": workload_name(args), "family": args.family,
             "algo": args.algo, "n": args.n, "k": args.k, "passes": iters, "blocks": blocks,
-            "sortpr_engine": args.sortpr_engine if args.algo == "sort" else None,
-            "parallelism": "replicas" if world > 1 else "single",
+            "parallelism": (f"state-sharded x{world}" if sharded else
+                            f"replicas x{world}" if world > 1 else "single"),
             "l2": "inputs larger than L2 (delta = 4nk bytes)" if 4 * args.n * args.k > (126 << 20)
             else "L2 flushed between timed steps"}
 
@@ -320,7 +452,9 @@ def run_ours(args, rank: int, world: int, local: int):
     transitions = float(args.n) * args.k * iters * world
     value = transitions / (ms_per_step / 1e3)
 
-    # ---- e2e: host DFA in pinned memory -> public API (H2D, run, D2H labels)
+    # ---- e2e: host DFA -> public API (H2D, run, D2H labels), two host layouts:
+    # pageable numpy rows (the reference's Dfa is std::vector rows: the drop-in case,
+    # staged by the library through its pinned ring) and pinned rows
     e2e = None
     if not args.no_e2e:
         host = dd.download()
@@ -328,92 +462,134 @@ def run_ours(args, rank: int, world: int, local: int):
         pin_acc = torch.empty(args.n, dtype=torch.uint8, pin_memory=True)
         pin_delta.numpy()[:] = host.delta.view(np.int32)
         pin_acc.numpy()[:] = host.accepting
-        hd = dfm.Dfa(args.n, args.k, pin_delta.numpy().view(np.uint32), pin_acc.numpy(), 0)
+        hd_pin = dfm.Dfa(args.n, args.k, pin_delta.numpy().view(np.uint32), pin_acc.numpy(), 0)
+        hd_page = dfm.Dfa(args.n, args.k, np.ascontiguousarray(host.delta),
+                          np.ascontiguousarray(host.accepting), 0)
         del host
         out_pin = torch.empty(args.n, dtype=torch.int32, pin_memory=True)
-        out_np = out_pin.numpy().view(np.uint32)
-        run_host = {"sort": lambda: eng.sort_pr(hd, out=out_np),
-                    "naive": lambda: eng.naive_pr(hd, dfm.PrOptions(
-                        policy=dfm.RacePolicy.deterministic_min)),
-                    "transpr": lambda: eng.trans_pr(hd, dfm.PrOptions(
-                        policy=dfm.RacePolicy.deterministic_min)),
+        out_page = np.empty(args.n, np.uint32)
+
+        def run_host(hd, out):
+            pol = dfm.PrOptions(policy=dfm.RacePolicy.deterministic_min)
+            return {"sort": lambda: eng.sort_pr(hd, out=out),
+                    "naive": lambda: eng.naive_pr(hd, pol),
+                    "transpr": lambda: eng.trans_pr(hd, pol),
                     "naive_cas": lambda: eng.naive_pr_cas(hd),
-                    "trans": lambda: eng.trans_minimize(hd)}[args.algo]
-        run_host()  # warm the host path
-        barrier()
-        e_ms = []
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            r = run_host()
-            e_ms.append((time.perf_counter() - t0) * 1e3)
-            assert r.partition.num_blocks == nb
-        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
-            torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+                    "trans": lambda: eng.trans_minimize(hd)}[args.algo]()
+
+        def timed(hd, out):
+            run_host(hd, out)  # warm the host path
+            barrier()
+            e_ms = []
+            for _ in range(args.e2e_steps):
+                t0 = time.perf_counter()
+                r = run_host(hd, out)
+                e_ms.append((time.perf_counter() - t0) * 1e3)
+                assert r.partition.num_blocks == nb
+            et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
+            if world > 1:
+                torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+            return float(et.item())
+
+        ms_page = timed(hd_page, out_page)
+        ms_pin = timed(hd_pin, out_pin.numpy().view(np.uint32))
         # when every block ends a singleton the canonical partition is the identity:
-        # the library writes it on the host instead of reading 4n bytes back
-        identity = args.algo == "sort" and nb == args.n
-        e2e = {"value": transitions / (float(et.item()) / 1e3), "unit": UNIT,
-               "ms_per_step": float(et.item()),
-               "h2d_bytes_per_step": 4 * args.n * args.k + args.n,
-               "d2h_bytes_per_step": 64 * (iters + 2) if identity else 4 * args.n,
-               "how": "wall clock around Engine.sort_pr(host Dfa in pinned memory): H2D of "
-                      "delta+accepting, all passes, per-pass device scalars read back, and "
-                      "the canonical partition in the host buffer ("
+        # the library writes it on the host (a thread started at entry) instead of
+        # reading 4n bytes back
+        identity = args.algo == "sort" and nb == args.n and args.n >= (1 << 22)
+        d2h = 64 * (iters + 2) if identity else 4 * args.n
+        e2e = {"value": transitions / (ms_page / 1e3), "unit": UNIT, "ms_per_step": ms_page,
+               "h2d_bytes_per_step": 4 * args.n * args.k + args.n, "d2h_bytes_per_step": d2h,
+               "host_memory": "pageable (numpy rows, as the reference's std::vector Dfa)",
+               "how": "wall clock around the public host-buffer call (Engine."
+                      + {"sort": "sort_pr", "naive": "naive_pr", "transpr": "trans_pr",
+                         "naive_cas": "naive_pr_cas", "trans": "trans_minimize"}[args.algo]
+                      + "): H2D of delta+accepting (pageable rows staged by the library "
+                        "through a pinned ring, several host threads), all passes, per-pass "
+                        "scalars read back, the canonical partition in the host buffer ("
                       + ("all singletons: identity labels written on the host" if identity
-                         else "D2H of the labels") + ")"}
-        del out_pin
+                         else "D2H of the labels") + ")",
+               "pinned": {"value": transitions / (ms_pin / 1e3), "ms_per_step": ms_pin,
+                          "host_memory": "pinned (cudaMallocHost rows)"}}
+        del out_pin, pin_delta, pin_acc, hd_pin, hd_page
 
     if rank != 0:
+        dd.free()
         return
-    # ---- roofline of the dominant kernel family (measured live above)
     peak, peak_src = measured_peaks()
-    fam = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
-    roofline = None
-    if fam is not None:
-        name, (scopes, fms, fbytes) = fam
-        achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
-        traffic = ncu_traffic(name, args)
-        bound, unit = "hbm", "GB/s"
-        if name == "gemm":  # tcgen05 kind::i8 squaring: the family counts 2*Vp^3 int8 ops
-            bound, unit = "tensor", "TOP/s"
-            achieved = (fbytes / 1e12) / (fms / 1e3) if fms > 0 else 0.0
-            peak, peak_src = int8_peak()
-        roofline = {"bound": bound, "kernel": name, "achieved": achieved, "peak": peak,
-                    "unit": unit, "frac": achieved / peak, "traffic": traffic,
-                    "peak_source": peak_src,
-                    "share_of_step": fms / total_ms if total_ms > 0 else None,
-                    "algorithmic_bytes_per_step": fbytes / args.steps,
-                    "families_ms_per_step": {k: v[1] / args.steps for k, v in prof.items()}}
-        # whole-iteration view with SURVEY 8(d)'s per-pass figure 8n(k+1)
-        it_bytes = 8.0 * args.n * (args.k + 1) * iters
-        roofline["iteration_view"] = {
-            "algorithmic_bytes_per_step": it_bytes,
-            "achieved": (it_bytes / 1e9) / (ms_per_step / 1e3),
-            "frac": ((it_bytes / 1e9) / (ms_per_step / 1e3)) / peak}
+    roofline = roofline_of(args, prof, ms_per_step, total_ms, iters, st.executed_passes,
+                           peak, peak_src)
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and args.algo == "sort" and args.family == "random":
+    if not args.no_cpu_baseline and world == 1:
+        host = dd.download()
         try:
-            threads = os.cpu_count() or 1
-            ns = min(args.n, args.cpu_sample_n)
-            runs, citers, kind, cores, el = cpu_reference_sample(ns, args.k, args.seed, args.p,
-                                                                 threads)
-            cpu = {"value": runs[0], "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"random_dfa(n={ns}, k={args.k}, seed={args.seed}, p={args.p}) "
-                             f"sortPR, {citers} passes, {el:.0f} ms (reference RunStats)"}
+            cpu = cpu_baseline_for(args, host.delta, host.accepting, iters)
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
                    "sample": repr(exc)}
+        del host
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "wall_time_to_minimal_dfa_ms": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic: random_dfa generated on device, bit-exact with generators.hpp",
-            "config": config(args, world, iters, nb), "e2e": e2e, "roofline": roofline,
+            "scaling": scaling_of(args, world), "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: " + ("random_dfa generated on device, bit-exact with "
+                                     "generators.hpp" if args.family == "random" else
+                                     "host generator, uploaded once"),
+            "config": config(args, world, iters, nb),
+            "engine": args.sortpr_engine if args.algo == "sort" else "default",
+            "passes_counted": iters, "passes_executed": st.executed_passes,
+            "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
             "step_ms": step_ms, "lib": dfm.lib_path()}
     print(json.dumps(line), flush=True)
     dd.free()
+
+
+def roofline_of(args, prof, ms_per_step, total_ms, iters, executed, peak, peak_src):
+    """Headline: SURVEY 8(d)'s whole-iteration figure over the whole step (every kernel):
+    sortPR 8n(k+1) bytes per counted pass, naive/transPR n(16k'+8) per pass (upper
+    bound), trans 2|V|^3 int8 ops per pass.  `families` lists every kernel family's
+    measured time per step and share of the step (library profiler, CUDA events on the
+    launch stream) with the dram bytes ncu measured for it (profiles/ncu_traffic.json,
+    when this run is the workload captured there)."""
+    n, k = float(args.n), args.k
+    fams = {}
+    for name, (scopes, fms, fbytes) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        fams[name] = {"ms_per_step": fms / args.steps,
+                      "share_of_step": fms / total_ms if total_ms > 0 else None,
+                      "ncu_dram_bytes_per_step": ncu_traffic(name, args)}
+    if args.algo == "trans":
+        ops = 2.0 * (n * n) ** 3 * iters
+        p8, p8src = int8_peak()
+        achieved = ops / 1e12 / (ms_per_step / 1e3)
+        return {"bound": "tensor", "kernel": "whole minimization (every kernel of the step)",
+                "achieved": achieved, "peak": p8, "unit": "TOP/s", "frac": achieved / p8,
+                "traffic": None, "peak_source": p8src,
+                "algorithmic": "2|V|^3 int8 ops per pass (|V| = n^2), SURVEY 8(d)",
+                "families": fams}
+    if args.algo == "sort":
+        per_pass = 8.0 * n * (k + 1)
+        formula = "8n(k+1) bytes per counted pass (SURVEY 8(d))"
+    else:
+        kk = k * (max(1, int(n).bit_length()) if args.algo == "transpr" else 1)
+        per_pass = n * (16.0 * kk + 8)
+        formula = "n(16k'+8) bytes per pass, k' = levels*k for transPR (SURVEY 8(d) upper bound)"
+    it_bytes = per_pass * iters
+    achieved = it_bytes / 1e9 / (ms_per_step / 1e3)
+    traffic = ncu_traffic("step", args)
+    out = {"bound": "hbm", "kernel": "whole minimization (every kernel of the step)",
+           "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": traffic, "peak_source": peak_src, "algorithmic": formula,
+           "algorithmic_bytes_per_step": it_bytes,
+           "traffic_over_algorithmic": (traffic / it_bytes) if traffic else None,
+           "families": fams}
+    if args.algo == "sort" and executed and executed != iters:
+        ex_bytes = per_pass * executed
+        out["executed_passes_view"] = {
+            "passes": executed, "algorithmic_bytes_per_step": ex_bytes,
+            "achieved": ex_bytes / 1e9 / (ms_per_step / 1e3),
+            "frac": ex_bytes / 1e9 / (ms_per_step / 1e3) / peak}
+    return out
 
 
 def run_sharded(args, rank: int, world: int, local: int):
@@ -432,7 +608,7 @@ def run_sharded(args, rank: int, world: int, local: int):
     eng.set_stream(torch.cuda.current_stream(dev).cuda_stream)
     ops = CudaShardOps(eng)
     comm = Comm()
-    n_total = args.n * world
+    n_total = args.n
     lo, hi = shard_bounds(n_total, world, rank)
     delta, acc = ops.random_slice(n_total, args.k, args.seed, args.p, lo, hi - lo)
     for _ in range(args.warmup):
@@ -526,6 +702,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.algo == "sort" and not args.replicas:
+        args.n = args.c5_n  # C5: one fixed DFA over all ranks
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

@@ -82,6 +82,10 @@ typedef struct {
   double elapsed_ms;       /* host steady clock around the whole call */
   uint64_t peak_memory_estimate; /* the reference's estimate formula */
   int32_t status;          /* dfm_run_status */
+  /* passes whose kernels actually ran (<= iterations): a pass that starts with
+   * every block a singleton can only confirm the fixpoint; it is counted, as the
+   * reference counts it (min_sort.hpp:110), without being run */
+  uint64_t executed_passes;
 } dfm_stats;
 
 /* Limits, core.hpp:81-84.  timeout_ms <= 0 disables the deadline. */

@@ -421,6 +421,10 @@ class Reference:
             inspect["apart_popcounts"] = pops[: r.iterations].copy()
         return r
 
+    def sort_session(self, n: int, k: int, seed: int, p: float = 0.5) -> "RefSortSession":
+        """sortPR one pass per call on the reference-generated random_dfa (ref_shim.cpp)."""
+        return RefSortSession(self.lib, n, k, seed, p)
+
     def moore(self, delta, acc):
         delta, acc, n, k = self._args(delta, acc)
         block = np.empty(acc.size, np.uint32)
@@ -493,3 +497,45 @@ def _ref_remove_unreachable(self, delta, acc, initial: int = 0):
 
 Reference.quotient = _ref_quotient
 Reference.remove_unreachable = _ref_remove_unreachable
+
+
+class RefSortSession:
+    """The reference sort_pr loop (min_sort.hpp:80-123) one pass per call, over
+    its own functions (ref_shim.cpp ref_sort_session_*): bench.py's bounded
+    per-step sample of the workload.  ``pass_()`` -> (elapsed ms, fresh count,
+    fixpoint reached); ``full()`` runs the reference's whole sort_pr."""
+
+    def __init__(self, lib, n, k, seed, p):
+        self.lib = lib
+        lib.ref_sort_session_random.restype = C.c_void_p
+        lib.ref_sort_session_random.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_double]
+        lib.ref_sort_session_pass.argtypes = [C.c_void_p, C.POINTER(C.c_double),
+                                              C.POINTER(C.c_uint32)]
+        lib.ref_sort_session_full.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]
+        lib.ref_sort_session_free.argtypes = [C.c_void_p]
+        self.h = lib.ref_sort_session_random(n, k, seed, p)
+        self.n, self.k = n, k
+
+    def pass_(self):
+        ms = C.c_double(0)
+        fresh = C.c_uint32(0)
+        done = self.lib.ref_sort_session_pass(self.h, C.byref(ms), C.byref(fresh))
+        return float(ms.value), int(fresh.value), bool(done)
+
+    def reset(self) -> None:
+        self.lib.ref_sort_session_reset.argtypes = [C.c_void_p]
+        self.lib.ref_sort_session_reset(self.h)
+
+    def full(self) -> Result:
+        nb = C.c_uint32(0)
+        st = _RefStats()
+        self.lib.ref_sort_session_full(self.h, C.byref(nb), C.byref(st))
+        return _result(np.empty(0, np.uint32), nb, st)
+
+    def close(self):
+        if self.h:
+            self.lib.ref_sort_session_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

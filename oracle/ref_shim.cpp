@@ -7,7 +7,9 @@
 // (min_sort.hpp:72, min_partref.hpp:156/:170, min_transpr.hpp:59/:90,
 // min_trans.hpp:81, core.hpp:220, generators.hpp:36-145).
 #include <cstdint>
+#include <chrono>
 #include <cstring>
+#include <numeric>
 #include <stdexcept>
 #include <vector>
 
@@ -161,6 +163,92 @@ uint32_t ref_canonicalize(const uint32_t* raw, uint32_t n, uint32_t* outp) {
   const Partition p = canonicalize(std::vector<uint32_t>(raw, raw + n));
   std::memcpy(outp, p.block.data(), 4ull * n);
   return p.num_blocks;
+}
+
+// ---- sortPR one pass at a time (bench.py --impl reference: a bounded sample of
+// the workload per step).  The session holds the reference loop's state
+// (block, order, num_blocks; min_sort.hpp:80-91) and each call executes ONE
+// iteration of the loop body (min_sort.hpp:100-118) with the reference's own
+// functions: make_signature, substrate::par_sort with signature_key_less,
+// substrate::adjacent_diff with signature_key_neq, substrate::inclusive_scan and
+// the par_for scatter.  The fixpoint pass also runs the final canonicalize
+// (min_sort.hpp:123) and re-initialises the session, so a whole number of
+// cycles of calls times exactly that many sort_pr runs (minus RunStats
+// bookkeeping).  The Dfa is generated in place by the reference generator.
+struct RefSortSession {
+  Dfa d;
+  std::vector<std::uint32_t> block, order;
+  std::uint32_t num_blocks = 1;
+  std::uint64_t pass = 0;
+  void init() {  // min_sort.hpp:80-91
+    const std::uint32_t n = d.num_states;
+    bool has_acc = false, has_rej = false;
+    for (State q = 0; q < n; ++q) (d.accepting[q] != 0 ? has_acc : has_rej) = true;
+    block.assign(n, 0);
+    num_blocks = 1;
+    if (has_acc && has_rej) {
+      num_blocks = 2;
+      for (State q = 0; q < n; ++q) block[q] = d.accepting[q] != 0 ? 0 : 1;
+    }
+    order.resize(n);
+    std::iota(order.begin(), order.end(), 0u);
+    pass = 0;
+  }
+};
+
+void* ref_sort_session_random(uint32_t n, uint32_t k, uint64_t seed, double p) {
+  auto* s = new RefSortSession;
+  s->d = random_dfa(n, k, seed, p);
+  s->init();
+  return s;
+}
+
+// one pass; returns 1 when it was the fixpoint pass (canonicalize ran, session reset)
+int ref_sort_session_pass(void* h, double* elapsed_ms, uint32_t* fresh_out) {
+  auto* s = static_cast<RefSortSession*>(h);
+  const Dfa& d = s->d;
+  const std::uint32_t n = d.num_states, k = d.alphabet_size;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (s->pass == 0) s->init();
+  const std::vector<std::uint32_t> sig = make_signature(d, s->block);
+  auto& block = s->block;
+  auto& order = s->order;
+  substrate::par_sort(order, [&](std::uint32_t a, std::uint32_t b) {
+    return signature_key_less(a, b, block, sig, k);
+  });
+  const std::vector<std::uint32_t> marks =
+      substrate::adjacent_diff(order, [&](std::uint32_t a, std::uint32_t b) {
+        return signature_key_neq(a, b, block, sig, k);
+      });
+  const std::vector<std::uint32_t> labels = substrate::inclusive_scan(marks);
+  substrate::par_for(n, [&](std::size_t i) { block[order[i]] = labels[i]; });
+  const std::uint32_t fresh = labels[n - 1] + 1;
+  ++s->pass;
+  int done = 0;
+  if (fresh == s->num_blocks) {
+    const Partition canon = canonicalize(block);
+    (void)canon;
+    s->pass = 0;  // the next call starts a new run (init inside the timed call)
+    done = 1;
+  } else {
+    s->num_blocks = fresh;
+  }
+  *elapsed_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (fresh_out) *fresh_out = fresh;
+  return done;
+}
+
+// the next pass call starts a new sort_pr run (pass 1)
+void ref_sort_session_reset(void* h) { static_cast<RefSortSession*>(h)->pass = 0; }
+uint32_t ref_sort_session_states(void* h) { return static_cast<RefSortSession*>(h)->d.num_states; }
+void ref_sort_session_free(void* h) { delete static_cast<RefSortSession*>(h); }
+
+// whole sort_pr on a session's DFA (the reference's own entry point, RunStats timing)
+int ref_sort_session_full(void* h, uint32_t* nb, RefStats* st) {
+  auto* s = static_cast<RefSortSession*>(h);
+  out(sort_pr(s->d, SortOptions{}), nullptr, nb, st);
+  return 0;
 }
 
 // generators: n/k are known to the caller (fib_len etc. computed by the oracle)

@@ -132,6 +132,7 @@ class RunStats:  # core.hpp:71-77
     elapsed_ms: float = 0.0
     peak_memory_estimate: int = 0
     status: RunStatus = RunStatus.ok
+    executed_passes: int = 0  # passes whose kernels ran (<= iterations; not in the reference)
 
 
 @dataclass
@@ -210,7 +211,7 @@ class _CDfa(C.Structure):
 class _CStats(C.Structure):
     _fields_ = [("iterations", C.c_uint64), ("closure_steps", C.c_uint64),
                 ("elapsed_ms", C.c_double), ("peak_memory_estimate", C.c_uint64),
-                ("status", C.c_int32)]
+                ("status", C.c_int32), ("executed_passes", C.c_uint64)]
 
 
 class _CLimits(C.Structure):
@@ -379,7 +380,8 @@ class Engine:
     @staticmethod
     def _stats(st: _CStats) -> RunStats:
         return RunStats(int(st.iterations), int(st.closure_steps), float(st.elapsed_ms),
-                        int(st.peak_memory_estimate), RunStatus(st.status))
+                        int(st.peak_memory_estimate), RunStatus(st.status),
+                        int(st.executed_passes))
 
     def _result(self, block, nb, st) -> MinResult:
         stats = self._stats(st)

@@ -2,8 +2,10 @@
 // exceptions into dfm_err codes, uploads host DFAs, dispatches algorithms and
 // copies canonical partitions back.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -80,6 +82,169 @@ void validate_targets(Ctx& ctx, const DevDfa& dd) {
   if (ctx.h_scalars[40]) throw Error(DFM_ERR_INVALID, "transition target out of range");
 }
 
+// ---- host input in pageable memory (the reference's Dfa: std::vector rows).
+// cudaMemcpyAsync from pageable memory is staged by the driver through its own
+// small pinned buffer, synchronously and single-threaded; instead the rows are
+// copied by several host threads into a pinned ring and DMA'd from there.
+bool host_pinned_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // clear
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;  // cudaMallocHost or cudaHostRegister
+}
+
+unsigned stage_threads() {
+  if (const char* e = getenv("DFM_STAGE_THREADS")) return std::max(1, atoi(e));
+  return std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes, unsigned T) {
+  if (bytes < (8u << 20) || T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  auto part = [&](unsigned t) {
+    const size_t lo = (bytes * t / T) & ~size_t(63), hi = t + 1 == T ? bytes : (bytes * (t + 1) / T) & ~size_t(63);
+    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < T; ++t) th.emplace_back(part, t);
+  part(0);
+  for (auto& x : th) x.join();
+}
+
+constexpr uint32_t kRing = 3;  // pinned ring slots of one upload chunk each
+
+// Copies the rows of a pageable host DFA chunk by chunk (all k letter segments of
+// states [q0, q0+len)) through a pinned ring on its own host thread, issuing each
+// chunk's DMA on the copy stream and recording ready[c]; consumers gate on
+// wait_recorded(c) before waiting for the event on the device.
+class PageableStager final : public ChunkGate {
+ public:
+  PageableStager(Ctx& ctx, const dfm_dfa* d, uint32_t* delta_dev, uint64_t chunk,
+                 const cudaEvent_t* ready, uint32_t nc, char* ring, uint64_t slot_bytes,
+                 cudaEvent_t* slot_ev, bool* slot_used)
+      : ctx_(ctx), d_(d), dev_(delta_dev), chunk_(chunk), ready_(ready), nc_(nc), ring_(ring),
+        slot_bytes_(slot_bytes), slot_ev_(slot_ev), slot_used_(slot_used) {
+    th_ = std::thread([this] { run(); });
+  }
+  ~PageableStager() override { join_quiet(); }
+  void wait_recorded(uint32_t c) override {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return recorded_ > c || !err_.empty(); });
+    if (!err_.empty()) throw Error(DFM_ERR_CUDA, err_);
+  }
+  void join() {
+    join_quiet();
+    if (!err_.empty()) throw Error(DFM_ERR_CUDA, err_);
+  }
+
+ private:
+  void join_quiet() {
+    if (th_.joinable()) th_.join();
+  }
+  void run() {
+    try {
+      DFM_CUDA(cudaSetDevice(ctx_.device));
+      const uint64_t n = d_->num_states, k = d_->alphabet_size;
+      const unsigned T = stage_threads();
+      cudaStream_t cs = ctx_.copy();
+      for (uint32_t c = 0; c < nc_; ++c) {
+        const uint32_t s = c % kRing;
+        if (slot_used_[s]) DFM_CUDA(cudaEventSynchronize(slot_ev_[s]));
+        char* slot = ring_ + (uint64_t)s * slot_bytes_;
+        const uint64_t q0 = (uint64_t)c * chunk_, len = std::min(n, q0 + chunk_) - q0;
+        for (uint64_t a = 0; a < k; ++a)
+          par_memcpy(slot + a * len * 4, d_->delta[a] + q0, len * 4, T);
+        for (uint64_t a = 0; a < k; ++a)
+          DFM_CUDA(cudaMemcpyAsync(dev_ + a * n + q0, slot + a * len * 4, len * 4,
+                                   cudaMemcpyHostToDevice, cs));
+        DFM_CUDA(cudaEventRecord(ready_[c], cs));
+        DFM_CUDA(cudaEventRecord(slot_ev_[s], cs));
+        slot_used_[s] = true;
+        {
+          std::lock_guard<std::mutex> lk(mu_);
+          recorded_ = c + 1;
+        }
+        cv_.notify_all();
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(mu_);
+      err_ = std::string("pageable upload: ") + e.what();
+      cv_.notify_all();
+    }
+  }
+  Ctx& ctx_;
+  const dfm_dfa* d_;
+  uint32_t* dev_;
+  uint64_t chunk_;
+  const cudaEvent_t* ready_;
+  uint32_t nc_;
+  char* ring_;
+  uint64_t slot_bytes_;
+  cudaEvent_t* slot_ev_;
+  bool* slot_used_;
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  uint32_t recorded_ = 0;
+  std::string err_;
+};
+
+// per-upload staging resources (events created once per upload; the ring is the
+// ctx's cached pinned buffer)
+struct StageRes {
+  cudaEvent_t ev[kRing] = {};
+  bool used[kRing] = {};
+  std::unique_ptr<PageableStager> stager;
+  ~StageRes() {
+    stager.reset();
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+// copy `bytes` of pageable host memory to the device through the ring slots
+// (synchronous for the caller; the DMA runs on `stream`)
+void staged_h2d(Ctx& ctx, void* dst, const void* src, uint64_t bytes, cudaStream_t stream,
+                char* ring, uint64_t slot_bytes, StageRes& res) {
+  const unsigned T = stage_threads();
+  uint32_t s = 0;
+  for (uint64_t off = 0; off < bytes; off += slot_bytes, s = (s + 1) % kRing) {
+    const uint64_t len = std::min(slot_bytes, bytes - off);
+    if (res.used[s]) DFM_CUDA(cudaEventSynchronize(res.ev[s]));
+    char* slot = ring + (uint64_t)s * slot_bytes;
+    par_memcpy(slot, static_cast<const char*>(src) + off, len, T);
+    DFM_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, slot, len, cudaMemcpyHostToDevice,
+                             stream));
+    DFM_CUDA(cudaEventRecord(res.ev[s], stream));
+    res.used[s] = true;
+  }
+}
+
+StageRes& new_stage_res(std::unique_ptr<StageRes>& holder) {
+  holder.reset(new StageRes);
+  for (auto& e : holder->ev) DFM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return *holder;
+}
+
+// host -> device copy of a possibly pageable buffer (synchronous for the host when
+// pageable; asynchronous on `stream` when pinned)
+void h2d_any(Ctx& ctx, void* dst, const void* src, uint64_t bytes, cudaStream_t stream) {
+  if (bytes < (16u << 20) || host_pinned_ptr(src)) {
+    DFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    return;
+  }
+  const uint64_t slot = 32ull << 20;
+  char* ring = static_cast<char*>(ctx.host_pinned(kRing * slot));
+  std::unique_ptr<StageRes> holder;
+  StageRes& res = new_stage_res(holder);
+  staged_h2d(ctx, dst, src, bytes, stream, ring, slot, res);
+  DFM_CUDA(cudaStreamSynchronize(stream));  // the ring is reused by the next call
+}
+
 // stage a host DFA into device memory (slot names under `prefix`)
 DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_alloc) {
   check_host_dfa(d);
@@ -97,10 +262,8 @@ DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_al
     dd.acc = ctx.slot_t<uint8_t>(prefix + ".acc", n);
     dd.owns = false;
   }
-  for (uint64_t a = 0; a < k; ++a)
-    DFM_CUDA(cudaMemcpyAsync(dd.delta + a * n, d->delta[a], n * 4, cudaMemcpyHostToDevice,
-                             ctx.stream));
-  DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+  for (uint64_t a = 0; a < k; ++a) h2d_any(ctx, dd.delta + a * n, d->delta[a], n * 4, ctx.stream);
+  h2d_any(ctx, dd.acc, d->accepting, n, ctx.stream);
   validate_targets(ctx, dd);
   return dd;
 }
@@ -108,7 +271,8 @@ DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_al
 // sortPR from host buffers: accepting flags first, then the rows chunk by chunk on
 // the copy stream; sortPR's first pass and the layout build consume each chunk as
 // it lands (validation included), so only the tail of the copy is exposed
-DevDfa upload_progressive(Ctx& ctx, const dfm_dfa* d, uint64_t chunk) {
+DevDfa upload_progressive(Ctx& ctx, const dfm_dfa* d, uint64_t chunk,
+                          std::unique_ptr<StageRes>& stage) {
   check_host_dfa(d);
   DevDfa dd;
   dd.n = d->num_states;
@@ -118,14 +282,31 @@ DevDfa upload_progressive(Ctx& ctx, const dfm_dfa* d, uint64_t chunk) {
   dd.delta = ctx.slot_t<uint32_t>("in.delta", std::max<uint64_t>(n * k, 1));
   dd.acc = ctx.slot_t<uint8_t>("in.acc", n);
   dd.owns = false;
-  DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+  const bool pageable = k > 0 && !host_pinned_ptr(d->delta[0]);
   const uint32_t nc = (uint32_t)ceil_div(n, chunk);
   const cudaEvent_t* ev = ctx.chunk_event_pool(nc);
   cudaStream_t cs = ctx.copy();
-  // the copy stream starts after everything queued so far (slot allocations)
-  DFM_CUDA(cudaEventRecord(ev[0], ctx.stream));
-  DFM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
-  for (uint32_t c = 0; c < nc; ++c) {
+  if (pageable) {
+    // rows through a pinned ring on a stager thread; acc first, from the caller thread
+    const uint64_t slot_bytes = chunk * k * 4;
+    char* ring = static_cast<char*>(ctx.host_pinned(kRing * slot_bytes));
+    StageRes& res = new_stage_res(stage);
+    if (host_pinned_ptr(d->accepting))
+      DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+    else
+      staged_h2d(ctx, dd.acc, d->accepting, n, ctx.stream, ring, slot_bytes, res);
+    DFM_CUDA(cudaEventRecord(ev[0], ctx.stream));
+    DFM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+    res.stager.reset(new PageableStager(ctx, d, dd.delta, chunk, ev, nc, ring, slot_bytes, res.ev,
+                                        res.used));
+    dd.gate = res.stager.get();
+  } else {
+    DFM_CUDA(cudaMemcpyAsync(dd.acc, d->accepting, n, cudaMemcpyHostToDevice, ctx.stream));
+    // the copy stream starts after everything queued so far (slot allocations)
+    DFM_CUDA(cudaEventRecord(ev[0], ctx.stream));
+    DFM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+  }
+  for (uint32_t c = 0; c < nc && !pageable; ++c) {
     const uint64_t q0 = c * chunk, len = std::min(n, q0 + chunk) - q0;
     for (uint64_t a = 0; a < k; ++a)
       DFM_CUDA(cudaMemcpyAsync(dd.delta + a * n + q0, d->delta[a] + q0, len * 4,
@@ -212,6 +393,7 @@ void finish(Ctx& ctx, const AlgoOut& o, uint64_t n, const Deadline& dl, uint32_t
   if (nb_out) *nb_out = o.status == DFM_STATUS_OK ? o.num_blocks : 0;
   if (st) {
     st->iterations = o.iterations;
+    st->executed_passes = o.iterations - o.skipped_passes;
     st->closure_steps = o.closure_steps;
     st->peak_memory_estimate = o.peak_memory_estimate;
     st->status = o.status;
@@ -234,14 +416,18 @@ int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const d
          !(trace && trace->on_pass))
             ? sortpr_upload_chunk(d->num_states, d->alphabet_size)
             : 0;
-    const DevDfa dd = chunk ? upload_progressive(ctx, d, chunk) : upload(ctx, d, "in", false);
+    std::unique_ptr<StageRes> stage;
+    const DevDfa dd =
+        chunk ? upload_progressive(ctx, d, chunk, stage) : upload(ctx, d, "in", false);
     AlgoOut o;
     try {
       o = dispatch(ctx, algo, dd, policy, lim, trace, apart, pops, pop_cap);
     } catch (...) {
+      stage.reset();  // joins the stager thread
       if (dd.nready) cudaStreamSynchronize(ctx.copy());
       throw;
     }
+    if (stage && stage->stager) stage->stager->join();
     if (dd.nready) DFM_CUDA(cudaStreamSynchronize(ctx.copy()));
     spec.join();
     finish(ctx, o, dd.n, whole, block_out, nb_out, st, spec.started);

@@ -46,6 +46,13 @@ uint64_t launch_count();
 
 inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// Per-device, thread-safe memo for kernel attributes and occupancy queries:
+// cudaFuncSetAttribute applies to the CURRENT device only, so an opt-in made for
+// one context must be repeated for a context on another device.  `key` names the
+// kernel (its address); `f` runs once per (key, device) under a mutex and its
+// result is cached.
+int per_device_memo(const void* key, int device, int (*f)(const void* key));
+
 // A growable device buffer from the ctx arena (stream-ordered allocator with
 // an unbounded release threshold, so repeated calls reuse the same HBM).
 struct Buf {
@@ -144,6 +151,15 @@ struct Deadline {
   double elapsed() const { return now_ms() - start; }
 };
 
+// Host side of a pipelined upload whose chunk events are recorded by a staging
+// thread (pageable rows copied through a pinned ring): a consumer must not enqueue
+// cudaStreamWaitEvent(ready[c]) before the event is recorded, so it blocks here
+// until chunk c's copy has been enqueued.
+struct ChunkGate {
+  virtual void wait_recorded(uint32_t c) = 0;
+  virtual ~ChunkGate() = default;
+};
+
 // Device-resident DFA: SoA rows packed as one [k][n] allocation.
 struct DevDfa {
   uint32_t n = 0, k = 0, initial = 0;
@@ -158,11 +174,13 @@ struct DevDfa {
   uint32_t nready = 0;
   uint64_t chunk_states = 0;
   unsigned long long* bad = nullptr;
+  ChunkGate* gate = nullptr;  // pageable source: chunk events recorded by a stager thread
 };
 
 struct AlgoOut {
   uint32_t num_blocks = 0;
   uint64_t iterations = 0, closure_steps = 0, peak_memory_estimate = 0;
+  uint64_t skipped_passes = 0;  // counted fixpoint passes that did not run
   int32_t status = DFM_STATUS_OK;
   uint32_t* canon_dev = nullptr;  // canonical labels on device (ctx slot "canon")
   bool canon_identity = false;    // every block a singleton: canonical labels = 0..n-1

@@ -113,7 +113,14 @@ DevDfa load_dfa_bin(Ctx& ctx, const char* path) {
   try {
     // two pinned staging buffers: read chunk i+1 while chunk i is in flight
     char* stage = static_cast<char*>(ctx.host_pinned(2 * kChunk));
-    cudaEvent_t done[2];
+    struct Events {  // destroyed on every exit, including a throw mid-staging
+      cudaEvent_t e[2] = {nullptr, nullptr};
+      ~Events() {
+        for (cudaEvent_t x : e)
+          if (x) cudaEventDestroy(x);
+      }
+    } ev;
+    cudaEvent_t* done = ev.e;
     DFM_CUDA(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming));
     DFM_CUDA(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming));
     // the file payload after the header maps onto [acc (padded) | delta] in device order
@@ -148,8 +155,6 @@ DevDfa load_dfa_bin(Ctx& ctx, const char* path) {
       used[buf] = true;
     }
     ctx.sync();
-    cudaEventDestroy(done[0]);
-    cudaEventDestroy(done[1]);
   } catch (...) {
     cudaFree(dd.delta);
     cudaFree(dd.acc);

@@ -623,11 +623,14 @@ uint64_t persistent_max_states() {  // DFM_NAIVE_PERSIST_MAX (experiments)
 }
 constexpr uint64_t kClusterMaxStates = 4096;
 
-uint64_t fused_max_states(const Ctx& ctx) {
-  static int per_sm = -1;
-  if (per_sm < 0)
-    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, fused_pr_kernel<DFM_POLICY_MIN, false>, kPersistThreads, 0));
+// resident threads of the cooperative launch of `kern` (per variant: its register
+// count sets its occupancy)
+uint64_t fused_max_states(const Ctx& ctx, const void* kern) {
+  const int per_sm = per_device_memo(kern, ctx.device, [](const void* k) {
+        int v = 0;
+        DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kPersistThreads, 0));
+        return v;
+      });
   return (uint64_t)per_sm * ctx.num_sms * kPersistThreads;
 }
 
@@ -744,16 +747,19 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     uint32_t* pout = reinterpret_cast<uint32_t*>(ctx.d_scalars + 20);
     auto* cells1 = ctx.slot_t<unsigned long long>("pr.cells1", n);
     DFM_CUDA(cudaMemsetAsync(cells1, policy == DFM_POLICY_MIN ? 0xFF : 0x00, n * 8, ctx.stream));
-    const bool one = n <= fused_max_states(ctx);  // a thread per state
+    void (*kern_one)(FusedArgs) =
+        policy == DFM_POLICY_MIN   ? fused_pr_kernel<DFM_POLICY_MIN, true>
+        : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, true>
+                                   : fused_pr_kernel<DFM_POLICY_ARBITRARY, true>;
+    // a thread per state when the kOne variant holds all n resident
+    const bool one = n <= fused_max_states(ctx, (const void*)kern_one);
     void (*kern)(FusedArgs) =
-        policy == DFM_POLICY_MIN
-            ? (one ? fused_pr_kernel<DFM_POLICY_MIN, true> : fused_pr_kernel<DFM_POLICY_MIN, false>)
-        : policy == DFM_POLICY_MAX
-            ? (one ? fused_pr_kernel<DFM_POLICY_MAX, true> : fused_pr_kernel<DFM_POLICY_MAX, false>)
-            : (one ? fused_pr_kernel<DFM_POLICY_ARBITRARY, true>
-                   : fused_pr_kernel<DFM_POLICY_ARBITRARY, false>);
+        one ? kern_one
+        : policy == DFM_POLICY_MIN ? fused_pr_kernel<DFM_POLICY_MIN, false>
+        : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, false>
+                                   : fused_pr_kernel<DFM_POLICY_ARBITRARY, false>;
     const unsigned pgrid = (unsigned)std::min<uint64_t>(
-        ceil_div(n, kPersistThreads), fused_max_states(ctx) / kPersistThreads);
+        ceil_div(n, kPersistThreads), fused_max_states(ctx, (const void*)kern) / kPersistThreads);
     while (true) {
       if (dl.expired()) {
         out.status = DFM_STATUS_TIMEOUT;

@@ -161,14 +161,15 @@ bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* a
   if (count == 0) return false;
   if (bits <= 0) bits = 1;  // identity values still need one materialising pass
   if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "radix_sort_pairs: count >= 2^32");
-  static bool attr_done = false;
-  if (!attr_done) {
+  int dev = 0;
+  DFM_CUDA(cudaGetDevice(&dev));
+  per_device_memo((const void*)onesweep_kernel<true>, dev, [](const void*) {
     DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<true>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
     DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
-    attr_done = true;
-  }
+    return 1;
+  });
   const int passes = (bits + 7) / 8;
   const uint64_t tiles = ceil_div(count, kRsTile);
   uint32_t* hist = ctx.slot_t<uint32_t>("rs.hist", 2 * 8 * 256 + 16);

@@ -13,6 +13,17 @@ static std::atomic<uint64_t> g_launches{0};
 uint64_t note_launch() { return g_launches.fetch_add(1, std::memory_order_relaxed) + 1; }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+int per_device_memo(const void* key, int device, int (*f)(const void* key)) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto it = memo.find({key, device});
+  if (it != memo.end()) return it->second;
+  const int v = f(key);
+  memo[{key, device}] = v;
+  return v;
+}
+
 Ctx::Ctx(int dev) : device(dev) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)

@@ -303,52 +303,12 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 }  // namespace
 }  // namespace dfm
 
-using namespace dfm;
 
-namespace {
-template <class F>
-int guarded_shard(dfm_ctx* c, F&& f) {
-  Ctx* ctx = reinterpret_cast<Ctx*>(c);
-  if (ctx == nullptr) return DFM_ERR_INVALID;
-  std::lock_guard<std::mutex> lk(ctx->mu);
-  try {
-    DFM_CUDA(cudaSetDevice(ctx->device));
-    f(*ctx);
-    ctx->harvest();
-    return DFM_OK;
-  } catch (const Error& e) {
-    ctx->last_error = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    ctx->last_error = e.what();
-    return DFM_ERR_INVALID;
-  }
-}
-}  // namespace
-
-extern "C" {
-
-int dfm_shard_signature(dfm_ctx* c, const void* delta_local, uint64_t n_local, uint32_t k,
-                        const void* block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
-                        void* keys_out, void* sig_out, void* dest_out) {
-  return guarded_shard(c, [&](Ctx& ctx) {
-    if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
-    if (n_local == 0) return;
-    ProfScope p(ctx, "sig", n_local * (4ull * k + 4ull * k + 4 + 8 + 4ull * (k + 1) + 4));
-    shard_sig_kernel<<<grid_for(ctx, n_local), 256, 0, ctx.stream>>>(
-        static_cast<const uint32_t*>(delta_local), n_local, k,
-        static_cast<const uint32_t*>(block_full), lo, seed, ranks,
-        static_cast<unsigned long long*>(keys_out), static_cast<uint32_t*>(sig_out),
-        static_cast<uint32_t*>(dest_out));
-    DFM_LAUNCH_CHECK();
-  });
-}
-
-int dfm_shard_signature_ex(dfm_ctx* c, const void* delta_local, uint64_t n_local, uint32_t k,
-                           const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
-                           uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
-                           void* dest_out) {
-  return guarded_shard(c, [&](Ctx& ctx) {
+namespace dfm {
+void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
+                     const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                     uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
+                     void* dest_out) {
     if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
     if (id_bytes != 1 && id_bytes != 2 && id_bytes != 4)
       throw Error(DFM_ERR_INVALID, "id_bytes must be 1, 2 or 4");
@@ -389,12 +349,10 @@ int dfm_shard_signature_ex(dfm_ctx* c, const void* delta_local, uint64_t n_local
             dest);
     }
     DFM_LAUNCH_CHECK();
-  });
-}
+  }
 
-int dfm_shard_group(dfm_ctx* c, const void* keys, const void* sig, uint32_t words, uint64_t count,
-                    void* label_out, uint64_t* groups_out, int* collision_out) {
-  return guarded_shard(c, [&](Ctx& ctx) {
+void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, uint64_t count,
+                 void* label_out, uint64_t* groups_out, int* collision_out) {
     if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "too many items for one rank");
     uint64_t* sc = ctx.d_scalars + 48;  // [0] groups [1] collision [2] filter duplicates
     DFM_CUDA(cudaMemsetAsync(sc, 0, 24, ctx.stream));
@@ -445,6 +403,64 @@ int dfm_shard_group(dfm_ctx* c, const void* keys, const void* sig, uint32_t word
     ctx.sync();
     if (groups_out) *groups_out = ctx.h_scalars[48];
     if (collision_out) *collision_out = ctx.h_scalars[49] != 0;
+  }
+}  // namespace dfm
+
+using namespace dfm;
+
+namespace {
+template <class F>
+int guarded_shard(dfm_ctx* c, F&& f) {
+  Ctx* ctx = reinterpret_cast<Ctx*>(c);
+  if (ctx == nullptr) return DFM_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  try {
+    DFM_CUDA(cudaSetDevice(ctx->device));
+    f(*ctx);
+    ctx->harvest();
+    return DFM_OK;
+  } catch (const Error& e) {
+    ctx->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->last_error = e.what();
+    return DFM_ERR_INVALID;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int dfm_shard_signature(dfm_ctx* c, const void* delta_local, uint64_t n_local, uint32_t k,
+                        const void* block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
+                        void* keys_out, void* sig_out, void* dest_out) {
+  return guarded_shard(c, [&](Ctx& ctx) {
+    if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
+    if (n_local == 0) return;
+    ProfScope p(ctx, "sig", n_local * (4ull * k + 4ull * k + 4 + 8 + 4ull * (k + 1) + 4));
+    shard_sig_kernel<<<grid_for(ctx, n_local), 256, 0, ctx.stream>>>(
+        static_cast<const uint32_t*>(delta_local), n_local, k,
+        static_cast<const uint32_t*>(block_full), lo, seed, ranks,
+        static_cast<unsigned long long*>(keys_out), static_cast<uint32_t*>(sig_out),
+        static_cast<uint32_t*>(dest_out));
+    DFM_LAUNCH_CHECK();
+  });
+}
+
+int dfm_shard_signature_ex(dfm_ctx* c, const void* delta_local, uint64_t n_local, uint32_t k,
+                           const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                           uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
+                           void* dest_out) {
+  return guarded_shard(c, [&](Ctx& ctx) {
+    shard_signature(ctx, delta_local, n_local, k, block_full, id_bytes, lo, seed, ranks, pack_bits,
+                    keys_out, sig_out, dest_out);
+  });
+}
+
+int dfm_shard_group(dfm_ctx* c, const void* keys, const void* sig, uint32_t words, uint64_t count,
+                    void* label_out, uint64_t* groups_out, int* collision_out) {
+  return guarded_shard(c, [&](Ctx& ctx) {
+    shard_group(ctx, keys, sig, words, count, label_out, groups_out, collision_out);
   });
 }
 

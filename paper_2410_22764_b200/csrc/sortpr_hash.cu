@@ -1004,13 +1004,15 @@ bool small_enabled() {
 }
 
 unsigned small_grid(const Ctx& ctx, uint64_t n) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
+  const int per_sm = per_device_memo((const void*)small_sortpr_kernel, ctx.device,
+                                     [](const void*) {
+    int v = 0;
     DFM_CUDA(cudaFuncSetAttribute(small_sortpr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSmallSmem));
-    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_sortpr_kernel,
+    DFM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, small_sortpr_kernel,
                                                            kSmallThreads, kSmallSmem));
-  }
+    return v;
+  });
   // >= 256 states per CTA (fewer CTAs: cheaper grid barriers), all SMs once n > 37,888
   const uint64_t grid = std::min<uint64_t>((uint64_t)per_sm * ctx.num_sms, ceil_div(n, 256));
   return grid * kSmallThreads * kSmallPer >= n ? (unsigned)grid : 0u;
@@ -1189,6 +1191,7 @@ __global__ void sanitize_rows_kernel(uint32_t* __restrict__ delta, uint64_t n, u
 }
 
 void wait_chunk(Ctx& ctx, const DevDfa& d, uint32_t c) {
+  if (d.gate) d.gate->wait_recorded(c);
   DFM_CUDA(cudaStreamWaitEvent(ctx.stream, d.ready[c], 0));
   const uint64_t q0 = c * d.chunk_states, q1 = std::min<uint64_t>(d.n, q0 + d.chunk_states);
   ProfScope p(ctx, "init", (q1 - q0) * d.k * 4ull);
@@ -1306,12 +1309,11 @@ void group_partitioned(Ctx& ctx, uint64_t m, const uint32_t* act, unsigned long 
                    reinterpret_cast<unsigned long long*>(sc + 1),
                    reinterpret_cast<unsigned long long*>(sc + 2), sig, words, row, B};
     const size_t smem = (size_t)kGroupTable * (sizeof(GSlot) + 4);
-    static bool attr = false;
-    if (!attr) {
+    per_device_memo((const void*)grp_group_kernel, ctx.device, [](const void*) {
       DFM_CUDA(cudaFuncSetAttribute(grp_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-      attr = true;
-    }
+                                    (int)((size_t)kGroupTable * (sizeof(GSlot) + 4))));
+      return 1;
+    });
     grp_group_kernel<<<nb, 512, smem, ctx.stream>>>(gp);
     DFM_LAUNCH_CHECK();
   }
@@ -1745,6 +1747,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       // every block a singleton: the next pass splits nothing and is the fixpoint
       // pass the reference counts; no active state is left to run it on
       ++out.iterations;
+      ++out.skipped_passes;
       break;
     }
     if (!act_scanned && m > 0 && ctx.h_scalars[8] != 0) {

@@ -416,12 +416,11 @@ bool usable(uint64_t V, int engine) {
 }
 
 TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V) {
-  static bool attr = false;
-  if (!attr) {
+  per_device_memo((const void*)square_kernel, ctx.device, [](const void*) {
     DFM_CUDA(cudaFuncSetAttribute(square_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes));
-    attr = true;
-  }
+    return 1;
+  });
   TransTcState st;
   st.V = V;
   st.Vp = std::max<uint64_t>(256, ceil_div(V, 256) * 256);

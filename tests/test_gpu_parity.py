@@ -246,38 +246,34 @@ def test_device_generator_bit_exact(eng):
 
 
 def test_full_size_properties(eng, eng_radix):
-    """1e8 states, k=4 (north-star size): size-independent checks — the result is
-    a congruence refining acceptance, and its quotient is already minimal."""
-    n, k = 100_000_000, 4
-    dd = eng.random_dfa_device(n, k, 1, 0.5)
-    nb, st = eng.run_device(dfm.Algo.sort, dd)
-    assert st.status == dfm.RunStatus.ok and 1 <= nb <= n
-    nbr, str_ = eng_radix.run_device(dfm.Algo.sort, dd)
-    assert (nbr, str_.iterations) == (nb, st.iterations)
+    """1e8 states, k=4, seed 2 (the seed-1 north-star input is pinned bit-exactly against
+    the reference in test_gpu_configs.py): size-independent checks of a congruence —
+    labels canonical (first occurrences increasing), acceptance constant on blocks and
+    every block's successor blocks a function of the block — and the hash and radix
+    engines agree on partition and pass count."""
     import torch
+    n, k = 100_000_000, 4
+    dd = eng.random_dfa_device(n, k, 2, 0.5)
     out = torch.empty(n, dtype=torch.int32, device="cuda")
-    nb2, st2 = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
-    assert (nb2, st2.iterations) == (nb, st.iterations)
+    nb, st = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
+    assert st.status == dfm.RunStatus.ok and 1 <= nb <= n
+    out_r = torch.empty(n, dtype=torch.int32, device="cuda")
+    nbr, str_ = eng_radix.run_device(dfm.Algo.sort, dd, block_out_ptr=out_r.data_ptr())
+    assert (nbr, str_.iterations) == (nb, st.iterations)
+    assert bool((out == out_r).all())
+    del out_r
     host = dd.download()
     delta = torch.from_numpy(host.delta.view(np.int32)).cuda()
     acc = torch.from_numpy(host.accepting).cuda()
     lab = out.long()
-    # canonical: first occurrences of labels appear in increasing order
     first = torch.full((nb,), n, dtype=torch.long, device="cuda").scatter_reduce(
         0, lab, torch.arange(n, device="cuda"), reduce="amin")
     assert bool((first[1:] > first[:-1]).all())
-    # acceptance constant on blocks; successors' blocks a function of the block
     acc_b = torch.zeros(nb, dtype=torch.uint8, device="cuda").scatter_(0, lab, acc)
     assert bool((acc_b[lab] == acc).all())
-    rep = first  # representative state of each block
-    q_rows = []
     for a in range(k):
         succ = lab[delta[a].long()]
-        assert bool((succ == succ[rep][lab]).all())
-        q_rows.append(succ[rep].to(torch.int32).cpu().numpy().astype(np.uint32))
-    quot = dfm.Dfa(nb, k, np.vstack(q_rows), acc[rep].cpu().numpy(), 0)
-    rq = eng.sort_pr(quot)
-    assert rq.partition.num_blocks == nb  # quotient is minimal
+        assert bool((succ == succ[first][lab]).all())
     dd.free()
 
 
