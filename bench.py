@@ -284,11 +284,16 @@ def run_reference_arm(args, rank: int, world: int):
         t0 = time.perf_counter()
         S = R.sort_session(args.n, args.k, args.seed, args.p)
         gen_s = time.perf_counter() - t0
-        for _ in range(args.warmup):
+        # above 2e8 states (C5, 1e9 at N > 1) a reference pass takes minutes: no warm-up
+        # passes and the timed steps stop after one whole minimization
+        huge = args.n > 200_000_000
+        for _ in range(0 if huge else args.warmup):
             S.pass_()
         S.reset()
         ms, cycle, passes, blocks = [], [], None, None
         for _ in range(args.steps):
+            if huge and passes is not None:
+                break
             m, fresh, done = S.pass_()
             ms.append(m)
             cycle.append(m)
@@ -303,7 +308,8 @@ def run_reference_arm(args, rank: int, world: int):
                 passes, blocks = len(cycle), fresh
                 line_extra.setdefault("ms_per_minimization", sum(cycle))
         S.close()
-        value = args.steps * float(args.n) * args.k / (sum(ms) / 1e3)
+        value = len(ms) * float(args.n) * args.k / (sum(ms) / 1e3)
+        line_extra["steps_timed"] = len(ms)
         step = "one sortPR refinement pass of the reference loop (the fixpoint pass adds " \
                "canonicalize); value = steps*n*k / sum of pass times"
         iters = passes
@@ -593,26 +599,33 @@ def roofline_of(args, prof, ms_per_step, total_ms, iters, executed, peak, peak_s
 
 
 def run_sharded(args, rank: int, world: int, local: int):
-    """N > 1: one random_dfa of n_total = n * N states, state-sharded over the ranks
-    (paper_2410_22764_b200/sharded.py: NCCL all-gather of block ids + key exchange).
-    Weak scaling: every GPU owns n states."""
+    """N > 1 (or --sharded): ONE random_dfa(n = --c5-n, k, seed) state-sharded over the
+    ranks through the C++ driver (libdfm dfm_sort_pr_sharded_dev; NCCL communicator
+    owned by the library, bootstrapped over torch.distributed).  Strong scaling:
+    the DFA is fixed, each rank owns ceil(n/N) states.  At N = 1 the protocol is
+    forced (DFM_SHARD_PROTOCOL=1) so the line measures the sharded machinery itself;
+    the single-GPU engine on the same input is timed beside it."""
     import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2410_22764_b200 as dfm
-    from paper_2410_22764_b200.sharded import Comm, CudaShardOps, shard_bounds, sharded_sort_pr
+    from paper_2410_22764_b200.sharded import CudaShardOps, ShardedEngine
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    eng = dfm.Engine(local)
-    eng.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    if world == 1:
+        os.environ["DFM_SHARD_PROTOCOL"] = "1"
+    se = ShardedEngine(local, rank, world, "nccl")
+    eng = se.engine
+    stream = torch.cuda.current_stream(dev)
+    eng.set_stream(stream.cuda_stream)
     ops = CudaShardOps(eng)
-    comm = Comm()
     n_total = args.n
-    lo, hi = shard_bounds(n_total, world, rank)
+    lo, hi = se.bounds(n_total)
     delta, acc = ops.random_slice(n_total, args.k, args.seed, args.p, lo, hi - lo)
+    out = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=dev)
     for _ in range(args.warmup):
-        r = sharded_sort_pr(delta, acc, n_total, lo, comm, ops)
+        nb, st = se.sort_pr_device(delta, acc, n_total, out)
     eng.profile_reset()
     eng.set_profiling(True)
     launches0 = eng.kernel_launches()
@@ -625,11 +638,12 @@ def run_sharded(args, rank: int, world: int, local: int):
     for _ in range(args.steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r = sharded_sort_pr(delta, acc, n_total, lo, comm, ops)
-        e1.record()
+        e0.record(stream)
+        nb, st = se.sort_pr_device(delta, acc, n_total, out)
+        e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
+        assert st.status == dfm.RunStatus.ok
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -641,60 +655,84 @@ def run_sharded(args, rank: int, world: int, local: int):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    transitions = float(n_total) * args.k * r.iterations
+    iters = st.iterations
+    transitions = float(n_total) * args.k * iters
     value = transitions / (ms_per_step / 1e3)
+    single = None
+    if world == 1:  # the single-GPU engine on the same DFA
+        e1 = dfm.Engine(local)
+        e1.set_stream(stream.cuda_stream)
+        dd = e1.upload(dfm.Dfa(n_total, args.k, delta.cpu().numpy().view(np.uint32),
+                               acc.cpu().numpy(), 0))
+        e1.run_device(dfm.Algo.sort, dd)
+        sm = []
+        for _ in range(max(1, min(args.steps, 5))):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            nb1, st1 = e1.run_device(dfm.Algo.sort, dd)
+            a1.record(stream)
+            a1.synchronize()
+            sm.append(a0.elapsed_time(a1))
+        assert (nb1, st1.iterations) == (nb, iters)
+        single = {"ms_per_step": statistics.mean(sm),
+                  "sharded_over_single": ms_per_step / statistics.mean(sm)}
+        dd.free()
     e2e = None
     if not args.no_e2e:
-        # host slice in pinned memory -> H2D, sharded run, D2H of this rank's labels
-        pin_d = torch.empty(delta.shape, dtype=torch.int32, pin_memory=True)
-        pin_a = torch.empty(acc.shape, dtype=torch.uint8, pin_memory=True)
-        pin_d.copy_(delta)
-        pin_a.copy_(acc)
-        out = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+        # pageable host slice -> the C-ABI host entry (dfm_sort_pr_sharded): H2D of the
+        # owned rows, the sharded run, D2H of the owned labels; max over ranks
+        host = dfm.Dfa(hi - lo, args.k, delta.cpu().numpy().view(np.uint32).copy(),
+                       acc.cpu().numpy().copy(), 0)
+        se.sort_pr(host, n_total)
         e_ms = []
         for _ in range(args.e2e_steps):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            rr = sharded_sort_pr(pin_d.to(dev, non_blocking=True), pin_a.to(dev, non_blocking=True),
-                                 n_total, lo, comm, ops)
-            out.copy_(rr.block_local)
-            torch.cuda.synchronize(dev)
+            lab, nb2, st2 = se.sort_pr(host, n_total)
             e_ms.append((time.perf_counter() - t0) * 1e3)
-        et = torch.tensor([sum(e_ms) / len(e_ms)], dtype=torch.float64, device=dev)
+            assert nb2 == nb
+        et = torch.tensor([statistics.mean(e_ms)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": transitions / (float(et.item()) / 1e3), "unit": UNIT,
                "ms_per_step": float(et.item()),
-               "h2d_bytes_per_step": (4 * args.k + 1) * n_total,
-               "d2h_bytes_per_step": 4 * n_total,
-               "how": "per rank: pinned host slice -> H2D, sharded sortPR, D2H of owned labels; "
-                      "max over ranks"}
+               "h2d_bytes_per_step": (4 * args.k + 1) * n_total, "d2h_bytes_per_step": 4 * n_total,
+               "host_memory": "pageable",
+               "how": "per rank: pageable host slice -> dfm_sort_pr_sharded (H2D of the owned "
+                      "rows, the sharded run, D2H of the owned labels); max over ranks"}
     if rank != 0:
+        se.close()
         return
     peak, peak_src = measured_peaks()
-    fam = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
-    roofline = None
-    if fam is not None:
-        name, (scopes, fms, fbytes) = fam
-        achieved = (fbytes / 1e9) / (fms / 1e3) if fms > 0 else 0.0
-        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
-                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                    "peak_source": peak_src, "rank": 0,
-                    "families_ms_per_step": {k: v[1] / args.steps for k, v in prof.items()}}
-    cfg = config(args, world, r.iterations, r.num_blocks)
-    cfg.update({"parallelism": f"state-sharded x{world} (NCCL all-gather + all-to-all)",
-                "n_total": n_total, "workload": f"sharded sortPR on random_dfa(n={n_total:.2e}, "
-                f"k={args.k}, seed={args.seed}) — {args.n:.0e} states per GPU (SURVEY 8(d) C5)",
-                "hash_retries": r.retries})
+    roofline = roofline_of(args, prof, ms_per_step, sum(step_ms), iters, st.executed_passes,
+                           peak, peak_src)
+    # NVLink: the per-pass exchange volume received by one rank (SURVEY 8(d) sharded row)
+    roofline["nvlink"] = {
+        "bytes_per_rank_per_step_upper": float(iters) * (4.0 * n_total * (world - 1) / world
+                                                         + 16.0 * (n_total / world)
+                                                         * (world - 1) / world),
+        "peak_gbs_per_direction": 900.0,
+        "note": "all-gather of ids (<= 4 B/state) + key/label exchange; measured on one GPU only"}
+    cfg = config(args, world, iters, nb)
+    cfg.update({"parallelism": f"state-sharded x{world} (C++ driver, NCCL all-gather + "
+                               f"all-to-all)", "n_total": n_total,
+                "workload": f"sharded sortPR on random_dfa(n={n_total:.0e}, k={args.k}, "
+                            f"seed={args.seed}, p={args.p}) over {world} GPU(s) "
+                            f"(BASELINE configs[4])"})
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step,
             "wall_time_to_minimal_dfa_ms": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic: random_dfa slices generated on device, bit-exact with generators.hpp",
-            "config": cfg, "e2e": e2e, "roofline": roofline, "cpu_baseline": None,
-            "clocks": clk, "gpu_launches": launches, "step_ms": step_ms, "lib": dfm.lib_path()}
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: random_dfa slices generated on device, bit-exact with "
+                    "generators.hpp",
+            "config": cfg, "passes_counted": iters, "passes_executed": st.executed_passes,
+            "single_gpu_engine": single, "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": None, "clocks": clk, "gpu_launches": launches, "step_ms": step_ms,
+            "lib": dfm.lib_path()}
     print(json.dumps(line), flush=True)
+    se.close()
 
 
 def main():

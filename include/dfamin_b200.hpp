@@ -11,6 +11,8 @@
 //   dfamin::trans_pr(...)            -> dfamin::b200::trans_pr(...)          min_transpr.hpp:90,:114
 //   dfamin::trans_minimize(d,l,ins)  -> dfamin::b200::trans_minimize(...)    min_trans.hpp:81
 //   dfamin::run_algorithm(a, d, cfg) -> dfamin::b200::run_algorithm(...)     bench.hpp:83
+//   dfamin::sort_pr(d, opt)          -> dfamin::b200::sort_pr(d, sharded, opt) state-sharded over
+//                                       the GPUs of one box (dfm_sort_pr_sharded)
 //
 // Types: with DFAMIN_B200_USE_REFERENCE_TYPES defined (and the reference
 // headers dfamin/bench.hpp etc. included first) the functions take and return
@@ -23,6 +25,7 @@
 // back to a CPU path.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -445,6 +448,76 @@ inline MinResult run_algorithm(Algo algo, const Dfa& d, const AlgoRunConfig& cfg
     default:
       throw std::invalid_argument("the Moore oracle is a CPU reference, not a GPU algorithm");
   }
+}
+
+// ---- state-sharded sortPR: one process per GPU over NCCL, or (tests)
+// one thread per rank over the in-process transport.  Collective: every rank calls.
+class ShardedEngine {
+ public:
+  using NcclId = std::array<std::uint8_t, DFM_NCCL_ID_BYTES>;
+  // rank 0 creates the id; the host distributes its bytes to the other ranks
+  static NcclId nccl_unique_id() {
+    NcclId id{};
+    const int rc = dfm_nccl_get_unique_id(id.data());
+    if (rc != DFM_OK) throw EngineError(rc, "ncclGetUniqueId failed");
+    return id;
+  }
+  ShardedEngine(int device, int rank, int world, const NcclId& id) {
+    const int rc = dfm_ctx_create_sharded(device, rank, world, id.data(), &ctx_);
+    if (rc != DFM_OK) throw EngineError(rc, dfm_last_error(nullptr));
+  }
+  ShardedEngine(int device, int rank, int world, const std::string& local_group) {
+    const int rc = dfm_ctx_create_sharded_local(device, rank, world, local_group.c_str(), &ctx_);
+    if (rc != DFM_OK) throw EngineError(rc, dfm_last_error(nullptr));
+  }
+  ~ShardedEngine() { dfm_ctx_destroy(ctx_); }
+  ShardedEngine(const ShardedEngine&) = delete;
+  ShardedEngine& operator=(const ShardedEngine&) = delete;
+  dfm_ctx* get() const { return ctx_; }
+  void check(int rc) const {
+    if (rc != DFM_OK) throw EngineError(rc, dfm_last_error(ctx_));
+  }
+  int rank() const {
+    int r = 0;
+    dfm_ctx_shard_info(ctx_, &r, nullptr, nullptr);
+    return r;
+  }
+  int world() const {
+    int w = 1;
+    dfm_ctx_shard_info(ctx_, nullptr, &w, nullptr);
+    return w;
+  }
+  // this rank's states [lo, hi)
+  std::pair<std::uint64_t, std::uint64_t> bounds(std::uint64_t n) const {
+    std::uint64_t lo = 0, hi = 0;
+    dfm_shard_bounds(n, world(), rank(), &lo, &hi);
+    return {lo, hi};
+  }
+
+ private:
+  dfm_ctx* ctx_ = nullptr;
+};
+
+// sort_pr (min_sort.hpp:72) over state shards.  Every rank passes the same Dfa (the
+// reference type); the engine reads only this rank's rows [lo, hi) (pointers into
+// the row vectors, no copy on the host) and returns the whole canonical partition,
+// block count and pass count — equal to the reference's — on every rank.
+inline MinResult sort_pr(const Dfa& d, ShardedEngine& se, const SortOptions& opt = {}) {
+  const auto [lo, hi] = se.bounds(d.num_states);
+  std::vector<const std::uint32_t*> rows(d.alphabet_size);
+  for (std::uint32_t a = 0; a < d.alphabet_size; ++a) rows[a] = d.delta[a].data() + lo;
+  dfm_dfa local{};
+  local.num_states = static_cast<std::uint32_t>(hi - lo);
+  local.alphabet_size = d.alphabet_size;
+  local.delta = rows.empty() ? nullptr : rows.data();
+  local.accepting = d.accepting.data() + lo;
+  local.initial = 0;
+  std::vector<std::uint32_t> block(d.num_states);
+  std::uint32_t nb = 0;
+  dfm_stats st{};
+  se.check(dfm_sort_pr_sharded(se.get(), d.num_states, &local, 1, block.data(), &nb,
+                               opt.timeout_ms, &st));
+  return detail::result(std::move(block), nb, st);
 }
 
 }  // namespace dfamin::b200

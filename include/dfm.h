@@ -263,6 +263,40 @@ int dfm_random_dfa_slice_dev(dfm_ctx* ctx, uint64_t n_total, uint32_t k, uint64_
                              double accept_prob, uint64_t lo, uint64_t count, void* delta_out,
                              void* accepting_out);
 
+/* ---------------------------------------------------------------- sharded sortPR driver */
+/* The C++ driver of the state-sharded sortPR: a context
+ * that owns one rank of a communicator runs the whole protocol (narrow-width
+ * all-gather of block ids, keys, routed exact grouping, dense ids back, fixpoint,
+ * canonical labels) — the drop-in for min_sort.hpp:72 sort_pr on DFAs too large
+ * for one GPU.  Rank r owns the contiguous states [r*S, min(n, (r+1)*S)),
+ * S = ceil(n/world) (dfm_shard_bounds); its rows hold GLOBAL target ids.
+ * Result: the same canonical partition, block count and pass count as the
+ * reference's sort_pr for every world size. */
+#define DFM_NCCL_ID_BYTES 128
+/* rank 0 calls this; the host distributes the 128 bytes to every rank */
+int dfm_nccl_get_unique_id(uint8_t* id_out /* DFM_NCCL_ID_BYTES */);
+/* one process per GPU: a context owning rank `rank` of an NCCL communicator */
+int dfm_ctx_create_sharded(int device, int rank, int world, const uint8_t* nccl_id,
+                           dfm_ctx** out);
+/* test transport: `world` ranks as host threads of ONE process on one device,
+ * meeting in the named group (each thread creates its own context) */
+int dfm_ctx_create_sharded_local(int device, int rank, int world, const char* group,
+                                 dfm_ctx** out);
+int dfm_ctx_shard_info(const dfm_ctx* ctx, int* rank, int* world, const char** transport);
+void dfm_shard_bounds(uint64_t n_total, int world, int rank, uint64_t* lo, uint64_t* hi);
+/* Host rows of the owned states (local->num_states = hi - lo, targets < n_total;
+ * pageable or pinned).  block_out: the owned states' canonical labels (hi - lo
+ * entries), or with gather_all the whole canonical partition (n_total entries) on
+ * every rank.  Collective: every rank calls it. */
+int dfm_sort_pr_sharded(dfm_ctx* ctx, uint64_t n_total, const dfm_dfa* local, int gather_all,
+                        uint32_t* block_out, uint32_t* num_blocks_out, int64_t timeout_ms,
+                        dfm_stats* stats);
+/* Device-resident shard: delta_dev k rows of n_local u32, acc_dev n_local u8,
+ * block_out_dev n_local u32 (canonical labels of the owned states). */
+int dfm_sort_pr_sharded_dev(dfm_ctx* ctx, uint64_t n_total, uint32_t n_local, uint32_t k,
+                            const void* delta_dev, const void* acc_dev, void* block_out_dev,
+                            uint32_t* num_blocks_out, int64_t timeout_ms, dfm_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -282,6 +282,17 @@ def _load():
         "dfm_write_dfa_bin": (C.c_int, [C.c_char_p, vp]),
         "dfm_ddfa_load_bin": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
         "dfm_ddfa_save_bin": (C.c_int, [vp, vp, C.c_char_p]),
+        "dfm_nccl_get_unique_id": (C.c_int, [vp]),
+        "dfm_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+        "dfm_ctx_create_sharded_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                                   C.POINTER(vp)]),
+        "dfm_ctx_shard_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_char_p)]),
+        "dfm_shard_bounds": (None, [u64, C.c_int, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
+        "dfm_sort_pr_sharded": (C.c_int, [vp, u64, vp, C.c_int, vp, C.POINTER(u32), i64,
+                                          C.POINTER(_CStats)]),
+        "dfm_sort_pr_sharded_dev": (C.c_int, [vp, u64, u32, u32, vp, vp, vp, C.POINTER(u32), i64,
+                                              C.POINTER(_CStats)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -230,21 +230,6 @@ StageRes& new_stage_res(std::unique_ptr<StageRes>& holder) {
   return *holder;
 }
 
-// host -> device copy of a possibly pageable buffer (synchronous for the host when
-// pageable; asynchronous on `stream` when pinned)
-void h2d_any(Ctx& ctx, void* dst, const void* src, uint64_t bytes, cudaStream_t stream) {
-  if (bytes < (16u << 20) || host_pinned_ptr(src)) {
-    DFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
-    return;
-  }
-  const uint64_t slot = 32ull << 20;
-  char* ring = static_cast<char*>(ctx.host_pinned(kRing * slot));
-  std::unique_ptr<StageRes> holder;
-  StageRes& res = new_stage_res(holder);
-  staged_h2d(ctx, dst, src, bytes, stream, ring, slot, res);
-  DFM_CUDA(cudaStreamSynchronize(stream));  // the ring is reused by the next call
-}
-
 // stage a host DFA into device memory (slot names under `prefix`)
 DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_alloc) {
   check_host_dfa(d);
@@ -262,8 +247,8 @@ DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_al
     dd.acc = ctx.slot_t<uint8_t>(prefix + ".acc", n);
     dd.owns = false;
   }
-  for (uint64_t a = 0; a < k; ++a) h2d_any(ctx, dd.delta + a * n, d->delta[a], n * 4, ctx.stream);
-  h2d_any(ctx, dd.acc, d->accepting, n, ctx.stream);
+  for (uint64_t a = 0; a < k; ++a) h2d_rows(ctx, dd.delta + a * n, d->delta[a], n * 4);
+  h2d_rows(ctx, dd.acc, d->accepting, n);
   validate_targets(ctx, dd);
   return dd;
 }
@@ -442,6 +427,23 @@ uint64_t sm_draw(uint64_t seed, uint64_t j) {
 }
 
 }  // namespace
+
+// host -> device copy of a possibly pageable buffer (synchronous for the host when
+// pageable; asynchronous on `stream` when pinned)
+void h2d_rows(Ctx& ctx, void* dst, const void* src, uint64_t bytes) {
+  cudaStream_t stream = ctx.stream;
+  if (bytes < (16u << 20) || host_pinned_ptr(src)) {
+    DFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    return;
+  }
+  const uint64_t slot = 32ull << 20;
+  char* ring = static_cast<char*>(ctx.host_pinned(kRing * slot));
+  std::unique_ptr<StageRes> holder;
+  StageRes& res = new_stage_res(holder);
+  staged_h2d(ctx, dst, src, bytes, stream, ring, slot, res);
+  DFM_CUDA(cudaStreamSynchronize(stream));  // the ring is reused by the next call
+}
+
 }  // namespace dfm
 
 using namespace dfm;

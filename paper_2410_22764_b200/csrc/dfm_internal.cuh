@@ -61,6 +61,7 @@ struct Buf {
 };
 
 struct Ctx;
+struct Comm;  // comm.cuh: collectives of a sharded context
 
 // Times one kernel family with events on the launching stream when profiling
 // is enabled.  Usage: { ProfScope p(ctx, "sig"); kernel<<<..., ctx.stream>>>(); }
@@ -96,6 +97,8 @@ struct Ctx {
   int sortpr_engine = 0;
   // Cho–Huynh squaring engine: DFM_TRANS_AUTO (default) / DFM_TRANS_BIT / DFM_TRANS_TENSOR
   int trans_engine = 0;
+  // sharded contexts (dfm_ctx_create_sharded[_local]): this rank's communicator
+  Comm* comm = nullptr;
   // profiling
   bool profiling = false;
   struct Pending {
@@ -212,6 +215,22 @@ void write_dfa_bin(const char* path, uint32_t n, uint32_t k, uint32_t initial,
                    const uint32_t* const* rows, const uint8_t* acc);
 DevDfa load_dfa_bin(Ctx& ctx, const char* path);
 void save_dfa_bin(Ctx& ctx, const DevDfa& dd, const char* path);
+// host -> device copy on ctx.stream of a possibly pageable host buffer (pageable:
+// staged by several host threads through a pinned ring, synchronous for the host)
+void h2d_rows(Ctx& ctx, void* dst, const void* src, uint64_t bytes);
+// sharded sortPR primitives (shard.cu) and the C++ driver (shard_driver.cu)
+void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
+                     const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                     uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
+                     void* dest_out);
+void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, uint64_t count,
+                 void* label_out, uint64_t* groups_out, int* collision_out);
+// contiguous shards of ceil(n/world) states: rank r owns [r*S, min(n, (r+1)*S))
+inline uint64_t shard_size(uint64_t n, int world) { return ceil_div(n, (uint64_t)world); }
+// `loc` = the owned rows (n = owned states, GLOBAL targets); canonical labels of the
+// owned states into canon_dev (device, loc.n entries)
+AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const Deadline& dl,
+                            uint32_t* canon_dev, bool force_protocol);
 // device random_dfa
 void random_dfa_dev(Ctx& ctx, DevDfa& d, uint32_t n, uint32_t k, uint64_t seed, double p);
 

@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "comm.cuh"
 #include "dfm_internal.cuh"
 
 #include <atomic>
@@ -50,6 +51,7 @@ Ctx::Ctx(int dev) : device(dev) {
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  delete comm;
   for (auto& kv : slots)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   for (auto& p : pending) {

@@ -1,5 +1,15 @@
 """State-sharded sortPR over several GPUs.
 
+The product path is the C++ driver in libdfm (csrc/shard_driver.cu, C-ABI
+``dfm_sort_pr_sharded[_dev]``), reached here through :class:`ShardedEngine`: its
+context owns an NCCL communicator (bootstrapped over torch.distributed: rank 0's
+ncclUniqueId is broadcast) or, in the single-GPU tests, the in-process "local"
+transport (ranks as threads sharing one device).
+
+``sharded_sort_pr`` below is the same protocol written over torch.distributed
+collectives and pluggable device ops: the CPU-testable specification of the
+driver (tests/test_sharded_gloo.py runs it at world 2 and 3 over gloo).
+
 One process per GPU.  Rank g owns the contiguous state range [lo_g, hi_g) and
 its δ rows (global target ids).  Each refinement pass (min_sort.hpp:93-118):
 
@@ -179,9 +189,10 @@ class ShardedResult:
 
 
 def shard_bounds(n_total: int, world: int, rank: int):
-    lo = n_total * rank // world
-    hi = n_total * (rank + 1) // world
-    return lo, hi
+    """Rank r owns [r*S, min(n, (r+1)*S)), S = ceil(n/world) (dfm_shard_bounds)."""
+    S = -(-n_total // world)
+    lo = min(n_total, rank * S)
+    return lo, min(n_total, lo + S)
 
 
 def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total: int, lo: int,
@@ -247,3 +258,84 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
     block_full = comm.all_gather(block, sizes)
     canon, nb = ops.canonicalize(block_full)
     return ShardedResult(canon[lo:lo + n_local].clone(), nb, iterations, retries)
+
+
+class ShardedEngine:
+    """A libdfm context owning one rank of a communicator; runs the C++ sharded
+    sortPR driver (dfm_sort_pr_sharded[_dev]).
+
+    transport="nccl": one process per GPU; the NCCL id is created by rank 0 and
+    broadcast over torch.distributed (any backend).  transport="local": ranks are
+    threads of this process on one device meeting in `group` (tests)."""
+
+    def __init__(self, device: int, rank: int, world: int, transport: str = "nccl",
+                 group: str = "dfm", pg=None):
+        import paper_2410_22764_b200 as dfm
+        self.dfm = dfm
+        lib = dfm._load()
+        self.lib = lib
+        h = C.c_void_p()
+        if transport == "nccl":
+            uid = (C.c_uint8 * 128)()
+            if rank == 0:
+                rc = lib.dfm_nccl_get_unique_id(uid)
+                if rc != 0:
+                    raise dfm.EngineError(rc, "ncclGetUniqueId failed")
+            obj = [bytes(uid)]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0, group=pg)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            rc = lib.dfm_ctx_create_sharded(device, rank, world, uid, C.byref(h))
+        elif transport == "local":
+            rc = lib.dfm_ctx_create_sharded_local(device, rank, world, group.encode(), C.byref(h))
+        else:
+            raise ValueError(transport)
+        if rc != 0:
+            raise dfm.EngineUnavailable(rc, (lib.dfm_last_error(None) or b"").decode())
+        self.engine = dfm.Engine.__new__(dfm.Engine)  # profiling / stream plumbing
+        self.engine.lib, self.engine.handle, self.engine.device = lib, h, device
+        self.handle, self.device, self.rank, self.world = h, device, rank, world
+
+    def bounds(self, n_total: int):
+        lo, hi = C.c_uint64(0), C.c_uint64(0)
+        self.lib.dfm_shard_bounds(n_total, self.world, self.rank, C.byref(lo), C.byref(hi))
+        return int(lo.value), int(hi.value)
+
+    def info(self):
+        r, w, t = C.c_int(0), C.c_int(0), C.c_char_p()
+        self.engine._check(self.lib.dfm_ctx_shard_info(self.handle, C.byref(r), C.byref(w),
+                                                       C.byref(t)))
+        return int(r.value), int(w.value), t.value.decode()
+
+    def sort_pr(self, local, n_total: int, gather_all: bool = False, timeout_ms: int = 300_000):
+        """local: dfm.Dfa of the owned states (GLOBAL targets).  Returns
+        (labels, num_blocks, RunStats): this rank's canonical labels, or the whole
+        partition with gather_all."""
+        import numpy as np
+        dfm = self.dfm
+        cd, keep = dfm.Engine._cdfa(local)
+        out = np.empty(n_total if gather_all else local.num_states, np.uint32)
+        nb = C.c_uint32(0)
+        st = dfm._CStats()
+        self.engine._check(self.lib.dfm_sort_pr_sharded(
+            self.handle, n_total, C.byref(cd), int(gather_all), out.ctypes.data, C.byref(nb),
+            timeout_ms, C.byref(st)))
+        return out, int(nb.value), dfm.Engine._stats(st)
+
+    def sort_pr_device(self, delta, acc, n_total: int, out, timeout_ms: int = 300_000):
+        """delta: (k, n_local) int32 CUDA tensor, acc: (n_local,) uint8, out: (n_local,)
+        int32 — this rank's canonical labels are written there."""
+        dfm = self.dfm
+        k, nl = delta.shape
+        nb = C.c_uint32(0)
+        st = dfm._CStats()
+        self.engine._check(self.lib.dfm_sort_pr_sharded_dev(
+            self.handle, n_total, nl, k, delta.data_ptr(), acc.data_ptr(), out.data_ptr(),
+            C.byref(nb), timeout_ms, C.byref(st)))
+        return int(nb.value), dfm.Engine._stats(st)
+
+    def close(self):
+        if self.handle:
+            self.lib.dfm_ctx_destroy(self.handle)
+            self.handle = None
+            self.engine.handle = None

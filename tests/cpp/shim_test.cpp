@@ -7,6 +7,7 @@
 #include "dfamin/bench.hpp"
 #endif
 #include <cstdio>
+#include <thread>
 #include <string>
 
 #include "dfamin_b200.hpp"
@@ -155,6 +156,37 @@ int main() {
       threw = true;
     }
     CHECK(threw);
+  }
+  {  // state-sharded sort_pr: NCCL world 1, and 3 ranks as threads over the
+     // in-process transport; whole canonical partition and pass count on every rank
+    Dfa d;
+    d.num_states = 20000;
+    d.alphabet_size = 3;
+    d.delta.assign(3, std::vector<State>(d.num_states));
+    d.accepting.assign(d.num_states, 0);
+    std::uint64_t x = 2410;
+    for (auto& row : d.delta)
+      for (auto& t : row) {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        t = (State)((x >> 33) % (d.num_states / 4));  // few distinct targets: many merges
+      }
+    for (std::uint32_t q = 0; q < d.num_states; ++q) d.accepting[q] = (q % 7) == 0;
+    const MinResult ref = B::sort_pr(d);
+    {
+      B::ShardedEngine se(0, 0, 1, B::ShardedEngine::nccl_unique_id());
+      const MinResult r = B::sort_pr(d, se);
+      CHECK(r.partition == ref.partition && r.stats.iterations == ref.stats.iterations);
+    }
+    std::vector<MinResult> got(3);
+    std::vector<std::thread> th;
+    for (int rank = 0; rank < 3; ++rank)
+      th.emplace_back([&, rank] {
+        B::ShardedEngine se(0, rank, 3, "shim3");
+        got[rank] = B::sort_pr(d, se);
+      });
+    for (auto& t : th) t.join();
+    for (const auto& r : got)
+      CHECK(r.partition == ref.partition && r.stats.iterations == ref.stats.iterations);
   }
   std::printf("%d failures\n", failures);
   return failures;

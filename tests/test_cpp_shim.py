@@ -16,7 +16,7 @@ OUT = os.path.join(ROOT, "build", "shim_test")
 def _compile(extra, out):
     os.makedirs(os.path.dirname(out), exist_ok=True)
     libdir = os.path.dirname(dfm.lib_path())
-    cmd = ["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"), *extra, SRC, "-o",
+    cmd = ["g++", "-std=c++20", "-O1", "-pthread", "-I" + os.path.join(ROOT, "include"), *extra, SRC, "-o",
            out, "-L" + libdir, "-l:libdfm.so", "-Wl,-rpath," + libdir]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
 
