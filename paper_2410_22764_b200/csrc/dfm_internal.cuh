@@ -225,6 +225,9 @@ void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32
                      void* dest_out);
 void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, uint64_t count,
                  void* label_out, uint64_t* groups_out, int* collision_out);
+// exact packed keys (+1) from a key space of 2^key_bits: presence bitmap + rank
+void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key_bits,
+                        void* label_out, uint64_t* groups_out);
 // contiguous shards of ceil(n/world) states: rank r owns [r*S, min(n, (r+1)*S))
 inline uint64_t shard_size(uint64_t n, int world) { return ceil_div(n, (uint64_t)world); }
 // `loc` = the owned rows (n = owned states, GLOBAL targets); canonical labels of the

@@ -295,6 +295,43 @@ __global__ void random_slice_kernel(uint32_t* __restrict__ delta, uint8_t* __res
   }
 }
 
+// Direct grouping of exact packed keys from a small key space (2^bits keys): a
+// presence bitmap (L2-resident) and the key's rank among the present keys as its
+// dense group id — one atomic per warp-distinct key, no table, no probing.
+__global__ void __launch_bounds__(256) direct_set_kernel(const unsigned long long* __restrict__ keys,
+                                                         uint64_t count, uint32_t* bits) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t key = keys[i] - 1;  // packed keys are stored + 1
+    const uint32_t peers = __match_any_sync(__activemask(), key);
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+      const uint32_t m = 1u << (key & 31);
+      if ((bits[key >> 5] & m) == 0) atomicOr(&bits[key >> 5], m);
+    }
+  }
+}
+
+struct DirPopIn {
+  const uint32_t* bits;
+  __device__ uint32_t operator()(uint64_t w) const { return __popc(bits[w]); }
+};
+struct DirPopOut {
+  uint32_t* prefix;
+  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { prefix[w] = excl; }
+};
+
+__global__ void __launch_bounds__(256) direct_label_kernel(const unsigned long long* __restrict__ keys,
+                                                           uint64_t count,
+                                                           const uint32_t* __restrict__ bits,
+                                                           const uint32_t* __restrict__ prefix,
+                                                           uint32_t* __restrict__ label) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t key = keys[i] - 1;
+    label[i] = prefix[key >> 5] + __popc(bits[key >> 5] & ((1u << (key & 31)) - 1u));
+  }
+}
+
 unsigned grid_for(const Ctx& ctx, uint64_t items) {
   return (unsigned)std::min<uint64_t>(ceil_div(std::max<uint64_t>(items, 1), 256),
                                       (uint64_t)ctx.num_sms * 16);
@@ -350,6 +387,32 @@ void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32
     }
     DFM_LAUNCH_CHECK();
   }
+
+void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key_bits,
+                        void* label_out, uint64_t* groups_out) {
+  if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "too many items for one rank");
+  if (key_bits > 32) throw Error(DFM_ERR_INVALID, "direct grouping needs <= 32 key bits");
+  const uint64_t words = ceil_div(1ull << key_bits, 32);
+  uint32_t* bits = ctx.slot_t<uint32_t>("shard.dbits", words);
+  uint32_t* prefix = ctx.slot_t<uint32_t>("shard.dpref", words);
+  uint64_t* total = ctx.d_scalars + 48;
+  ProfScope p(ctx, "group", count * 16ull + words * 12);
+  DFM_CUDA(cudaMemsetAsync(bits, 0, words * 4, ctx.stream));
+  const auto* k = static_cast<const unsigned long long*>(keys);
+  if (count) {
+    direct_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(k, count, bits);
+    DFM_LAUNCH_CHECK();
+  }
+  prims::lookback_scan(ctx, "shard.dscan", words, DirPopIn{bits}, DirPopOut{prefix}, total);
+  if (count) {
+    direct_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+        k, count, bits, prefix, static_cast<uint32_t*>(label_out));
+    DFM_LAUNCH_CHECK();
+  }
+  DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 48, total, 8, cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  if (groups_out) *groups_out = ctx.h_scalars[48];
+}
 
 void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, uint64_t count,
                  void* label_out, uint64_t* groups_out, int* collision_out) {

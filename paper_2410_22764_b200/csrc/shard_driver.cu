@@ -328,7 +328,11 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
     uint32_t* label = ctx.slot_t<uint32_t>("sd.label", std::max<uint64_t>(nrecv, 1));
     uint64_t groups = 0;
     int coll = 0;
-    shard_group(ctx, rkeys, rsig, words, nrecv, label, &groups, &coll);
+    const uint64_t kbits = (uint64_t)(k + 1) * w;
+    if (packed && kbits <= 30 && (1ull << kbits) <= std::max<uint64_t>(16 * nrecv, 1ull << 20))
+      shard_group_direct(ctx, rkeys, nrecv, (uint32_t)kbits, label, &groups);
+    else
+      shard_group(ctx, rkeys, rsig, words, nrecv, label, &groups, &coll);
     Agree mine{groups, (uint64_t)coll, (uint64_t)dl.expired()};
     comm.all_gather_host(&mine.groups, all.data(), 3, st);
     bool any_coll = false, any_expired = false;

@@ -875,6 +875,78 @@ __global__ void mirror_kernel(const uint32_t* __restrict__ block, uint64_t n,
   }
 }
 
+// Packed mirror with FB-bit fields, 32/FB per word (FB = 5: six ids per word, 66.7
+// MB at 1e8 states instead of the 8-bit mirror's 100 MB): the L2-resident source
+// of the direct-gather keys below.
+template <int FB>
+__global__ void mirror_packed_kernel(const uint32_t* __restrict__ block, uint64_t n,
+                                     uint32_t* __restrict__ out) {
+  constexpr int kPer = 32 / FB;
+  const uint64_t words = (n + kPer - 1) / kPer;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const uint64_t q = w * kPer + e;
+      if (q < n) word |= block[q] << (e * FB);
+    }
+    out[w] = word;
+  }
+}
+
+// Exact packed keys of the active states by direct gathers from the packed mirror
+// (the blocked builder's output, without its layout): key = (block[q], id(δa(q))...)
+// and the presence bit of the key in the rank-compacted direct table (interleaved
+// {bitmap word, exclusive popcount} pairs).  Used for passes whose ids fit FB <= 8
+// bits: the mirror is L2-resident, so the gathers run at the L2 request rate and the
+// blocked layout is left to the 32-bit passes (built on the side stream meanwhile).
+template <int FB, int kK>
+__global__ void __launch_bounds__(256) direct_keys_kernel(
+    const uint32_t* __restrict__ delta, uint64_t n, uint32_t kr, const uint32_t* __restrict__ mirror,
+    const uint32_t* __restrict__ act, uint64_t m, const uint32_t* __restrict__ block, int w,
+    unsigned long long* __restrict__ keys, uint32_t* present) {
+  constexpr uint32_t kPer = 32 / FB;
+  constexpr uint32_t kMask = (1u << FB) - 1u;
+  const uint32_t k = kK > 0 ? (uint32_t)kK : kr;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_ids = policy_evict_last();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint32_t q = act ? act[i] : (uint32_t)i;
+    unsigned long long key = block[q];
+    uint32_t t[kK > 0 ? kK : 8];
+    for (uint32_t a0 = 0; a0 < k; a0 += (kK > 0 ? kK : 8)) {
+      const uint32_t na = kK > 0 ? (uint32_t)kK : min(8u, k - a0);
+#pragma unroll
+      for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : 8u); ++a)
+        if (a < na) t[a] = ld_stream(delta + (uint64_t)(a0 + a) * n + q, pol_stream);
+      uint32_t wd[kK > 0 ? kK : 8];
+#pragma unroll
+      for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : 8u); ++a)
+        if (a < na) {
+          asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+              : "=r"(wd[a]) : "l"(mirror + t[a] / kPer), "l"(pol_ids));
+        }
+#pragma unroll
+      for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : 8u); ++a)
+        if (a < na) key = (key << w) | ((wd[a] >> ((t[a] % kPer) * FB)) & kMask);
+    }
+    keys[i] = key;
+    const uint32_t bit = 1u << (key & 31);
+    uint32_t* word = present + 2 * (key >> 5);
+    if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
+  }
+}
+
+// opt-in (DFM_SORTPR_DIRECT=1): measured slower on random_dfa(1e8, 4) — 2.0 ms for the
+// 4e8 gathers from the 66.7 MB 5-bit mirror while the layout streams beside it, vs
+// 1.7 ms for the blocked pass (profiles/r02c)
+bool pass_direct_enabled() {
+  const char* e = getenv("DFM_SORTPR_DIRECT");
+  return e != nullptr && e[0] == '1';
+}
+
 // canonical labels from maintained leaders (leader = minimum state of its block):
 // label(block) = rank of its leader among all leaders (core.hpp:123-136)
 struct LeadIn {
@@ -1527,7 +1599,58 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       const bool part = blocked && part_on && !force_global && !(direct && table <= kSmallTable) &&
                         m >= kPartMinStates && m < (1ull << 31);
       force_global = false;
-      if (blocked) {
+      // narrow exact passes (ids <= 8 bits): keys by direct gathers from an L2-resident
+      // packed mirror; the blocked layout keeps building on the side stream for the
+      // 32-bit passes
+      const bool dgather = blocked && !part && packed && direct && table > kSmallTable && w <= 8 &&
+                           pass_direct_enabled();
+      if (dgather) {
+        keys = ctx.slot_t<unsigned long long>("sh.keys", m);
+        const uint64_t words = ceil_div(table, 32);
+        present = ctx.slot_t<uint32_t>("sh.present", 2 * words);
+        DFM_CUDA(cudaMemsetAsync(present, 0, 2 * words * 4, ctx.stream));
+        const int FB = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : w;  // 5, 6, 7 pack 6/5/4 per word
+        const uint64_t per = 32 / FB;
+        uint32_t* pm = ctx.slot_t<uint32_t>("sh.pmirror", ceil_div(n, per));
+        {
+          ProfScope p(ctx, "mirror", n * 4 + ceil_div(n, per) * 4);
+          const unsigned g = grid_for(ctx, ceil_div(n, per));
+          switch (FB) {
+            case 1: mirror_packed_kernel<1><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            case 2: mirror_packed_kernel<2><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            case 4: mirror_packed_kernel<4><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            case 5: mirror_packed_kernel<5><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            case 6: mirror_packed_kernel<6><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            case 7: mirror_packed_kernel<7><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+            default: mirror_packed_kernel<8><<<g, 256, 0, ctx.stream>>>(block, n, pm); break;
+          }
+          DFM_LAUNCH_CHECK();
+        }
+        // delta 4k + k gathers (4 B requests) + own id 4 + act 4 + key 8 per active state
+        ProfScope p(ctx, "sig", m * (8ull * k + 4 + (act ? 4 : 0) + 8));
+        const unsigned g = grid_for(ctx, m);
+#define DFM_DK(FBV)                                                                        \
+  if (k == 2)                                                                              \
+    direct_keys_kernel<FBV, 2><<<g, 256, 0, ctx.stream>>>(d.delta, n, k, pm, act, m, block, w, \
+                                                          keys, present);                  \
+  else if (k == 4)                                                                         \
+    direct_keys_kernel<FBV, 4><<<g, 256, 0, ctx.stream>>>(d.delta, n, k, pm, act, m, block, w, \
+                                                          keys, present);                  \
+  else                                                                                     \
+    direct_keys_kernel<FBV, 0><<<g, 256, 0, ctx.stream>>>(d.delta, n, k, pm, act, m, block, w, \
+                                                          keys, present);
+        switch (FB) {
+          case 1: DFM_DK(1) break;
+          case 2: DFM_DK(2) break;
+          case 4: DFM_DK(4) break;
+          case 5: DFM_DK(5) break;
+          case 6: DFM_DK(6) break;
+          case 7: DFM_DK(7) break;
+          default: DFM_DK(8) break;
+        }
+#undef DFM_DK
+        DFM_LAUNCH_CHECK();
+      } else if (blocked) {
         if (lay_pending) {  // built on the side stream during pass 1
           DFM_CUDA(cudaStreamWaitEvent(ctx.stream, lay_ready, 0));
           lay_pending = false;

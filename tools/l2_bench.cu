@@ -99,7 +99,7 @@ int main() {
   printf("%10s", "footprint");
   for (auto nm : names) printf(" %12s", nm);
   printf("   (G ops/s)\n");
-  for (uint64_t mb : {1ull, 4ull, 16ull, 32ull, 48ull, 64ull, 96ull, 128ull, 512ull, 2048ull}) {
+  for (uint64_t mb : {1ull, 16ull, 32ull, 48ull, 56ull, 64ull, 72ull, 80ull, 96ull, 112ull, 128ull, 512ull}) {
     const uint64_t words = (mb << 20) / 4;
     fill_idx<<<148 * 8, 256>>>(idx, m, words);
     float t[7] = {run<0>(tab, words, m, sink, idx), run<1>(tab, words, m, sink, idx),
