@@ -322,6 +322,16 @@ struct FusedArgs {
   uint32_t max_passes;
   int start_sel;  // buffer holding the labels the next pass reads
   uint32_t* out;  // [0] passes executed, [1] stable, [2] buffer holding the labels
+  // work-efficient passes (null: off): predecessor lists (CSR over all letters) and
+  // mark[r] = the first pass that must re-evaluate r — set when a successor of r
+  // split (its label changed).  A state is evaluated in pass P iff it split in P-1
+  // (new leader), mark[q] >= P, or mark[leader(q)] >= P (a successor of its leader
+  // changed); otherwise every label it would compare is unchanged since its last
+  // evaluation, which found no difference, so its verdict is "no split" again.
+  const uint32_t* pred_off;
+  const uint32_t* pred_src;
+  uint32_t* mark;
+  uint32_t dirty_from;  // first pass that writes marks (it evaluates every state)
 };
 
 // label words carry the previous pass's split flag in bit 31 (state ids < 2^31), so
@@ -363,15 +373,19 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
       if (qi >= a.n) continue;
       const uint32_t q = (uint32_t)qi;
-      const uint32_t leader = label_on_the_fly(Lm[q], cprev);
+      const uint32_t lw = Lm[q];
+      const uint32_t leader = label_on_the_fly(lw, cprev);
       bool sp = false;
-      if (one && leader != cl && q != leader) {
+      bool eval = q != leader;
+      if (eval && a.mark != nullptr && pass > a.dirty_from && !(lw & kSplitBit))
+        eval = a.mark[q] >= pass || a.mark[leader] >= pass;
+      if (one && leader != cl && eval) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if ((uint64_t)u < a.letters) crow[u] = a.rows[(uint64_t)u * a.n + leader];
         cl = leader;
       }
-      if (q != leader) {
+      if (eval) {
         for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
           uint32_t tq[4], tl[4], lq[4], ll[4];
 #pragma unroll
@@ -395,6 +409,10 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       Lw[q] = leader | (sp ? kSplitBit : 0u);  // this pass's split rides with the label
       any |= sp;
       elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
+      if (sp && a.mark != nullptr)  // q's label changes: its predecessors re-evaluate
+        // (pass >= dirty_from always holds here: marks exist only from that launch on)
+        for (uint32_t e = a.pred_off[q], e1 = a.pred_off[q + 1]; e < e1; ++e)
+          a.mark[a.pred_src[e]] = pass + 1;
     }
     if (prev_changed == 0u) {  // pass p was stable: this pass rewrote the same labels
       stable = true;
@@ -625,6 +643,39 @@ constexpr uint64_t kClusterMaxStates = 4096;
 
 // resident threads of the cooperative launch of `kern` (per variant: its register
 // count sets its occupancy)
+__global__ void pred_count_kernel(const uint32_t* __restrict__ rows, uint64_t n, uint64_t letters,
+                                  uint32_t* __restrict__ deg) {
+  const uint64_t total = n * letters, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride)
+    atomicAdd(&deg[rows[j]], 1u);
+}
+__global__ void pred_fill_kernel(const uint32_t* __restrict__ rows, uint64_t n, uint64_t letters,
+                                 uint32_t* __restrict__ cursor, uint32_t* __restrict__ src) {
+  const uint64_t total = n * letters, stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride)
+    src[atomicAdd(&cursor[rows[j]], 1u)] = (uint32_t)(j % n);
+}
+struct DegIn {
+  const uint32_t* deg;
+  __device__ uint32_t operator()(uint64_t i) const { return deg[i]; }
+};
+struct DegOut {
+  uint32_t* off;
+  uint32_t* cursor;
+  __device__ void operator()(uint64_t i, uint32_t excl, uint32_t) const {
+    off[i] = excl;
+    cursor[i] = excl;
+  }
+};
+
+// large alphabets only: the marks cost one store per predecessor of each split state
+// and two reads per state; the saving is up to 2k gathers per stable state per pass
+bool dirty_enabled(uint64_t n, uint64_t letters) {
+  const char* e = getenv("DFM_NAIVE_DIRTY");
+  if (e != nullptr) return e[0] == '1';
+  return letters >= 8 && n * letters < (1ull << 31);
+}
+
 uint64_t fused_max_states(const Ctx& ctx, const void* kern) {
   const int per_sm = per_device_memo(kern, ctx.device, [](const void* k) {
         int v = 0;
@@ -760,13 +811,40 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
                                    : fused_pr_kernel<DFM_POLICY_ARBITRARY, false>;
     const unsigned pgrid = (unsigned)std::min<uint64_t>(
         ceil_div(n, kPersistThreads), fused_max_states(ctx, (const void*)kern) / kPersistThreads);
+    const uint32_t *pred_off = nullptr, *pred_src = nullptr;
+    uint32_t* mark = nullptr;
+    uint32_t dirty_from = 0;
+    // the predecessor lists pay off only over many passes: built once a run has gone
+    // 64 passes without converging (transPR's few-pass runs never build them)
+    auto build_dirty = [&]() {
+      // predecessor lists over all letters (CSR by target), built once per run
+      ProfScope p(ctx, "init", n * letters * 12 + n * 12);
+      uint32_t* deg = ctx.slot_t<uint32_t>("pr.deg", n + 1);
+      uint32_t* off = ctx.slot_t<uint32_t>("pr.poff", n + 1);
+      uint32_t* cur = ctx.slot_t<uint32_t>("pr.pcur", n + 1);
+      uint32_t* src = ctx.slot_t<uint32_t>("pr.psrc", std::max<uint64_t>(n * letters, 1));
+      mark = ctx.slot_t<uint32_t>("pr.mark", n);
+      DFM_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 4, ctx.stream));
+      DFM_CUDA(cudaMemsetAsync(mark, 0, n * 4, ctx.stream));
+      const unsigned g2 = (unsigned)std::min<uint64_t>(ceil_div(n * letters, 256), ctx.num_sms * 16ull);
+      pred_count_kernel<<<g2, 256, 0, ctx.stream>>>(rows, n, letters, deg);
+      DFM_LAUNCH_CHECK();
+      prims::lookback_scan(ctx, "pr.degscan", n + 1, DegIn{deg}, DegOut{off, cur}, nullptr);
+      pred_fill_kernel<<<g2, 256, 0, ctx.stream>>>(rows, n, letters, cur, src);
+      DFM_LAUNCH_CHECK();
+      pred_off = off;
+      pred_src = src;
+      dirty_from = pass + 1;
+    };
     while (true) {
       if (dl.expired()) {
         out.status = DFM_STATUS_TIMEOUT;
         return out;
       }
+      if (mark == nullptr && pass >= 64 && dirty_enabled(n, letters)) build_dirty();
       DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
-      FusedArgs fa{rows, n, letters, lab[0], lab[1], cells, cells1, chg, pass, chunk, sel, pout};
+      FusedArgs fa{rows, n,     letters, lab[0], lab[1], cells,    cells1,   chg,
+                   pass, chunk, sel,     pout,   pred_off, pred_src, mark,   dirty_from};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&fa};
       ProfScope prof(ctx, "elect", 0);

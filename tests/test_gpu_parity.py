@@ -481,3 +481,30 @@ def test_one_barrier_kernel_all_policies_partition(eng):
             for pol, name in ((MIN, "min"), (MAX, "max")):
                 assert eng.naive_pr(d, dfm.PrOptions(policy=pol)).stats.iterations == \
                     O.naive_pr(*pair, name).iterations
+
+
+@pytest.mark.parametrize("name,pair", [
+    ("vlts_k12", lambda: O.vlts_dfa(300, 60_000, 12)),
+    ("random_k9", lambda: O.random_dfa(20_000, 9, 77, 0.5)),
+    ("fib14_k1", lambda: O.fib_dfa(14)),
+    ("comb_k2", lambda: O.comb_dfa(3000, 3)),
+])
+def test_naive_work_efficient_passes(eng, monkeypatch, name, pair):
+    """The work-efficient fused pass (predecessor marks: a state re-evaluates only when
+    a label it compares changed) gives the reference's partition AND pass count —
+    forced on (DFM_NAIVE_DIRTY=1) for small alphabets too, and against it off."""
+    delta, acc = pair()
+    d = to_dfa((delta, acc))
+    for pol, name_ in ((MIN, "min"), (MAX, "max")):
+        ref = O.naive_pr(delta, acc, name_)
+        for flag in ("1", "0"):
+            monkeypatch.setenv("DFM_NAIVE_DIRTY", flag)
+            r = eng.naive_pr(d, dfm.PrOptions(policy=pol))
+            assert r.stats.iterations == ref.iterations, (name, name_, flag)
+            assert (r.partition.block == ref.block).all(), (name, name_, flag)
+    monkeypatch.setenv("DFM_NAIVE_DIRTY", "1")
+    rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+    ref_t = O.trans_pr(delta, acc, "min")
+    assert rt.stats.iterations == ref_t.iterations and (rt.partition.block == ref_t.block).all()
+    assert (eng.naive_pr(d, dfm.PrOptions(policy=ARB)).partition.block ==
+            O.naive_pr(delta, acc, "min").block).all()
