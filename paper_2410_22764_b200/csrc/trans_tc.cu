@@ -229,6 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int8_t* rrow = reach + (uint64_t)row * Vp;
     int8_t* nrow = next + (uint64_t)row * Vp;
     bool hit = false;
+    // an R half whose occupancy bit is clear is zero (and may be unwritten: dead_copy
+    // skips all-zero tiles)
+    const bool r_lo = tile_nz(nz, T, mt, nt), r_hi = tile_nz(nz, T, mt, nt + 1);
 #pragma unroll 1
     for (int c = 0; c < kBN / 32; ++c) {
       uint32_t v[32];
@@ -239,9 +242,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int b = 0; b < 32; ++b) v[b] = 0;
       }
       const uint32_t j0 = n0 + c * 32;
-      const uint4* rp = reinterpret_cast<const uint4*>(rrow + j0);
-      const uint4 r0 = rp[0], r1 = rp[1];
-      const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      uint32_t rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (c < 4 ? r_lo : r_hi) {
+        const uint4* rp = reinterpret_cast<const uint4*>(rrow + j0);
+        const uint4 r0 = rp[0], r1 = rp[1];
+        rw[0] = r0.x; rw[1] = r0.y; rw[2] = r0.z; rw[3] = r0.w;
+        rw[4] = r1.x; rw[5] = r1.y; rw[6] = r1.z; rw[7] = r1.w;
+      }
       uint32_t mask = 0;
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
@@ -274,6 +281,215 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
   }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent variant: one CTA per SM walks the live-tile list (static round robin),
+// so the TMEM allocation, barrier setup and tensormap prefetch happen once per pass
+// instead of once per tile; TMEM holds TWO 256-column accumulators, so the
+// epilogue of tile i (warps 4..7) overlaps the TMA loads and MMAs of tile i+1
+// (acc_full / acc_empty mbarrier pairs per buffer); the smem ring's stage counter
+// runs across tiles.  The producer and MMA warps find a tile's live K blocks
+// warp-cooperatively (one ballot per 32 K blocks) in the same order.  The epilogue
+// skips reading R where both 128x128 halves of the R tile are zero (occupancy
+// bits), and dead_copy skips all-zero tiles: a tile whose occupancy bit is clear
+// is never read by anyone (TMA loads, epilogue, copy), so it need not be written.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tile_coords(uint32_t tid, uint32_t Vp, uint32_t& m0, uint32_t& n0) {
+  const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN;
+  const uint32_t group = tid / (kGroupM * tiles_n);
+  const uint32_t first_m = group * kGroupM;
+  const uint32_t gm = min((uint32_t)kGroupM, tiles_m - first_m);
+  const uint32_t in_group = tid - group * kGroupM * tiles_n;
+  m0 = (first_m + in_group % gm) * kBM;
+  n0 = (in_group / gm) * kBN;
+}
+
+// live K blocks kb0..kb0+31 of output tile (mt, nt..nt+1), one bit per lane
+__device__ __forceinline__ uint32_t live_mask32(const uint32_t* nz, uint32_t T, uint32_t mt,
+                                                uint32_t nt, uint32_t kb0, uint32_t kblocks,
+                                                uint32_t lane) {
+  const uint32_t kb = kb0 + lane;
+  const bool lv = kb < kblocks && tile_nz(nz, T, mt, kb) &&
+                  (tile_nz(nz, T, kb, nt) || tile_nz(nz, T, kb, nt + 1));
+  return __ballot_sync(0xffffffffu, lv);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    square_persistent_kernel(const __grid_constant__ CUtensorMap map,
+                             const int8_t* __restrict__ reach, int8_t* __restrict__ next,
+                             const unsigned long long* __restrict__ apart,
+                             unsigned long long* apart_next, uint32_t Vp, uint32_t W,
+                             const uint32_t* __restrict__ nz, uint32_t* __restrict__ nz_next,
+                             unsigned long long* live_blocks,
+                             const uint32_t* __restrict__ tile_list, uint32_t n_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t kblocks = Vp / kBK, T = Vp / 128;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {  // TMA producer (whole warp finds the live blocks, lane 0 issues)
+    uint32_t j = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint32_t m0, n0;
+      tile_coords(tile_list[t], Vp, m0, n0);
+      const uint32_t mt = m0 / 128, nt = n0 / 128;
+      for (uint32_t kb0 = 0; kb0 < kblocks; kb0 += 32) {
+        uint32_t mask = live_mask32(nz, T, mt, nt, kb0, kblocks, lane);
+        while (mask) {
+          const uint32_t kb = kb0 + __ffs(mask) - 1;
+          mask &= mask - 1;
+          if (lane == 0) {
+            const int s = j % kStages;
+            if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
+            uint8_t* a = smem + s * kStageBytes;
+            uint8_t* b = a + kStageA;
+            mbar_expect_tx(&full[s], kStageBytes);
+            tma_load_2d(a, &map, &full[s], (int)(kb * kBK), (int)m0);
+            tma_load_2d(b, &map, &full[s], (int)n0, (int)(kb * kBK));
+            tma_load_2d(b + kStageB / 2, &map, &full[s], (int)(n0 + 128), (int)(kb * kBK));
+          }
+          ++j;
+        }
+      }
+    }
+  } else if (warp == 1) {  // MMA issuer
+    uint32_t j = 0, tl = 0;
+    unsigned long long done = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      uint32_t m0, n0;
+      tile_coords(tile_list[t], Vp, m0, n0);
+      const uint32_t mt = m0 / 128, nt = n0 / 128;
+      const uint32_t buf = tl & 1, use = tl >> 1;
+      if (tl >= 2) mbar_wait(&acc_empty[buf], (use - 1) & 1);  // epilogue drained it
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dacc = tmem + buf * kBN;
+      bool first = true;
+      for (uint32_t kb0 = 0; kb0 < kblocks; kb0 += 32) {
+        uint32_t mask = live_mask32(nz, T, mt, nt, kb0, kblocks, lane);
+        while (mask) {
+          mask &= mask - 1;
+          if (lane == 0) {
+            const int s = j % kStages;
+            mbar_wait(&full[s], (j / kStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a = smem_u32(smem + s * kStageBytes);
+            const uint32_t b = a + kStageA;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 32; ++kk) {
+              const uint64_t da = smem_desc(a + kk * 32, 16, 1024);
+              const uint64_t db = smem_desc(b + kk * 32 * 128, kStageB / 2, 1024);
+              umma_i8(dacc, da, db, (!first || kk != 0) ? 1u : 0u);
+            }
+            umma_commit(&empty[s]);
+          }
+          first = false;
+          ++j;
+          ++done;
+        }
+      }
+      if (lane == 0) umma_commit(&acc_full[buf]);  // (every listed tile has a live block)
+    }
+    if (lane == 0 && done) atomicAdd(live_blocks, done);
+  } else if (warp >= 4) {  // epilogue
+    const uint32_t quarter = warp - 4;
+    uint32_t tl = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      uint32_t m0, n0;
+      tile_coords(tile_list[t], Vp, m0, n0);
+      const uint32_t mt = m0 / 128;
+      const uint32_t buf = tl & 1, use = tl >> 1;
+      const bool r_lo = tile_nz(nz, T, mt, n0 / 128), r_hi = tile_nz(nz, T, mt, n0 / 128 + 1);
+      mbar_wait(&acc_full[buf], use & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t row = m0 + quarter * 32 + lane;
+      const int8_t* rrow = reach + (uint64_t)row * Vp;
+      int8_t* nrow = next + (uint64_t)row * Vp;
+      bool hit = false;
+#pragma unroll 1
+      for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((quarter * 32) << 16) + buf * kBN + c * 32, v);
+        const uint32_t j0 = n0 + c * 32;
+        uint32_t rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (c < 4 ? r_lo : r_hi) {
+          const uint4* rp = reinterpret_cast<const uint4*>(rrow + j0);
+          const uint4 r0 = rp[0], r1 = rp[1];
+          rw[0] = r0.x; rw[1] = r0.y; rw[2] = r0.z; rw[3] = r0.w;
+          rw[4] = r1.x; rw[5] = r1.y; rw[6] = r1.z; rw[7] = r1.w;
+        }
+        uint32_t mask = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+          const uint32_t rb = (rw[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
+          mask |= ((v[b] != 0u) | (rb != 0u) ? 1u : 0u) << b;
+        }
+        uint32_t ow[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const uint32_t nib = (mask >> (w * 4)) & 0xFu;
+          ow[w] = (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 |
+                  ((nib >> 3) & 1u) << 24;
+        }
+        uint4* op = reinterpret_cast<uint4*>(nrow + j0);
+        op[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        op[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+        const uint32_t abits = (j0 >> 6) < W ? (uint32_t)(apart[j0 >> 6] >> (j0 & 63)) : 0u;
+        hit |= (mask & abits) != 0u;
+        if (__any_sync(0xffffffffu, mask != 0u) && lane == 0) {
+          const uint32_t b = mt * T + j0 / 128;
+          atomicOr(&nz_next[b >> 5], 1u << (b & 31));
+        }
+      }
+      if (hit) atomicOr(&apart_next[row >> 6], 1ull << (row & 63));
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+bool persist_enabled() {
+  const char* e = getenv("DFM_TRANS_PERSIST");
+  return e == nullptr || e[0] != '0';
 }
 
 // Output tiles (in square_kernel's rasterised order) with / without a live K block;
@@ -319,6 +535,7 @@ __global__ void __launch_bounds__(256) dead_copy_kernel(const int8_t* __restrict
                                                         const uint32_t* __restrict__ dead_list,
                                                         const unsigned long long* __restrict__ apart,
                                                         unsigned long long* apart_next, uint32_t W,
+                                                        const uint32_t* __restrict__ nz,
                                                         uint32_t* __restrict__ nz_next) {
   __shared__ uint32_t s_occ[2];
   const uint32_t tiles_m = Vp / kBM, tiles_n = Vp / kBN, T = Vp / 128;
@@ -329,6 +546,9 @@ __global__ void __launch_bounds__(256) dead_copy_kernel(const int8_t* __restrict
   const uint32_t in_group = tid - group * kGroupM * tiles_n;
   const uint32_t m0 = (first_m + in_group % gm) * kBM;
   const uint32_t n0 = (in_group / gm) * kBN;
+  // an all-zero R tile stays unwritten: its occupancy bit stays clear, so no reader
+  // (TMA, epilogue, this copy) touches the stale bytes there
+  if (!tile_nz(nz, T, m0 / 128, n0 / 128) && !tile_nz(nz, T, m0 / 128, n0 / 128 + 1)) return;
   if (threadIdx.x < 2) s_occ[threadIdx.x] = 0;
   __syncthreads();
   for (uint32_t idx = threadIdx.x; idx < kBM * (kBN / 16); idx += blockDim.x) {
@@ -419,6 +639,8 @@ TransTcState init(Ctx& ctx, const DevDfa& d, uint64_t V) {
   per_device_memo((const void*)square_kernel, ctx.device, [](const void*) {
     DFM_CUDA(cudaFuncSetAttribute(square_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBytes));
+    DFM_CUDA(cudaFuncSetAttribute(square_persistent_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
     return 1;
   });
   TransTcState st;
@@ -472,9 +694,14 @@ void square_and_propagate(Ctx& ctx, TransTcState& st, const unsigned long long* 
     if (n_dead)
       dead_copy_kernel<<<n_dead, 256, 0, ctx.stream>>>(st.reach, st.next, (uint32_t)st.Vp,
                                                       dead_list, apart, apart_next, (uint32_t)W,
-                                                      st.nz_next);
+                                                      st.nz, st.nz_next);
     DFM_LAUNCH_CHECK();
-    if (n_live)
+    if (n_live && persist_enabled())
+      square_persistent_kernel<<<std::min<uint32_t>(n_live, (uint32_t)ctx.num_sms), kThreads,
+                                 kSmemBytes, ctx.stream>>>(
+          map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W, st.nz,
+          st.nz_next, live, live_list, n_live);
+    else if (n_live)
       square_kernel<<<n_live, kThreads, kSmemBytes, ctx.stream>>>(
           map, st.reach, st.next, apart, apart_next, (uint32_t)st.Vp, (uint32_t)W, st.nz,
           st.nz_next, live, live_list);
