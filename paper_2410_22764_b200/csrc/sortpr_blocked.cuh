@@ -394,6 +394,10 @@ struct SigParams {
   uint32_t* present;  // direct keys: bitmap of the keys present, words interleaved with
                       // their exclusive popcounts (rank-compacted table)
   uint32_t tile_bytes;  // shared tile size (16-byte multiple)
+  // uniqueness filter of a filtered pass (null: none): the level-0 set is done here,
+  // on the key still in registers, instead of a separate sweep over the keys
+  uint32_t* filt = nullptr;
+  bool filt_hashed = false;
 };
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
@@ -462,13 +466,15 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
     for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
       const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
       const uint32_t x = (uint32_t)(q - q0);
+      unsigned long long stored;
       const uint32_t b = p.block[q];
       if (!kHashed) {
         unsigned long long key = b;
 #pragma unroll
         for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
           key = (key << p.w) | tget(a * L.W + x);
-        p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
+        stored = p.vals ? mix64(key ^ p.seed) : key;
+        p.keys[i] = stored;
         if (p.present) {  // test before set: most keys of a dense pass are repeats
           const uint32_t bit = 1u << (key & 31);
           uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
@@ -484,10 +490,18 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
           row[a + 1] = s;
           h = mix64(h + kGolden + s);
         }
-        p.keys[i] = weak(h, p.seed);
+        stored = weak(h, p.seed);
+        p.keys[i] = stored;
       }
       if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
-      {
+      if (p.filt) {  // = filt_set_kernel level 0 on keys[i]
+        const uint64_t c =
+            (table_hash(stored, p.filt_hashed, p.seed) >> (64 - kFilterCellBits)) &
+            ((1ull << kFilterCellBits) - 1);
+        const uint32_t bb = (uint32_t)(c & 15) * 2;
+        const uint64_t pol_keep = policy_evict_last();
+        const uint32_t old = atom_or_keep(&p.filt[c >> 4], 1u << bb, pol_keep);
+        if (((old >> bb) & 3u) == 1u) red_or_keep(&p.filt[c >> 4], 2u << bb, pol_keep);
       }
     }
     __syncthreads();
