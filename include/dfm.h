@@ -43,7 +43,9 @@ typedef enum {
   DFM_ERR_CUDA = 2,     /* CUDA runtime / launch failure */
   DFM_ERR_CAPACITY = 3, /* dfm_expand_alphabet over max_memory_bytes (CapacityError) */
   DFM_ERR_NO_MEMORY = 4,/* device allocation failed */
-  DFM_ERR_NO_DEVICE = 5 /* no sm_100 device / extension unusable: never silently falls back */
+  DFM_ERR_NO_DEVICE = 5,/* no sm_100 device / extension unusable: never silently falls back */
+  DFM_ERR_PARSE = 6,    /* dfm_lts_parse: the reference's ParseError (ingest.hpp:20-28) */
+  DFM_ERR_BUDGET = 7    /* dfm_determinize: SubsetBudgetExceeded (ingest.hpp:31-39) */
 } dfm_err;
 
 /* RunStatus, core.hpp:58 */
@@ -262,6 +264,44 @@ int dfm_canonicalize_dev(dfm_ctx* ctx, const void* raw_dev, uint64_t n, void* ou
 int dfm_random_dfa_slice_dev(dfm_ctx* ctx, uint64_t n_total, uint32_t k, uint64_t seed,
                              double accept_prob, uint64_t lo, uint64_t count, void* delta_out,
                              void* accepting_out);
+
+/* ---------------------------------------------------------------- LTS ingestion (host) */
+/* The VLTS front-end of the reference, host-side: parse_lts
+ * (ingest.hpp:130-175), determinize (ingest.hpp:187-245), complete
+ * (ingest.hpp:253-284).  No context (no GPU) needed.  Same automaton, same numbering,
+ * same errors as the reference; the parser is multi-threaded. */
+typedef struct dfm_lts dfm_lts;
+typedef struct dfm_pdfa dfm_pdfa;
+/* DFM_ERR_PARSE: err receives "line <n>: <what>" (ParseError::what()), *err_line = n */
+int dfm_lts_parse(const char* text, uint64_t len, dfm_lts** out, uint64_t* err_line, char* err,
+                  uint32_t err_cap);
+int dfm_lts_info(const dfm_lts* lts, uint32_t* num_states, uint32_t* initial,
+                 uint32_t* num_labels, uint64_t* num_transitions);
+/* label i (interned in first-appearance order): pointer valid until dfm_lts_free */
+int dfm_lts_label(const dfm_lts* lts, uint32_t i, const char** data, uint64_t* len);
+/* the transitions in file order (each array num_transitions entries; NULL skips) */
+int dfm_lts_transitions(const dfm_lts* lts, uint32_t* src, uint32_t* label, uint32_t* dst);
+void dfm_lts_free(dfm_lts* lts);
+/* an LTS from arrays (labels NULL: named "0", "1", ...) */
+int dfm_lts_build(uint32_t num_states, uint32_t initial, uint32_t num_labels,
+                  const char* const* labels, const uint64_t* label_lens, uint64_t m,
+                  const uint32_t* src, const uint32_t* label, const uint32_t* dst, dfm_lts** out);
+/* subset construction from {initial}; DFM_ERR_BUDGET (and *budget_out) when more than
+ * max_subset_states subsets appear (reference default 1 << 22) */
+int dfm_determinize(const dfm_lts* lts, uint64_t max_subset_states, dfm_pdfa** out,
+                    uint64_t* budget_out);
+int dfm_pdfa_shape(const dfm_pdfa* p, uint32_t* num_states, uint32_t* alphabet_size,
+                   uint32_t* initial);
+/* k rows of n targets, 0xFFFFFFFF = missing (PartialDfa::kMissing) */
+int dfm_pdfa_rows(const dfm_pdfa* p, uint32_t* delta_flat);
+/* complete with one rejecting sink iff a transition is missing: *num_states_out = n or
+ * n + 1; delta_flat k * (*num_states_out) and accepting (*num_states_out) may be NULL
+ * (query the size first) */
+int dfm_complete(const dfm_pdfa* p, uint32_t* num_states_out, uint32_t* delta_flat,
+                 uint8_t* accepting);
+void dfm_pdfa_free(dfm_pdfa* p);
+int dfm_pdfa_build(uint32_t num_states, uint32_t alphabet_size, uint32_t initial,
+                   const uint32_t* delta_flat, dfm_pdfa** out);
 
 /* ---------------------------------------------------------------- sharded sortPR driver */
 /* The C++ driver of the state-sharded sortPR: a context

@@ -539,3 +539,50 @@ class RefSortSession:
 
     def __del__(self):
         self.close()
+
+
+def ref_ingest(text, max_subsets: int = 1 << 22) -> dict:
+    """The reference's parse_lts -> determinize -> complete on `text` (oracle/_ref):
+    {"status": "ok"|"parse"|"budget", "line", "what", "lts": (n, init, labels, src,
+    label, dst), "pdfa": delta (k, n), "dfa": (delta, acc)}."""
+    lib = _ref
+    lib.ref_ingest.restype = C.c_void_p
+    lib.ref_ingest.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64]
+    lib.ref_ingest_label.restype = C.c_char_p
+    for f in ("ref_ingest_status", "ref_ingest_lts", "ref_ingest_lts_arrays", "ref_ingest_label",
+              "ref_ingest_pdfa", "ref_ingest_dfa", "ref_ingest_free"):
+        getattr(lib, f).argtypes = None
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p(lib.ref_ingest(data, len(data), max_subsets))
+    try:
+        line = C.c_uint64(0)
+        msg = C.create_string_buffer(512)
+        st = lib.ref_ingest_status(h, C.byref(line), msg, C.c_uint32(512))
+        out = {"status": ["ok", "parse", "budget"][st], "line": int(line.value),
+               "what": msg.value.decode()}
+        if st != 0:
+            return out
+        n, init, nl, m = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        lib.ref_ingest_lts(h, C.byref(n), C.byref(init), C.byref(nl), C.byref(m))
+        src = np.empty(m.value, np.uint32)
+        lab = np.empty(m.value, np.uint32)
+        dst = np.empty(m.value, np.uint32)
+        lib.ref_ingest_lts_arrays(h, src.ctypes.data_as(C.c_void_p), lab.ctypes.data_as(C.c_void_p),
+                                  dst.ctypes.data_as(C.c_void_p))
+        labels = [lib.ref_ingest_label(h, C.c_uint32(i)).decode() for i in range(nl.value)]
+        out["lts"] = (int(n.value), int(init.value), labels, src, lab, dst)
+        pn, pk = C.c_uint32(), C.c_uint32()
+        lib.ref_ingest_pdfa(h, C.byref(pn), C.byref(pk), None)
+        pd = np.empty((pk.value, pn.value), np.uint32)
+        lib.ref_ingest_pdfa(h, C.byref(pn), C.byref(pk), pd.ctypes.data_as(C.c_void_p))
+        out["pdfa"] = pd
+        dn = C.c_uint32()
+        lib.ref_ingest_dfa(h, C.byref(dn), None, None)
+        dd = np.empty((pk.value, dn.value), np.uint32)
+        da = np.empty(dn.value, np.uint8)
+        lib.ref_ingest_dfa(h, C.byref(dn), dd.ctypes.data_as(C.c_void_p),
+                           da.ctypes.data_as(C.c_void_p))
+        out["dfa"] = (dd, da)
+        return out
+    finally:
+        lib.ref_ingest_free(h)

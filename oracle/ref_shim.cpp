@@ -251,6 +251,77 @@ int ref_sort_session_full(void* h, uint32_t* nb, RefStats* st) {
   return 0;
 }
 
+// ---- ingestion (ingest.hpp:130-284): the whole parse -> determinize -> complete
+// pipeline of the reference on one text, errors captured (tests/test_ingest.py)
+struct RefIngest {
+  Lts lts;
+  PartialDfa p;
+  Dfa d;
+  int status = 0;  // 0 ok, 1 ParseError, 2 SubsetBudgetExceeded
+  uint64_t line = 0;
+  std::string what;
+};
+
+void* ref_ingest(const char* text, uint64_t len, uint64_t max_subsets) {
+  auto* r = new RefIngest;
+  try {
+    r->lts = parse_lts(std::string_view(text, len));
+    r->p = determinize(r->lts, max_subsets);
+    r->d = complete(r->p);
+  } catch (const ParseError& e) {
+    r->status = 1;
+    r->line = e.line();
+    r->what = e.what();
+  } catch (const SubsetBudgetExceeded& e) {
+    r->status = 2;
+    r->line = e.budget();
+    r->what = e.what();
+  }
+  return r;
+}
+int ref_ingest_status(void* h, uint64_t* line, char* msg, uint32_t cap) {
+  auto* r = static_cast<RefIngest*>(h);
+  if (line) *line = r->line;
+  if (msg && cap) {
+    std::strncpy(msg, r->what.c_str(), cap - 1);
+    msg[cap - 1] = 0;
+  }
+  return r->status;
+}
+void ref_ingest_lts(void* h, uint32_t* n, uint32_t* init, uint32_t* nl, uint64_t* m) {
+  auto* r = static_cast<RefIngest*>(h);
+  *n = r->lts.num_states;
+  *init = r->lts.initial;
+  *nl = (uint32_t)r->lts.labels.size();
+  *m = r->lts.transitions.size();
+}
+void ref_ingest_lts_arrays(void* h, uint32_t* src, uint32_t* lab, uint32_t* dst) {
+  auto* r = static_cast<RefIngest*>(h);
+  for (size_t j = 0; j < r->lts.transitions.size(); ++j) {
+    src[j] = r->lts.transitions[j].src;
+    lab[j] = r->lts.transitions[j].label;
+    dst[j] = r->lts.transitions[j].dst;
+  }
+}
+const char* ref_ingest_label(void* h, uint32_t i) {
+  return static_cast<RefIngest*>(h)->lts.labels[i].c_str();
+}
+void ref_ingest_pdfa(void* h, uint32_t* n, uint32_t* k, uint32_t* delta) {
+  auto* r = static_cast<RefIngest*>(h);
+  *n = r->p.num_states;
+  *k = r->p.alphabet_size;
+  if (delta)
+    for (uint32_t a = 0; a < r->p.alphabet_size; ++a)
+      std::memcpy(delta + (size_t)a * r->p.num_states, r->p.delta[a].data(),
+                  4ull * r->p.num_states);
+}
+void ref_ingest_dfa(void* h, uint32_t* n, uint32_t* delta, uint8_t* acc) {
+  auto* r = static_cast<RefIngest*>(h);
+  *n = r->d.num_states;
+  if (delta) copy_dfa(r->d, delta, acc);
+}
+void ref_ingest_free(void* h) { delete static_cast<RefIngest*>(h); }
+
 // generators: n/k are known to the caller (fib_len etc. computed by the oracle)
 void ref_random_dfa(uint32_t n, uint32_t k, uint64_t seed, double p, uint32_t* delta,
                     uint8_t* acc) {

@@ -282,6 +282,20 @@ def _load():
         "dfm_write_dfa_bin": (C.c_int, [C.c_char_p, vp]),
         "dfm_ddfa_load_bin": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
         "dfm_ddfa_save_bin": (C.c_int, [vp, vp, C.c_char_p]),
+        "dfm_lts_parse": (C.c_int, [C.c_char_p, u64, C.POINTER(vp), C.POINTER(u64), C.c_char_p,
+                                    u32]),
+        "dfm_lts_info": (C.c_int, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32),
+                                   C.POINTER(u64)]),
+        "dfm_lts_label": (C.c_int, [vp, u32, C.POINTER(C.c_void_p), C.POINTER(u64)]),
+        "dfm_lts_transitions": (C.c_int, [vp, vp, vp, vp]),
+        "dfm_lts_free": (None, [vp]),
+        "dfm_lts_build": (C.c_int, [u32, u32, u32, vp, vp, u64, vp, vp, vp, C.POINTER(vp)]),
+        "dfm_determinize": (C.c_int, [vp, u64, C.POINTER(vp), C.POINTER(u64)]),
+        "dfm_pdfa_shape": (C.c_int, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
+        "dfm_pdfa_rows": (C.c_int, [vp, vp]),
+        "dfm_complete": (C.c_int, [vp, C.POINTER(u32), vp, vp]),
+        "dfm_pdfa_free": (None, [vp]),
+        "dfm_pdfa_build": (C.c_int, [u32, u32, u32, vp, C.POINTER(vp)]),
         "dfm_nccl_get_unique_id": (C.c_int, [vp]),
         "dfm_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, C.POINTER(vp)]),
         "dfm_ctx_create_sharded_local": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p,
@@ -769,3 +783,141 @@ def read_dfa_bin(path: str) -> Dfa:
     off = 24 + ((n + 3) & ~3)
     delta = np.frombuffer(raw[off:off + 4 * n * k].tobytes(), dtype="<u4").reshape(k, n).copy()
     return Dfa(n, k, delta, acc, int(initial))
+
+
+# ---------------------------------------------------------------- LTS ingestion (host)
+# ingest.hpp:130-284 behind libdfm's dfm_lts_* / dfm_determinize / dfm_complete (no GPU
+# needed): the same automaton, numbering and errors as the reference.
+class ParseError(ValueError):  # ingest.hpp:20-28
+    def __init__(self, line: int, what: str):
+        super().__init__(what)
+        self._line = int(line)
+
+    def line(self) -> int:
+        return self._line
+
+
+class SubsetBudgetExceeded(RuntimeError):  # ingest.hpp:31-39
+    def __init__(self, budget: int):
+        super().__init__(f"subset construction exceeded {budget} states")
+        self._budget = int(budget)
+
+    def budget(self) -> int:
+        return self._budget
+
+
+K_MISSING = 0xFFFFFFFF  # PartialDfa::kMissing
+
+
+@dataclass
+class Lts:  # core.hpp:36-47 (transitions as three aligned arrays)
+    num_states: int
+    initial: int
+    labels: list
+    src: np.ndarray
+    label: np.ndarray
+    dst: np.ndarray
+
+    @property
+    def transitions(self):
+        return list(zip(self.src.tolist(), self.label.tolist(), self.dst.tolist()))
+
+
+@dataclass
+class PartialDfa:  # ingest.hpp:177-184
+    num_states: int
+    alphabet_size: int
+    delta: np.ndarray  # (alphabet_size, num_states) uint32, K_MISSING where absent
+    initial: int = 0
+    kMissing = K_MISSING
+
+
+def _lts_handle(lts: Lts):
+    lib = _load()
+    h = C.c_void_p()
+    enc = [x.encode() for x in lts.labels]
+    arr = (C.c_char_p * max(len(enc), 1))(*enc)
+    lens = (C.c_uint64 * max(len(enc), 1))(*[len(x) for x in enc])
+    src = np.ascontiguousarray(lts.src, dtype=np.uint32)
+    lab = np.ascontiguousarray(lts.label, dtype=np.uint32)
+    dst = np.ascontiguousarray(lts.dst, dtype=np.uint32)
+    rc = lib.dfm_lts_build(lts.num_states, lts.initial, len(enc), C.cast(arr, C.c_void_p),
+                           C.cast(lens, C.c_void_p), src.size, src.ctypes.data, lab.ctypes.data,
+                           dst.ctypes.data, C.byref(h))
+    if rc != 0:
+        raise ValueError("malformed LTS")
+    return h
+
+
+def parse_lts(text) -> Lts:
+    """ingest.hpp:130-175; raises ParseError(line) like the reference."""
+    lib = _load()
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    line = C.c_uint64(0)
+    err = C.create_string_buffer(512)
+    rc = lib.dfm_lts_parse(data, len(data), C.byref(h), C.byref(line), err, 512)
+    if rc == 6:
+        msg = err.value.decode()
+        raise ParseError(int(line.value), msg)
+    if rc != 0:
+        raise EngineError(rc, "dfm_lts_parse failed")
+    try:
+        n, init, nl, m = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        lib.dfm_lts_info(h, C.byref(n), C.byref(init), C.byref(nl), C.byref(m))
+        labels = []
+        for i in range(nl.value):
+            p, ln = C.c_void_p(), C.c_uint64()
+            lib.dfm_lts_label(h, i, C.byref(p), C.byref(ln))
+            labels.append(C.string_at(p, ln.value).decode())
+        src = np.empty(m.value, np.uint32)
+        lab = np.empty(m.value, np.uint32)
+        dst = np.empty(m.value, np.uint32)
+        lib.dfm_lts_transitions(h, src.ctypes.data, lab.ctypes.data, dst.ctypes.data)
+        return Lts(int(n.value), int(init.value), labels, src, lab, dst)
+    finally:
+        lib.dfm_lts_free(h)
+
+
+def determinize(lts: Lts, max_subset_states: int = 1 << 22) -> PartialDfa:
+    """ingest.hpp:187-245 (subset construction, BFS numbering); raises
+    SubsetBudgetExceeded like the reference."""
+    lib = _load()
+    h = _lts_handle(lts)
+    try:
+        p = C.c_void_p()
+        budget = C.c_uint64(0)
+        rc = lib.dfm_determinize(h, max_subset_states, C.byref(p), C.byref(budget))
+        if rc == 7:
+            raise SubsetBudgetExceeded(int(budget.value))
+        if rc != 0:
+            raise EngineError(rc, "dfm_determinize failed")
+        try:
+            n, k, init = C.c_uint32(), C.c_uint32(), C.c_uint32()
+            lib.dfm_pdfa_shape(p, C.byref(n), C.byref(k), C.byref(init))
+            delta = np.empty((k.value, n.value), np.uint32)
+            lib.dfm_pdfa_rows(p, delta.ctypes.data)
+            return PartialDfa(int(n.value), int(k.value), delta, int(init.value))
+        finally:
+            lib.dfm_pdfa_free(p)
+    finally:
+        lib.dfm_lts_free(h)
+
+
+def complete(p: PartialDfa) -> Dfa:
+    """ingest.hpp:253-284: one rejecting sink appended iff a transition is missing."""
+    lib = _load()
+    h = C.c_void_p()
+    delta = np.ascontiguousarray(p.delta, dtype=np.uint32)
+    if lib.dfm_pdfa_build(p.num_states, p.alphabet_size, p.initial, delta.ctypes.data,
+                          C.byref(h)) != 0:
+        raise ValueError("malformed partial DFA")
+    try:
+        n = C.c_uint32()
+        lib.dfm_complete(h, C.byref(n), None, None)
+        out = np.empty((p.alphabet_size, n.value), np.uint32)
+        acc = np.empty(n.value, np.uint8)
+        lib.dfm_complete(h, C.byref(n), out.ctypes.data, acc.ctypes.data)
+        return Dfa(int(n.value), p.alphabet_size, out, acc, p.initial)
+    finally:
+        lib.dfm_pdfa_free(h)

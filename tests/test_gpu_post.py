@@ -105,3 +105,21 @@ def test_remove_unreachable_deep_chain(eng):
     r = eng.remove_unreachable(_dfa(pair, (1 << 20) - 10))
     dq, aq, iq = O.remove_unreachable(*pair, (1 << 20) - 10)
     assert r.num_states == aq.size and (r.delta == dq).all() and r.initial == iq
+
+
+def test_lts_pipeline_into_gpu_minimizers(eng):
+    """VLTS front-end: parse -> determinize -> complete (host, libdfm)
+    -> the GPU minimizers, against the reference's own pipeline and oracle."""
+    import numpy as np
+    from tests.test_ingest import det_lts_text, random_lts_text
+    rng = np.random.default_rng(5)
+    for text in (random_lts_text(rng, 40, 150, 3, 5), det_lts_text(rng, 3000, 4, 10)):
+        d = dfm.complete(dfm.determinize(dfm.parse_lts(text)))
+        r = O.ref_ingest(text)
+        assert (d.delta == r["dfa"][0]).all() and (d.accepting == r["dfa"][1]).all()
+        ref = O.sort_pr(*r["dfa"])
+        got = eng.sort_pr(d)
+        assert (got.partition.block == ref.block).all()
+        assert got.stats.iterations == ref.iterations
+        assert (eng.naive_pr(d, dfm.PrOptions(policy=dfm.RacePolicy.deterministic_min))
+                .partition.block == ref.block).all()
