@@ -309,7 +309,8 @@ int dfm_pdfa_build(uint32_t num_states, uint32_t alphabet_size, uint32_t initial
  * all-gather of block ids, keys, routed exact grouping, dense ids back, fixpoint,
  * canonical labels) — the drop-in for min_sort.hpp:72 sort_pr on DFAs too large
  * for one GPU.  Rank r owns the contiguous states [r*S, min(n, (r+1)*S)),
- * S = ceil(n/world) (dfm_shard_bounds); its rows hold GLOBAL target ids.
+ * S = ceil(n/world) rounded up to a multiple of 32 (dfm_shard_bounds); its rows
+ * hold GLOBAL target ids.
  * Result: the same canonical partition, block count and pass count as the
  * reference's sort_pr for every world size. */
 #define DFM_NCCL_ID_BYTES 128

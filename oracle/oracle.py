@@ -45,7 +45,7 @@ class _OrcStats(C.Structure):
 class _RefStats(C.Structure):
     _fields_ = [("iterations", C.c_uint64), ("closure_steps", C.c_uint64),
                 ("elapsed_ms", C.c_double), ("peak_memory_estimate", C.c_uint64),
-                ("status", C.c_int32)]
+                ("status", C.c_int32), ("call_ms", C.c_double)]
 
 
 PASS_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.c_uint32,
@@ -60,7 +60,8 @@ class Result:
     closure_steps: int
     peak_memory_estimate: int
     status: str
-    elapsed_ms: float = 0.0
+    elapsed_ms: float = 0.0  # the reference's RunStats.elapsed_ms (excludes its canonicalize)
+    call_ms: float = 0.0     # wall time of the whole reference call (oracle/_ref only)
 
 
 def _build_if_missing() -> None:
@@ -180,7 +181,7 @@ def _result(block, nb, st) -> Result:
     status = STATUS[st.status]
     return Result(block if status == "ok" else np.empty(0, np.uint32), int(nb.value),
                   int(st.iterations), int(st.closure_steps), int(st.peak_memory_estimate),
-                  status, float(getattr(st, "elapsed_ms", 0.0)))
+                  status, float(getattr(st, "elapsed_ms", 0.0)), float(getattr(st, "call_ms", 0.0)))
 
 
 def sort_pr(delta, acc, trace: list | None = None) -> Result:

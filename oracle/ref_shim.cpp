@@ -25,6 +25,7 @@ struct RefStats {
   double elapsed_ms;
   uint64_t peak_memory_estimate;
   int32_t status;
+  double call_ms;  // wall time of the whole reference call, incl. its final canonicalize
 };
 
 Dfa make(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc, uint32_t initial) {
@@ -38,7 +39,7 @@ Dfa make(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* acc, uint
   return d;
 }
 
-void out(const MinResult& r, uint32_t* block, uint32_t* nb, RefStats* st) {
+void out(const MinResult& r, uint32_t* block, uint32_t* nb, RefStats* st, double call_ms) {
   if (r.stats.status == RunStatus::ok && block != nullptr)
     std::memcpy(block, r.partition.block.data(), 4ull * r.partition.block.size());
   if (nb) *nb = r.partition.num_blocks;
@@ -48,7 +49,16 @@ void out(const MinResult& r, uint32_t* block, uint32_t* nb, RefStats* st) {
     st->elapsed_ms = r.stats.elapsed_ms;
     st->peak_memory_estimate = r.stats.peak_memory_estimate;
     st->status = static_cast<int32_t>(r.stats.status);
+    st->call_ms = call_ms;
   }
+}
+
+template <class F>
+MinResult timed_call(F&& f, double& ms) {
+  const auto t0 = std::chrono::steady_clock::now();
+  MinResult r = f();
+  ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return r;
 }
 
 substrate::RacePolicy policy_of(int p) {
@@ -80,7 +90,7 @@ int ref_sort_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* ac
   SortOptions opt;
   opt.timeout_ms = timeout_ms;
   if (trace_counts) opt.trace = &trace;
-  out(sort_pr(d, opt), block, nb, st);
+  { double ms_ = 0; const MinResult r_ = timed_call([&] { return sort_pr(d, opt); }, ms_); out(r_, block, nb, st, ms_); }
   if (trace_counts)
     for (size_t i = 0; i < trace.block_counts.size() && i < trace_cap; ++i)
       trace_counts[i] = trace.block_counts[i];
@@ -91,12 +101,12 @@ int ref_naive_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* a
                  int fused_cas, int64_t timeout_ms, uint32_t* block, uint32_t* nb, RefStats* st) {
   const Dfa d = make(n, k, delta, acc, 0);
   if (fused_cas) {
-    out(naive_pr_cas(d, timeout_ms), block, nb, st);
+    { double ms_ = 0; const MinResult r_ = timed_call([&] { return naive_pr_cas(d, timeout_ms); }, ms_); out(r_, block, nb, st, ms_); }
   } else {
     PrOptions opt;
     opt.policy = policy_of(policy);
     opt.timeout_ms = timeout_ms;
-    out(naive_pr(d, opt), block, nb, st);
+    { double ms_ = 0; const MinResult r_ = timed_call([&] { return naive_pr(d, opt); }, ms_); out(r_, block, nb, st, ms_); }
   }
   return 0;
 }
@@ -111,7 +121,7 @@ int ref_trans_pr(uint32_t n, uint32_t k, const uint32_t* delta, const uint8_t* a
   Limits lim;
   lim.max_memory_bytes = max_memory;
   lim.timeout_ms = timeout_ms;
-  out(trans_pr(d, opt, lim), block, nb, st);
+  { double ms_ = 0; const MinResult r_ = timed_call([&] { return trans_pr(d, opt, lim); }, ms_); out(r_, block, nb, st, ms_); }
   return 0;
 }
 
@@ -141,7 +151,7 @@ int ref_trans_minimize(uint32_t n, uint32_t k, const uint32_t* delta, const uint
   lim.max_memory_bytes = max_memory;
   lim.timeout_ms = timeout_ms;
   TransInspect ins;
-  out(trans_minimize(d, lim, &ins), block, nb, st);
+  { double ms_ = 0; const MinResult r_ = timed_call([&] { return trans_minimize(d, lim, &ins); }, ms_); out(r_, block, nb, st, ms_); }
   if (apart && !ins.apart.empty()) std::memcpy(apart, ins.apart.data(), ins.apart.size());
   if (popcounts)
     for (size_t i = 0; i < ins.apart_popcounts.size() && i < pop_cap; ++i)
@@ -247,7 +257,7 @@ void ref_sort_session_free(void* h) { delete static_cast<RefSortSession*>(h); }
 // whole sort_pr on a session's DFA (the reference's own entry point, RunStats timing)
 int ref_sort_session_full(void* h, uint32_t* nb, RefStats* st) {
   auto* s = static_cast<RefSortSession*>(h);
-  out(sort_pr(s->d, SortOptions{}), nullptr, nb, st);
+  { double ms_ = 0; const MinResult r_ = timed_call([&] { return sort_pr(s->d, SortOptions{}); }, ms_); out(r_, nullptr, nb, st, ms_); }
   return 0;
 }
 

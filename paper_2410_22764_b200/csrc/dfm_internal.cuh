@@ -220,7 +220,7 @@ void save_dfa_bin(Ctx& ctx, const DevDfa& dd, const char* path);
 void h2d_rows(Ctx& ctx, void* dst, const void* src, uint64_t bytes);
 // sharded sortPR primitives (shard.cu) and the C++ driver (shard_driver.cu)
 void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
-                     const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                     const void* block_full, uint32_t id_bits, uint64_t lo, uint64_t seed,
                      uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
                      void* dest_out);
 void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, uint64_t count,
@@ -228,8 +228,12 @@ void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, ui
 // exact packed keys (+1) from a key space of 2^key_bits: presence bitmap + rank
 void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key_bits,
                         void* label_out, uint64_t* groups_out);
-// contiguous shards of ceil(n/world) states: rank r owns [r*S, min(n, (r+1)*S))
-inline uint64_t shard_size(uint64_t n, int world) { return ceil_div(n, (uint64_t)world); }
+// contiguous shards of S = ceil(n/world) rounded up to a multiple of 32 states (a
+// rank's slice of a bit-packed id vector is whole words): rank r owns
+// [r*S, min(n, (r+1)*S))
+inline uint64_t shard_size(uint64_t n, int world) {
+  return ceil_div(ceil_div(n, (uint64_t)world), 32) * 32;
+}
 // `loc` = the owned rows (n = owned states, GLOBAL targets); canonical labels of the
 // owned states into canon_dev (device, loc.n entries)
 AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const Deadline& dl,

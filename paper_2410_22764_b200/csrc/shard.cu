@@ -26,37 +26,47 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// ids of the all-gathered block vector at kBits per state (1/2/4/8/16/32, packed
+// 32/kBits per word, little-endian: 8/16 bits are plain byte / short arrays)
+template <int kBits>
+__device__ __forceinline__ uint32_t full_id(const uint32_t* __restrict__ full, uint64_t t) {
+  if (kBits == 32) return full[t];
+  constexpr uint32_t per = 32 / kBits;
+  return (full[t / per] >> ((uint32_t)(t % per) * kBits)) & ((1u << kBits) - 1u);
+}
+
 // Exact packed keys while (k+1) * bits(B-1) <= 63 (the early passes): no signature
 // rows to route or verify; ids are read from the all-gathered block vector at its
-// narrow width (1/2/4 bytes while B <= 2^8 / 2^16 / 2^32)
-template <typename Id>
+// narrow width (1/2/4/8/16/32 bits: the early passes' vectors stay L2-resident)
+template <int kBits>
 __global__ void __launch_bounds__(256) shard_packed_kernel(
-    const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k, const Id* __restrict__ block_full,
+    const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k, const uint32_t* __restrict__ full,
     uint64_t lo, uint32_t w, uint32_t ranks, unsigned long long* __restrict__ keys,
     uint32_t* __restrict__ dest) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += stride) {
-    unsigned long long key = block_full[lo + i];
-    for (uint32_t a = 0; a < k; ++a) key = (key << w) | block_full[delta[(uint64_t)a * n_local + i]];
+    unsigned long long key = full_id<kBits>(full, lo + i);
+    for (uint32_t a = 0; a < k; ++a)
+      key = (key << w) | full_id<kBits>(full, delta[(uint64_t)a * n_local + i]);
     keys[i] = key + 1ull;  // never 0: 0 marks an empty table slot
     dest[i] = (uint32_t)__umul64hi(mix64(key ^ 0xD1B54A32D192ED03ull), ranks);
   }
 }
 
-template <typename Id>
+template <int kBits>
 __global__ void __launch_bounds__(256) shard_sig_kernel_w(
     const uint32_t* __restrict__ delta, uint64_t n_local, uint32_t k,
-    const Id* __restrict__ block_full, uint64_t lo, uint64_t seed, uint32_t ranks,
+    const uint32_t* __restrict__ full, uint64_t lo, uint64_t seed, uint32_t ranks,
     unsigned long long* __restrict__ keys, uint32_t* __restrict__ sig,
     uint32_t* __restrict__ dest) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += stride) {
-    const uint32_t b = block_full[lo + i];
+    const uint32_t b = full_id<kBits>(full, lo + i);
     uint32_t* row = sig + i * (uint64_t)(k + 1);
     row[0] = b;
     unsigned long long h = mix64(seed * kGolden + b);
     for (uint32_t a = 0; a < k; ++a) {
-      const uint32_t s = block_full[delta[(uint64_t)a * n_local + i]];
+      const uint32_t s = full_id<kBits>(full, delta[(uint64_t)a * n_local + i]);
       row[a + 1] = s;
       h = mix64(h + kGolden + s);
     }
@@ -343,50 +353,41 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 
 namespace dfm {
 void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
-                     const void* block_full, uint32_t id_bytes, uint64_t lo, uint64_t seed,
+                     const void* block_full, uint32_t id_bits, uint64_t lo, uint64_t seed,
                      uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
                      void* dest_out) {
-    if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
-    if (id_bytes != 1 && id_bytes != 2 && id_bytes != 4)
-      throw Error(DFM_ERR_INVALID, "id_bytes must be 1, 2 or 4");
-    if (pack_bits && (uint64_t)(k + 1) * pack_bits > 63)
-      throw Error(DFM_ERR_INVALID, "packed key does not fit 63 bits");
-    if (n_local == 0) return;
-    const auto* d = static_cast<const uint32_t*>(delta_local);
-    auto* keys = static_cast<unsigned long long*>(keys_out);
-    auto* dest = static_cast<uint32_t*>(dest_out);
-    const unsigned g = grid_for(ctx, n_local);
-    if (pack_bits) {
-      ProfScope p(ctx, "sig", n_local * (4ull * k + (uint64_t)id_bytes * (k + 1) + 8 + 4));
-      if (id_bytes == 1)
-        shard_packed_kernel<uint8_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint8_t*>(block_full), lo, pack_bits, ranks, keys, dest);
-      else if (id_bytes == 2)
-        shard_packed_kernel<uint16_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint16_t*>(block_full), lo, pack_bits, ranks, keys,
-            dest);
-      else
-        shard_packed_kernel<uint32_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint32_t*>(block_full), lo, pack_bits, ranks, keys,
-            dest);
-    } else {
-      auto* sig = static_cast<uint32_t*>(sig_out);
-      ProfScope p(ctx, "sig", n_local * (4ull * k + (uint64_t)id_bytes * (k + 1) + 8 +
-                                         4ull * (k + 1) + 4));
-      if (id_bytes == 1)
-        shard_sig_kernel_w<uint8_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint8_t*>(block_full), lo, seed, ranks, keys, sig, dest);
-      else if (id_bytes == 2)
-        shard_sig_kernel_w<uint16_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint16_t*>(block_full), lo, seed, ranks, keys, sig,
-            dest);
-      else
-        shard_sig_kernel_w<uint32_t><<<g, 256, 0, ctx.stream>>>(
-            d, n_local, k, static_cast<const uint32_t*>(block_full), lo, seed, ranks, keys, sig,
-            dest);
-    }
-    DFM_LAUNCH_CHECK();
+  if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
+  if (id_bits != 1 && id_bits != 2 && id_bits != 4 && id_bits != 8 && id_bits != 16 && id_bits != 32)
+    throw Error(DFM_ERR_INVALID, "id_bits must be 1, 2, 4, 8, 16 or 32");
+  if (pack_bits && (uint64_t)(k + 1) * pack_bits > 63)
+    throw Error(DFM_ERR_INVALID, "packed key does not fit 63 bits");
+  if (n_local == 0) return;
+  const auto* d = static_cast<const uint32_t*>(delta_local);
+  const auto* full = static_cast<const uint32_t*>(block_full);
+  auto* keys = static_cast<unsigned long long*>(keys_out);
+  auto* dest = static_cast<uint32_t*>(dest_out);
+  auto* sig = static_cast<uint32_t*>(sig_out);
+  const unsigned g = grid_for(ctx, n_local);
+  // delta 4k + k+1 id gathers (4-byte requests) + key 8 + dest 4 (+ row when hashed)
+  ProfScope p(ctx, "sig", n_local * (8ull * k + 4 + 8 + 4 + (pack_bits ? 0 : 4ull * (k + 1))));
+#define DFM_SHARD_KEYS(B)                                                                    \
+  if (pack_bits)                                                                             \
+    shard_packed_kernel<B><<<g, 256, 0, ctx.stream>>>(d, n_local, k, full, lo, pack_bits, ranks, \
+                                                      keys, dest);                           \
+  else                                                                                       \
+    shard_sig_kernel_w<B><<<g, 256, 0, ctx.stream>>>(d, n_local, k, full, lo, seed, ranks, keys, \
+                                                     sig, dest);
+  switch (id_bits) {
+    case 1: DFM_SHARD_KEYS(1) break;
+    case 2: DFM_SHARD_KEYS(2) break;
+    case 4: DFM_SHARD_KEYS(4) break;
+    case 8: DFM_SHARD_KEYS(8) break;
+    case 16: DFM_SHARD_KEYS(16) break;
+    default: DFM_SHARD_KEYS(32) break;
   }
+#undef DFM_SHARD_KEYS
+  DFM_LAUNCH_CHECK();
+}
 
 void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key_bits,
                         void* label_out, uint64_t* groups_out) {
@@ -515,8 +516,10 @@ int dfm_shard_signature_ex(dfm_ctx* c, const void* delta_local, uint64_t n_local
                            uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
                            void* dest_out) {
   return guarded_shard(c, [&](Ctx& ctx) {
-    shard_signature(ctx, delta_local, n_local, k, block_full, id_bytes, lo, seed, ranks, pack_bits,
-                    keys_out, sig_out, dest_out);
+    if (id_bytes != 1 && id_bytes != 2 && id_bytes != 4)
+      throw Error(DFM_ERR_INVALID, "id_bytes must be 1, 2 or 4");
+    shard_signature(ctx, delta_local, n_local, k, block_full, 8 * id_bytes, lo, seed, ranks,
+                    pack_bits, keys_out, sig_out, dest_out);
   });
 }
 

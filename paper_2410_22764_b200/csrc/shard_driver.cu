@@ -5,8 +5,8 @@
 // Rank r owns the contiguous states [r*S, min(n, (r+1)*S)), S = ceil(n/world), and
 // their rows (GLOBAL target ids).  Each pass of the reference loop
 // (min_sort.hpp:93-118):
-//   1. all-gather the owned block ids at the narrowest width holding B ids
-//      (u8 / u16 / u32) -> the full id vector on every rank        [NVLink]
+//   1. all-gather the owned block ids bit-packed at the narrowest width holding B
+//      ids (1/2/4/8/16/32 bits) -> the full id vector on every rank  [NVLink]
 //   2. per owned state its key: the exact packed (block, successor ids) while
 //      (k+1)*bits(B-1) <= 63, else a 64-bit hash + the signature row, and the
 //      rank dest(key) that groups it                                  [HBM, gathers]
@@ -74,12 +74,22 @@ __global__ void init_block_kernel(const uint8_t* __restrict__ acc, uint64_t n, b
     block[i] = split ? (acc[i] == 0 ? 1u : 0u) : 0u;  // min_sort.hpp:80-88
 }
 
-template <typename Id>
-__global__ void narrow_kernel(const uint32_t* __restrict__ block, uint64_t n, uint64_t S,
-                              Id* __restrict__ out) {
+// this rank's ids packed at kBits per state (32/kBits per word; S is a multiple of 32)
+template <int kBits>
+__global__ void pack_ids_kernel(const uint32_t* __restrict__ block, uint64_t n, uint64_t S,
+                                uint32_t* __restrict__ out) {
+  constexpr uint32_t per = 32 / kBits;
+  const uint64_t words = S / per;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < S; i += stride)
-    out[i] = i < n ? (Id)block[i] : (Id)0;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t word = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < per; ++e) {
+      const uint64_t i = w * per + e;
+      if (i < n) word |= (kBits == 32 ? block[i] : block[i] << (e * kBits));
+    }
+    out[w] = word;
+  }
 }
 
 __global__ void dest_hist_kernel(const uint32_t* __restrict__ dest, uint64_t n, uint32_t world,
@@ -248,24 +258,32 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
     // ---- 1. all-gather of the owned ids at the narrowest width
     const int w = std::max(1, bitw(B - 1));
     const bool packed = (uint64_t)(k + 1) * w <= 63;
-    const uint32_t idb = B <= 256 ? 1 : B <= 65536 ? 2 : 4;
-    void* send_ids = ctx.slot("sd.ids_send", S * idb);
-    void* full = ctx.slot("sd.ids_full", (uint64_t)world * S * idb);
+    // ids travel (and are gathered) at 1/2/4/8/16/32 bits: pass 1's vector is a bitmap
+    const uint32_t ib = B <= 2 ? 1 : B <= 4 ? 2 : B <= 16 ? 4 : B <= 256 ? 8 : B <= 65536 ? 16 : 32;
+    const uint64_t slice = S * ib / 8;  // bytes per rank
+    void* send_ids = ctx.slot("sd.ids_send", slice);
+    void* full = ctx.slot("sd.ids_full", (uint64_t)world * slice);
     {
-      ProfScope p(ctx, "allgather", S * idb * (uint64_t)world);
-      const unsigned g = sgrid(ctx, S);
-      if (idb == 1) narrow_kernel<uint8_t><<<g, 256, 0, st>>>(block, nl, S, static_cast<uint8_t*>(send_ids));
-      else if (idb == 2) narrow_kernel<uint16_t><<<g, 256, 0, st>>>(block, nl, S, static_cast<uint16_t*>(send_ids));
-      else narrow_kernel<uint32_t><<<g, 256, 0, st>>>(block, nl, S, static_cast<uint32_t*>(send_ids));
+      ProfScope p(ctx, "allgather", slice * (uint64_t)world);
+      const unsigned g = sgrid(ctx, S * ib / 32);
+      auto* sw = static_cast<uint32_t*>(send_ids);
+      switch (ib) {
+        case 1: pack_ids_kernel<1><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+        case 2: pack_ids_kernel<2><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+        case 4: pack_ids_kernel<4><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+        case 8: pack_ids_kernel<8><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+        case 16: pack_ids_kernel<16><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+        default: pack_ids_kernel<32><<<g, 256, 0, st>>>(block, nl, S, sw); break;
+      }
       DFM_LAUNCH_CHECK();
-      comm.all_gather(send_ids, full, S * idb, st);
+      comm.all_gather(send_ids, full, slice, st);
     }
     // ---- 2. keys (+ rows) and destinations of the owned states
     const uint32_t words = packed ? 0 : k + 1;
     auto* keys = ctx.slot_t<unsigned long long>("sd.keys", std::max<uint64_t>(nl, 1));
     uint32_t* sig = words ? ctx.slot_t<uint32_t>("sd.sig", std::max<uint64_t>(nl * words, 1)) : nullptr;
     uint32_t* dest = ctx.slot_t<uint32_t>("sd.dest", std::max<uint64_t>(nl, 1));
-    shard_signature(ctx, loc.delta, nl, k, full, idb, lo, seed, (uint32_t)world,
+    shard_signature(ctx, loc.delta, nl, k, full, ib, lo, seed, (uint32_t)world,
                     packed ? (uint32_t)w : 0u, keys, sig, dest);
     // ---- 3. route to the grouping ranks
     const unsigned long long* rkeys = keys;

@@ -46,11 +46,44 @@ struct SigParams {
   uint64_t seed;
   uint64_t* __restrict__ keys;
   uint32_t* __restrict__ sig;  // (k+1) words per active item, hashed mode only
+  const uint32_t* __restrict__ mirror;  // successor ids at kBits < 32 (32/kBits per word)
 };
+
+// successor id from the packed mirror (kBits < 32: L2-resident at 1/4/8/16 bits while
+// B <= 2/16/256/65536 — 12.5 / 50 / 100 / 200 MB at 1e8 states) or the block array
+template <int kBits>
+__device__ __forceinline__ uint32_t succ_id(const SigParams& p, uint32_t t) {
+  if (kBits == 32) return p.block[t];
+  constexpr uint32_t per = 32 / kBits;
+  return (p.mirror[t / per] >> ((t % per) * kBits)) & ((1u << kBits) - 1u);
+}
+
+template <int kBits>
+__global__ void __launch_bounds__(256) rmirror_kernel(const uint32_t* __restrict__ block, uint64_t n,
+                                                      uint32_t* __restrict__ out) {
+  constexpr int per = 32 / kBits;
+  const uint64_t words = (n + per - 1) / per;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += stride) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < per; ++e) {
+      const uint64_t q = w * per + e;
+      if (q < n) word |= block[q] << (e * kBits);
+    }
+    out[w] = word;
+  }
+}
+
+__global__ void __launch_bounds__(256) riota_kernel(uint32_t* __restrict__ out, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    out[q] = (uint32_t)q;
+}
 
 // K1: signature gather + key build, one thread per active state.  delta rows
 // are read coalesced (active list is ascending in q); block[] is gathered.
-template <bool kHashed>
+template <bool kHashed, int kBits>
 __global__ void __launch_bounds__(256) sig_kernel(SigParams p) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += stride) {
@@ -59,14 +92,14 @@ __global__ void __launch_bounds__(256) sig_kernel(SigParams p) {
     if (!kHashed) {
       uint64_t key = b;
       for (uint32_t a = 0; a < p.k; ++a)
-        key = (key << p.w) | p.block[p.delta[(uint64_t)a * p.n + q]];
+        key = (key << p.w) | succ_id<kBits>(p, p.delta[(uint64_t)a * p.n + q]);
       p.keys[i] = key;
     } else {
       uint32_t* row = p.sig + i * (uint64_t)(p.k + 1);
       row[0] = b;
       uint64_t h = mix64(p.seed * kGolden + b);
       for (uint32_t a = 0; a < p.k; ++a) {
-        const uint32_t s = p.block[p.delta[(uint64_t)a * p.n + q]];
+        const uint32_t s = succ_id<kBits>(p, p.delta[(uint64_t)a * p.n + q]);
         row[a + 1] = s;
         h = mix64(h + kGolden + s);
       }
@@ -280,14 +313,40 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
     uint32_t* act_next = act_buf[act_sel ^ 1];
     if (m > 0) {
       if (!packed && sig == nullptr) sig = ctx.slot_t<uint32_t>("sp.sig", n * (uint64_t)(k + 1));
-      SigParams sp{d.delta, n, k, block, act, m, w, seed, keysA, sig};
+      // narrow mirror of the ids for the successor gathers (rebuilt each pass)
+      const int mb = B <= 2 ? 1 : B <= 16 ? 4 : B <= 256 ? 8 : B <= 65536 ? 16 : 32;
+      uint32_t* mirror = nullptr;
+      if (mb < 32) {
+        mirror = ctx.slot_t<uint32_t>("sp.mirror", ceil_div(n, 32 / mb));
+        ProfScope p(ctx, "mirror", n * 4 + n * mb / 8);
+        const unsigned g = grid_for(ctx, ceil_div(n, 32 / mb));
+        if (mb == 1) rmirror_kernel<1><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+        else if (mb == 4) rmirror_kernel<4><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+        else if (mb == 8) rmirror_kernel<8><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+        else rmirror_kernel<16><<<g, 256, 0, ctx.stream>>>(block, n, mirror);
+        DFM_LAUNCH_CHECK();
+      }
+      SigParams sp{d.delta, n, k, block, act, m, w, seed, keysA, sig, mirror};
       {
         // delta stream 4k + successor-block gather 4k + own block 4 + active id 4 + key 8
         // (+ signature row 4(k+1) when hashed) per active state
         ProfScope p(ctx, "sig",
                     m * (8ull * k + 4 + (act ? 4 : 0) + 8 + (packed ? 0 : 4ull * (k + 1))));
-        if (packed) sig_kernel<false><<<grid_for(ctx, m), 256, 0, ctx.stream>>>(sp);
-        else sig_kernel<true><<<grid_for(ctx, m), 256, 0, ctx.stream>>>(sp);
+        const unsigned g = grid_for(ctx, m);
+#define DFM_SIG(H)                                                                   \
+  switch (mb) {                                                                      \
+    case 1: sig_kernel<H, 1><<<g, 256, 0, ctx.stream>>>(sp); break;                  \
+    case 4: sig_kernel<H, 4><<<g, 256, 0, ctx.stream>>>(sp); break;                  \
+    case 8: sig_kernel<H, 8><<<g, 256, 0, ctx.stream>>>(sp); break;                  \
+    case 16: sig_kernel<H, 16><<<g, 256, 0, ctx.stream>>>(sp); break;                \
+    default: sig_kernel<H, 32><<<g, 256, 0, ctx.stream>>>(sp); break;                \
+  }
+        if (packed) {
+          DFM_SIG(false)
+        } else {
+          DFM_SIG(true)
+        }
+#undef DFM_SIG
         DFM_LAUNCH_CHECK();
       }
       const bool alt = prims::radix_sort_pairs(ctx, keysA, valsA, keysB, valsB, m, bits, true);
@@ -345,7 +404,14 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
     act_sel ^= 1;
   }
   out.canon_dev = ctx.slot_t<uint32_t>("canon", n);
-  out.num_blocks = canonicalize_dev(ctx, block, n, out.canon_dev);
+  if (B == n) {  // every block a singleton: the canonical labels are 0..n-1
+    ProfScope p(ctx, "canon", n * 4);
+    riota_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(out.canon_dev, n);
+    DFM_LAUNCH_CHECK();
+    out.num_blocks = (uint32_t)n;
+  } else {
+    out.num_blocks = canonicalize_dev(ctx, block, n, out.canon_dev);
+  }
   out.status = DFM_STATUS_OK;
   return out;
 }

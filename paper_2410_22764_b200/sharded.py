@@ -189,8 +189,9 @@ class ShardedResult:
 
 
 def shard_bounds(n_total: int, world: int, rank: int):
-    """Rank r owns [r*S, min(n, (r+1)*S)), S = ceil(n/world) (dfm_shard_bounds)."""
-    S = -(-n_total // world)
+    """Rank r owns [r*S, min(n, (r+1)*S)), S = ceil(n/world) rounded up to a multiple of
+    32 (dfm_shard_bounds: a rank's slice of a bit-packed id vector is whole words)."""
+    S = -(-(-(-n_total // world)) // 32) * 32
     lo = min(n_total, rank * S)
     return lo, min(n_total, lo + S)
 

@@ -18,7 +18,8 @@ from oracle import oracle as O  # noqa: E402
 
 small = "--small" in sys.argv
 eng = dfm.Engine(0)
-MIN = dfm.PrOptions(policy=dfm.RacePolicy.deterministic_min)
+MIN = dfm.PrOptions(policy=dfm.RacePolicy.deterministic_min, timeout_ms=3_600_000)
+LIM = dfm.Limits(timeout_ms=3_600_000)
 cases = [("random", O.random_dfa(3000, 3, 7, 0.5)),      # small sortPR kernel, fused naive
          ("fib", O.fib_dfa(12)),                           # cluster naive (n <= 4096), trans
          ("comb", O.comb_dfa(2000, 3))]
@@ -28,19 +29,19 @@ if not small:
 for name, (delta, acc) in cases:
     d = dfm.Dfa(acc.size, delta.shape[0], delta, acc, 0)
     ref = O.sort_pr(delta, acc)
-    r = eng.sort_pr(d)
+    r = eng.sort_pr(d, dfm.SortOptions(timeout_ms=3_600_000))
     assert (r.partition.block == ref.block).all(), name
     if acc.size <= 300_000:
         rn = eng.naive_pr(d, MIN)
         rm = O.naive_pr(delta, acc, "min")
         assert (rn.partition.block == rm.block).all() and rn.stats.iterations == rm.iterations
-        assert (eng.naive_pr_cas(d).partition.block == ref.block).all(), name
-        rt = eng.trans_pr(d, MIN)
+        assert (eng.naive_pr_cas(d, timeout_ms=3_600_000).partition.block == ref.block).all(), name
+        rt = eng.trans_pr(d, MIN, LIM)
         assert (rt.partition.block == ref.block).all(), name
     if acc.size <= 256:
         for engine in ("bit", "tensor"):
             eng.set_trans_engine(engine)
-            rt = eng.trans_minimize(d)
+            rt = eng.trans_minimize(d, LIM)
             assert (rt.partition.block == ref.block).all(), (name, engine)
         eng.set_trans_engine("auto")
     print("ok", name, acc.size, flush=True)
