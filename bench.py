@@ -264,7 +264,18 @@ def cpu_baseline_for(args, delta, acc, our_iters, budget_ms=60_000):
                 "sample": f"reference {args.algo}, {R.worker_count()} threads: {smp}",
                 "timing": "wall time of the reference call incl. its final canonicalize"})
     R.set_threads(1)
-    v1, ms1, it1, smp1 = ref_bounded(R, args, delta, acc, budget_ms)
+    if acc.size * delta.shape[0] > 100_000_000 and args.family in ("random", "vlts", "chain"):
+        # one reference pass at 1 thread would take ~minutes here: a 10x smaller
+        # instance of the same family (stated in the sample)
+        a1 = argparse.Namespace(**vars(args))
+        a1.n = (acc.size // 10 if args.family != "vlts"
+                else max(args.vlts_m, acc.size // 10 // args.vlts_m * args.vlts_m))
+        d1, c1 = ref_generate(R, a1)
+        v1, ms1, it1, smp1 = ref_bounded(R, a1, d1, c1, budget_ms)
+        smp1 = f"{smp1} of a 10x smaller instance of the family ({c1.size} states)"
+        del d1, c1
+    else:
+        v1, ms1, it1, smp1 = ref_bounded(R, args, delta, acc, budget_ms)
     out["threads_1"] = {"value": v1, "ms": ms1, "passes": it1,
                         "sample": f"reference {args.algo}, 1 thread: {smp1}"}
     R.set_threads(0)

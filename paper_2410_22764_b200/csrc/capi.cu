@@ -97,7 +97,9 @@ bool host_pinned_ptr(const void* p) {
 
 unsigned stage_threads() {
   if (const char* e = getenv("DFM_STAGE_THREADS")) return std::max(1, atoi(e));
-  return std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2));
+  // measured on the 16-core B200 hosts (tools/e2e_stage.py, profiles/r02h): 4 / 8 / 12 /
+  // 16 threads -> 84 / 69 / 66 / 69 ms e2e for random_dfa(1e8, 4) from pageable rows
+  return std::max(1u, std::min(12u, std::thread::hardware_concurrency() * 3 / 4));
 }
 
 void par_memcpy(void* dst, const void* src, size_t bytes, unsigned T) {
@@ -198,6 +200,7 @@ class PageableStager final : public ChunkGate {
 struct StageRes {
   cudaEvent_t ev[kRing] = {};
   bool used[kRing] = {};
+  uint32_t next = 0;
   std::unique_ptr<PageableStager> stager;
   ~StageRes() {
     stager.reset();
@@ -211,7 +214,7 @@ struct StageRes {
 void staged_h2d(Ctx& ctx, void* dst, const void* src, uint64_t bytes, cudaStream_t stream,
                 char* ring, uint64_t slot_bytes, StageRes& res) {
   const unsigned T = stage_threads();
-  uint32_t s = 0;
+  uint32_t& s = res.next;  // ring cursor continues across pieces
   for (uint64_t off = 0; off < bytes; off += slot_bytes, s = (s + 1) % kRing) {
     const uint64_t len = std::min(slot_bytes, bytes - off);
     if (res.used[s]) DFM_CUDA(cudaEventSynchronize(res.ev[s]));
@@ -247,8 +250,10 @@ DevDfa upload(Ctx& ctx, const dfm_dfa* d, const std::string& prefix, bool own_al
     dd.acc = ctx.slot_t<uint8_t>(prefix + ".acc", n);
     dd.owns = false;
   }
-  for (uint64_t a = 0; a < k; ++a) h2d_rows(ctx, dd.delta + a * n, d->delta[a], n * 4);
-  h2d_rows(ctx, dd.acc, d->accepting, n);
+  std::vector<H2DPiece> pieces;
+  for (uint64_t a = 0; a < k; ++a) pieces.push_back({dd.delta + a * n, d->delta[a], n * 4});
+  pieces.push_back({dd.acc, d->accepting, n});
+  h2d_batch(ctx, pieces);
   validate_targets(ctx, dd);
   return dd;
 }
@@ -431,17 +436,31 @@ uint64_t sm_draw(uint64_t seed, uint64_t j) {
 // host -> device copy of a possibly pageable buffer (synchronous for the host when
 // pageable; asynchronous on `stream` when pinned)
 void h2d_rows(Ctx& ctx, void* dst, const void* src, uint64_t bytes) {
+  h2d_batch(ctx, {H2DPiece{dst, src, bytes}});
+}
+
+// several host pieces in one go: pinned ones are DMA'd directly, pageable ones go
+// through ONE pinned ring back to back (the copy of slot s+1 overlaps the DMA of
+// slot s across piece boundaries), one synchronisation at the end
+void h2d_batch(Ctx& ctx, const std::vector<H2DPiece>& pieces) {
   cudaStream_t stream = ctx.stream;
-  if (bytes < (16u << 20) || host_pinned_ptr(src)) {
-    DFM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
-    return;
-  }
-  const uint64_t slot = 32ull << 20;
-  char* ring = static_cast<char*>(ctx.host_pinned(kRing * slot));
+  const uint64_t slot = 64ull << 20;
+  char* ring = nullptr;
   std::unique_ptr<StageRes> holder;
-  StageRes& res = new_stage_res(holder);
-  staged_h2d(ctx, dst, src, bytes, stream, ring, slot, res);
-  DFM_CUDA(cudaStreamSynchronize(stream));  // the ring is reused by the next call
+  StageRes* res = nullptr;
+  for (const H2DPiece& p : pieces) {
+    if (p.bytes == 0) continue;
+    if (p.bytes < (16u << 20) || host_pinned_ptr(p.src)) {
+      DFM_CUDA(cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyHostToDevice, stream));
+      continue;
+    }
+    if (ring == nullptr) {
+      ring = static_cast<char*>(ctx.host_pinned(kRing * slot));
+      res = &new_stage_res(holder);
+    }
+    staged_h2d(ctx, p.dst, p.src, p.bytes, stream, ring, slot, *res);
+  }
+  if (ring) DFM_CUDA(cudaStreamSynchronize(stream));  // the ring is reused by the next call
 }
 
 }  // namespace dfm

@@ -218,6 +218,12 @@ void save_dfa_bin(Ctx& ctx, const DevDfa& dd, const char* path);
 // host -> device copy on ctx.stream of a possibly pageable host buffer (pageable:
 // staged by several host threads through a pinned ring, synchronous for the host)
 void h2d_rows(Ctx& ctx, void* dst, const void* src, uint64_t bytes);
+struct H2DPiece {
+  void* dst;
+  const void* src;
+  uint64_t bytes;
+};
+void h2d_batch(Ctx& ctx, const std::vector<H2DPiece>& pieces);
 // sharded sortPR primitives (shard.cu) and the C++ driver (shard_driver.cu)
 void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
                      const void* block_full, uint32_t id_bits, uint64_t lo, uint64_t seed,

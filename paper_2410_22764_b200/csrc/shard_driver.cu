@@ -600,11 +600,13 @@ int dfm_sort_pr_sharded(dfm_ctx* c, uint64_t n_total, const dfm_dfa* local, int 
     loc.delta = ctx.slot_t<uint32_t>("sd.in_delta", std::max<uint64_t>(nl * k, 1));
     loc.acc = ctx.slot_t<uint8_t>("sd.in_acc", std::max<uint64_t>(nl, 1));
     loc.owns = false;
+    std::vector<H2DPiece> pieces;
     for (uint64_t a = 0; a < k; ++a) {
       if (local->delta[a] == nullptr && nl) throw Error(DFM_ERR_INVALID, "null row");
-      if (nl) h2d_rows(ctx, loc.delta + a * nl, local->delta[a], nl * 4);
+      pieces.push_back({loc.delta + a * nl, local->delta[a], nl * 4});
     }
-    if (nl) h2d_rows(ctx, loc.acc, local->accepting, nl);
+    pieces.push_back({loc.acc, local->accepting, nl});
+    if (nl) h2d_batch(ctx, pieces);
     uint32_t* canon = ctx.slot_t<uint32_t>("sd.canon", std::max<uint64_t>(nl, 1));
     AlgoOut o = run_sort_pr_sharded(ctx, n_total, loc, dl, canon, force_protocol());
     if (o.status == DFM_STATUS_OK && block_out) labels_out(ctx, canon, n_total, nl, gather_all != 0, block_out);
