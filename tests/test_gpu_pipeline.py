@@ -76,3 +76,29 @@ def test_pipelined_upload_single_initial_block(eng, p):
     assert r.stats.status == dfm.RunStatus.ok
     assert (r.partition.num_blocks, r.stats.iterations) == (1, 1)
     assert not r.partition.block.any()
+
+
+def test_pinned_and_pageable_rows_give_the_same_result(eng):
+    """The same DFA from pageable rows (staged by the library through its pinned ring on
+    a stager thread) and from pinned rows (DMA'd directly): identical results."""
+    import torch
+    n, k = 17_000_001, 4
+    dd = eng.random_dfa_device(n, k, 31, 0.5)
+    nb, it, lab = _device_result(eng, dd, n)
+    host = dd.download()
+    dd.free()
+    pd = torch.empty((k, n), dtype=torch.int32, pin_memory=True)
+    pa = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    pd.numpy()[:] = host.delta.view(np.int32)
+    pa.numpy()[:] = host.accepting
+    pinned = dfm.Dfa(n, k, pd.numpy().view(np.uint32), pa.numpy(), 0)
+    for d in (host, pinned):
+        r = eng.sort_pr(d)
+        assert (r.partition.num_blocks, r.stats.iterations) == (nb, it)
+        assert (r.partition.block == lab).all()
+    # the one-shot upload (other algorithms) from both kinds of rows
+    small = dfm.Dfa(n, k, host.delta, host.accepting, 0)
+    for d in (small, pinned):
+        dd2 = eng.upload(d)
+        assert _device_result(eng, dd2, n)[2].tolist()[:1000] == lab.tolist()[:1000]
+        dd2.free()
