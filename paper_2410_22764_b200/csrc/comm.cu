@@ -79,7 +79,7 @@ class NcclComm final : public Comm {
     static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(&uid, id, sizeof(uid));
     nccl_check(nccl().CommInitRank(&comm_, w, uid, r), "ncclCommInitRank");
-    DFM_CUDA(cudaMalloc(&scratch_, 4096));
+    DFM_CUDA(cudaMalloc(&scratch_, kScratch));
   }
   ~NcclComm() override {
     if (scratch_) cudaFree(scratch_);
@@ -107,7 +107,7 @@ class NcclComm final : public Comm {
   }
   void all_gather_host(const uint64_t* mine, uint64_t* all, int count, cudaStream_t s) override {
     const uint64_t b = 8ull * count;
-    if (b * (world + 1) > 4096) throw Error(DFM_ERR_INVALID, "all_gather_host: too many values");
+    if (b * (world + 1) > kScratch) throw Error(DFM_ERR_INVALID, "all_gather_host: too many values");
     char* dev = static_cast<char*>(scratch_);
     DFM_CUDA(cudaMemcpyAsync(dev, mine, b, cudaMemcpyHostToDevice, s));
     all_gather(dev, dev + b, b, s);
@@ -116,6 +116,7 @@ class NcclComm final : public Comm {
   }
 
  private:
+  static constexpr uint64_t kScratch = 64ull << 10;  // (world + 1) * count u64 values
   ncclComm_t comm_ = nullptr;
   void* scratch_ = nullptr;
 };

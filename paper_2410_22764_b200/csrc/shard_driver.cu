@@ -305,9 +305,9 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
       const bool alt = nl ? prims::radix_sort_pairs(ctx, d64, ord_a, d64b, ord_b, nl, dbits, true)
                           : false;
       order = alt ? ord_b : ord_a;
-      DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars, counts_dev, 8ull * world, cudaMemcpyDeviceToHost, st));
+      DFM_CUDA(cudaMemcpyAsync(send_cnt.data(), counts_dev, 8ull * world, cudaMemcpyDeviceToHost,
+                               st));
       ctx.sync();
-      for (int r = 0; r < world; ++r) send_cnt[r] = ctx.h_scalars[r];
       comm.all_gather_host(send_cnt.data(), cnt_all.data(), world, st);
       nrecv = 0;
       for (int r = 0; r < world; ++r) {
