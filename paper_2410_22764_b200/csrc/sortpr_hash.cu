@@ -945,6 +945,11 @@ __global__ void __launch_bounds__(256) direct_keys_kernel(
 // opt-in (DFM_SORTPR_FILT_FUSED=1): the level-0 filter set inside lay_sig is exact but
 // measured slower — lay_sig 6.7 -> 8.1 ms of the step with the L2 atomics in it,
 // against the 0.95 ms filt_set sweep it replaces (random_dfa(1e8, 4); profiles/r02f)
+bool pass_timing() {
+  const char* e = getenv("DFM_SORTPR_PASS_TIMING");
+  return e != nullptr && e[0] == '1';
+}
+
 bool filt_fused_enabled() {
   const char* e = getenv("DFM_SORTPR_FILT_FUSED");
   return e != nullptr && e[0] == '1';
@@ -1844,6 +1849,13 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 1, sc + 1, 64, cudaMemcpyDeviceToHost, ctx.stream));
+    if (pass_timing()) {  // DFM_SORTPR_PASS_TIMING=1: host timestamps at each pass end
+      ctx.sync();
+      const bool lay_done = lay_ready == nullptr || cudaEventQuery(lay_ready) == cudaSuccess;
+      fprintf(stderr, "pass %llu done at %.3f ms (m=%llu, layout %s)\n",
+              (unsigned long long)out.iterations + 1, dl.elapsed(), (unsigned long long)m,
+              lay_done ? "ready" : "pending");
+    }
     if (d.nready) DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 40, d.bad, 8, cudaMemcpyDeviceToHost,
                                            ctx.stream));
     ctx.sync();
