@@ -539,6 +539,11 @@ def run_ours(args, rank: int, world: int, local: int):
                "pinned": {"value": transitions / (ms_pin / 1e3), "ms_per_step": ms_pin,
                           "host_memory": "pinned (cudaMallocHost rows)"}}
         del out_pin, pin_delta, pin_acc, hd_pin, hd_page
+        cpp = cpp_reference_types_e2e(args)
+        if cpp is not None:
+            assert (cpp["passes"], cpp["blocks"]) == (iters, nb), cpp
+            cpp["value"] = transitions / (cpp["ms_mean"] / 1e3)
+            e2e["cpp_reference_types"] = cpp
 
     if rank != 0:
         dd.free()
@@ -570,6 +575,32 @@ def run_ours(args, rank: int, world: int, local: int):
             "step_ms": step_ms, "lib": dfm.lib_path()}
     print(json.dumps(line), flush=True)
     dd.free()
+
+
+def cpp_reference_types_e2e(args):
+    """The C++ drop-in end to end (build/e2e_ref, tools/cpp/e2e_ref.cpp): the reference's
+    own dfamin::Dfa (std::vector rows) from its generator, dfamin::b200::sort_pr, wall
+    clock around the call.  None when the tool was not built or the workload has no
+    generator there."""
+    tool = os.path.join(ROOT, "build", "e2e_ref")
+    if args.algo != "sort" or not os.path.exists(tool):
+        return None
+    if args.family == "random":
+        cmd = [tool, "random", args.n, args.k, args.seed, 3]
+    elif args.family == "vlts":
+        cmd = [tool, "vlts", args.vlts_m, args.n, args.k, 3]
+    else:
+        return None
+    try:
+        r = subprocess.run([str(x) for x in cmd], capture_output=True, text=True, timeout=900)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # pragma: no cover
+        return {"error": repr(exc)}
+    out["how"] = ("tools/cpp/e2e_ref.cpp: the reference's dfamin::Dfa from its own generator "
+                  "(pageable std::vector rows), dfamin::b200::sort_pr (include/dfamin_b200.hpp "
+                  "with DFAMIN_B200_USE_REFERENCE_TYPES), wall clock around the call incl. "
+                  "upload, every pass and the canonical partition in the MinResult")
+    return out
 
 
 def roofline_of(args, prof, ms_per_step, total_ms, iters, executed, peak, peak_src):
