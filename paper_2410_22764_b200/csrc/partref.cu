@@ -332,6 +332,7 @@ struct FusedArgs {
   const uint32_t* pred_src;
   uint32_t* mark;
   uint32_t dirty_from;  // first pass that writes marks (it evaluates every state)
+  bool own_label;       // kOne: keep the state's own label word in a register
 };
 
 // label words carry the previous pass's split flag in bit 31 (state ids < 2^31), so
@@ -354,11 +355,15 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
   // state splits — taking the leader-row load off the pass's dependent chain
   constexpr bool one = kOne;  // the host launches kOne only when n <= resident threads
   uint32_t cl = 0xFFFFFFFFu, crow[4] = {0, 0, 0, 0}, qrow[4] = {0, 0, 0, 0};
+  // ... and so does its own label word: the word pass p reads at Lm[q] is the one this
+  // thread wrote in pass p-1 (one dependent L2 round trip fewer per pass)
+  uint32_t myw = 0;
   if (one && first < a.n) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if ((uint64_t)u < a.letters) qrow[u] = a.rows[(uint64_t)u * a.n + first];
   }
+  const bool own_label_enabled = a.own_label;
   while (p < a.max_passes) {
     const uint32_t pass = a.pass0 + p + 1;
     const uint32_t* Lm = sel ? a.lab1 : a.lab0;
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
       if (qi >= a.n) continue;
       const uint32_t q = (uint32_t)qi;
-      const uint32_t lw = Lm[q];
+      const uint32_t lw = (one && p > 0 && own_label_enabled) ? myw : Lm[q];
       const uint32_t leader = label_on_the_fly(lw, cprev);
       bool sp = false;
       bool eval = q != leader;
@@ -407,6 +412,7 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
         }
       }
       Lw[q] = leader | (sp ? kSplitBit : 0u);  // this pass's split rides with the label
+      if (one) myw = leader | (sp ? kSplitBit : 0u);
       any |= sp;
       elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
       if (sp && a.mark != nullptr)  // q's label changes: its predecessors re-evaluate
@@ -668,6 +674,11 @@ struct DegOut {
   }
 };
 
+bool own_label_on() {
+  const char* e = getenv("DFM_NAIVE_OWN_LABEL");
+  return e == nullptr || e[0] != '0';
+}
+
 // large alphabets only: the marks cost one store per predecessor of each split state
 // and two reads per state; the saving is up to 2k gathers per stable state per pass
 bool dirty_enabled(uint64_t n, uint64_t letters) {
@@ -844,7 +855,8 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       if (mark == nullptr && pass >= 64 && dirty_enabled(n, letters)) build_dirty();
       DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
       FusedArgs fa{rows, n,     letters, lab[0], lab[1], cells,    cells1,   chg,
-                   pass, chunk, sel,     pout,   pred_off, pred_src, mark,   dirty_from};
+                   pass, chunk, sel,     pout,   pred_off, pred_src, mark,   dirty_from,
+                   own_label_on()};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&fa};
       ProfScope prof(ctx, "elect", 0);
