@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DFM_ABI_VERSION 1
+#define DFM_ABI_VERSION 2  /* 2: dfm_stats.executed_passes, sharded driver, LTS ingestion */
 
 typedef enum {
   DFM_OK = 0,
@@ -325,6 +325,10 @@ int dfm_ctx_create_sharded_local(int device, int rank, int world, const char* gr
                                  dfm_ctx** out);
 int dfm_ctx_shard_info(const dfm_ctx* ctx, int* rank, int* world, const char** transport);
 void dfm_shard_bounds(uint64_t n_total, int world, int rank, uint64_t* lo, uint64_t* hi);
+/* Collective calls: an infrastructure fault on one rank (e.g. out of device memory)
+ * leaves the other ranks waiting in the next collective, as with NCCL itself — abort
+ * the job.  Algorithmic outcomes (timeout, an out-of-range target) are agreed on by
+ * all ranks and returned everywhere. */
 /* Host rows of the owned states (local->num_states = hi - lo, targets < n_total;
  * pageable or pinned).  block_out: the owned states' canonical labels (hi - lo
  * entries), or with gather_all the whole canonical partition (n_total entries) on

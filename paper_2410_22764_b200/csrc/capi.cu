@@ -469,7 +469,7 @@ using namespace dfm;
 
 extern "C" {
 
-const char* dfm_version(void) { return "libdfm 1 (B200 sm_100a)"; }
+const char* dfm_version(void) { return "libdfm 2 (B200 sm_100a)"; }
 
 int dfm_ctx_create(int device, dfm_ctx** out) {
   if (out == nullptr) return DFM_ERR_INVALID;
