@@ -234,6 +234,16 @@ void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, ui
 // exact packed keys (+1) from a key space of 2^key_bits: presence bitmap + rank
 void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key_bits,
                         void* label_out, uint64_t* groups_out);
+// the blocked signature builder over a shard's rows (sortpr_hash.cu): null when the
+// shard is too small or n_total exceeds the layout's range limit (~2e8 states)
+struct ShardLayout;
+ShardLayout* shard_layout_build(Ctx& ctx, const DevDfa& loc, uint64_t n_total);
+void shard_layout_free(ShardLayout* s);
+// keys (exact packed, or the shard kernels' hash chain + rows of `row` words) of the
+// m = loc.n owned states from the all-gathered ids at id_bits in {1, 4, 8, 16, 32}
+void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* full,
+                       const uint32_t* own, uint64_t m, int w, bool hashed, uint64_t seed,
+                       unsigned long long* keys, uint32_t* sig, uint32_t row);
 // contiguous shards of S = ceil(n/world) rounded up to a multiple of 32 states (a
 // rank's slice of a bit-packed id vector is whole words): rank r owns
 // [r*S, min(n, (r+1)*S))

@@ -47,6 +47,17 @@ unsigned sgrid(const Ctx& ctx, uint64_t items) {
 }
 int bitw(uint64_t x) { return x == 0 ? 0 : 64 - __builtin_clzll(x); }
 
+__device__ __forceinline__ uint64_t dmix64(uint64_t z) {  // = shard.cu mix64
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+bool shard_blocked_enabled() {
+  const char* e = getenv("DFM_SHARD_BLOCKED");
+  return e == nullptr || e[0] != '0';
+}
+
 __global__ void count_acc_kernel(const uint8_t* __restrict__ acc, uint64_t n,
                                  unsigned long long* out) {
   uint32_t c = 0;
@@ -133,6 +144,18 @@ __global__ void scatter_back_kernel(const uint32_t* __restrict__ order,
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     block[order[i]] = back[i];
+}
+
+// keys from the blocked builder -> the shard kernels' conventions (packed keys + 1,
+// hashed keys | 1: never 0, the empty-slot mark) and the grouping rank of each key
+__global__ void key_fix_dest_kernel(unsigned long long* __restrict__ keys, uint64_t n, bool packed,
+                                    uint32_t ranks, uint32_t* __restrict__ dest) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned long long key = keys[i];
+    keys[i] = packed ? key + 1ull : (key | 1ull);
+    dest[i] = (uint32_t)__umul64hi(dmix64(key ^ 0xD1B54A32D192ED03ull), ranks);
+  }
 }
 
 __global__ void iota_kernel(uint32_t* __restrict__ out, uint64_t n, uint64_t lo) {
@@ -249,6 +272,26 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
   }
   uint64_t B = split ? 2 : 1;
   uint64_t seed = kShardSeed0;
+  // blocked signature builder over the owned rows (targets = all n_total states): used
+  // only when EVERY rank could build it, so all ranks make keys the same way
+  struct LayHolder {
+    ShardLayout* p = nullptr;
+    ~LayHolder() { shard_layout_free(p); }
+  } lay;
+  if (shard_blocked_enabled()) {
+    ProfScope p(ctx, "layout", nl * k * 16ull);
+    lay.p = shard_layout_build(ctx, loc, n_total);
+  }
+  {
+    const uint64_t mine = lay.p != nullptr ? 1 : 0;
+    comm.all_gather_host(&mine, all.data(), 1, st);
+    bool every = true;
+    for (int r = 0; r < world; ++r) every = every && all[r] != 0;
+    if (!every) {
+      shard_layout_free(lay.p);
+      lay.p = nullptr;
+    }
+  }
   const int dbits = std::max(1, bitw((uint64_t)world - 1));
   auto* counts_dev = reinterpret_cast<unsigned long long*>(ctx.slot_t<uint64_t>("sd.counts", 64));
   std::vector<uint64_t> send_cnt(world), recv_cnt(world), so(world), sb(world), ro(world),
@@ -259,7 +302,7 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
     const int w = std::max(1, bitw(B - 1));
     const bool packed = (uint64_t)(k + 1) * w <= 63;
     // ids travel (and are gathered) at 1/2/4/8/16/32 bits: pass 1's vector is a bitmap
-    const uint32_t ib = B <= 2 ? 1 : B <= 4 ? 2 : B <= 16 ? 4 : B <= 256 ? 8 : B <= 65536 ? 16 : 32;
+    const uint32_t ib = B <= 2 ? 1 : B <= 16 ? 4 : B <= 256 ? 8 : B <= 65536 ? 16 : 32;
     const uint64_t slice = S * ib / 8;  // bytes per rank
     void* send_ids = ctx.slot("sd.ids_send", slice);
     void* full = ctx.slot("sd.ids_full", (uint64_t)world * slice);
@@ -283,8 +326,16 @@ AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const
     auto* keys = ctx.slot_t<unsigned long long>("sd.keys", std::max<uint64_t>(nl, 1));
     uint32_t* sig = words ? ctx.slot_t<uint32_t>("sd.sig", std::max<uint64_t>(nl * words, 1)) : nullptr;
     uint32_t* dest = ctx.slot_t<uint32_t>("sd.dest", std::max<uint64_t>(nl, 1));
-    shard_signature(ctx, loc.delta, nl, k, full, ib, lo, seed, (uint32_t)world,
-                    packed ? (uint32_t)w : 0u, keys, sig, dest);
+    if (lay.p != nullptr && (uint64_t)n_total * ib / 8 > (32ull << 20) && nl > 0) {
+      // the gathered vector is past the L2 plateau: shared-memory gathers per target range
+      shard_layout_keys(ctx, lay.p, (int)ib, static_cast<const uint32_t*>(full), block, nl, w,
+                        !packed, seed, keys, sig, k + 1);
+      key_fix_dest_kernel<<<sgrid(ctx, nl), 256, 0, st>>>(keys, nl, packed, (uint32_t)world, dest);
+      DFM_LAUNCH_CHECK();
+    } else {
+      shard_signature(ctx, loc.delta, nl, k, full, ib, lo, seed, (uint32_t)world,
+                      packed ? (uint32_t)w : 0u, keys, sig, dest);
+    }
     // ---- 3. route to the grouping ranks
     const unsigned long long* rkeys = keys;
     const uint32_t* rsig = sig;

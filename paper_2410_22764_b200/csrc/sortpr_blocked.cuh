@@ -39,6 +39,7 @@ struct Layout {
   // soon as its rows are in HBM (pipelined upload); one chunk = plain range-major
   uint32_t Wc = 0, nC = 0;
   uint64_t n = 0, T = 0;
+  uint64_t nt = 0;  // target states: == n on one GPU; the global count for a shard's rows
   uint32_t k = 0;
   uint16_t* tgt = nullptr;
   uint16_t* lsf = nullptr;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32
     const uint32_t j0 = g * c, j1 = min(L.R, j0 + c);
     // id slice of states [j0*kRs, min(n, j1*kRs)): words of the packed mirror
     const uint64_t st0 = (uint64_t)j0 * kRs;
-    const uint64_t st1 = min(L.n, (uint64_t)j1 * kRs);
+    const uint64_t st1 = min(L.nt, (uint64_t)j1 * kRs);
     const uint64_t w0 = st0 * kIdBits / 32, w1 = (st1 * kIdBits + 31) / 32;
     const uint32_t nwords = (uint32_t)(w1 - w0);
     const uint4* src4 = reinterpret_cast<const uint4*>(ids + w0);  // 16-byte aligned: kRs*bits/8

@@ -1205,12 +1205,13 @@ uint32_t layout_window(uint64_t n, uint32_t k) {
 }
 
 // layout buffers and geometry; chunks of wc windows (0: one chunk)
-void layout_init(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t wc) {
+void layout_init(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t wc, uint64_t nt = 0) {
   L.n = d.n;
+  L.nt = nt ? nt : d.n;
   L.k = d.k;
   L.T = L.n * L.k;
-  L.R = (uint32_t)ceil_div(L.n, kRs);
-  L.W = layout_window(L.n, L.k);
+  L.R = (uint32_t)ceil_div(L.nt, kRs);
+  L.W = layout_window(L.nt, L.k);
   L.E = L.W * L.k;
   L.nW = (uint32_t)ceil_div(L.n, L.W);
   L.Wc = wc == 0 ? L.nW : std::min(wc, L.nW);
@@ -1290,8 +1291,8 @@ uint32_t layout_chunk_windows() {  // DFM_LAYOUT_CHUNK_WINDOWS (tests): force ch
   return e ? (uint32_t)strtoul(e, nullptr, 10) : 0u;
 }
 
-void build_layout(Ctx& ctx, const DevDfa& d, Layout& L) {
-  layout_init(ctx, d, L, layout_chunk_windows());
+void build_layout(Ctx& ctx, const DevDfa& d, Layout& L, uint64_t nt = 0) {
+  layout_init(ctx, d, L, layout_chunk_windows(), nt);
   for (uint32_t ch = 0; ch < L.nC; ++ch) layout_chunk(ctx, d, L, ch);
 }
 
@@ -1437,6 +1438,29 @@ uint64_t sortpr_upload_chunk(uint64_t n, uint32_t k) {
   const uint32_t W = layout_window(n, k);
   const uint64_t wc = std::max<uint64_t>(1, ((64ull << 20) / (4ull * k)) / W);
   return wc * W;
+}
+
+// ---- the blocked builder over a shard's rows (csrc/shard_driver.cu): sources = the
+// owned states, targets = all n_total states, ids from the all-gathered vector; keys
+// and rows as the shard kernels make them (same packing, same hash chain)
+struct ShardLayout {
+  Layout L;
+};
+ShardLayout* shard_layout_build(Ctx& ctx, const DevDfa& loc, uint64_t n_total) {
+  const uint64_t T = (uint64_t)loc.n * loc.k;
+  if (!(loc.k > 0 && loc.k <= 1024 && T < (1ull << 32) && ceil_div(n_total, kRs) <= kMaxRanges &&
+        T >= kBlockedMinTransitions && !blocked_disabled()))
+    return nullptr;
+  auto* s = new ShardLayout;
+  build_layout(ctx, loc, s->L, n_total);
+  return s;
+}
+void shard_layout_free(ShardLayout* s) { delete s; }
+void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* full,
+                       const uint32_t* own, uint64_t m, int w, bool hashed, uint64_t seed,
+                       unsigned long long* keys, uint32_t* sig, uint32_t row) {
+  layout_keys(ctx, s->L, id_bits, full, nullptr, m, own, w, hashed, seed, keys, sig, row,
+              nullptr, nullptr, nullptr);
 }
 
 AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {

@@ -163,3 +163,71 @@ def test_out_of_range_target_rejected_on_every_rank(monkeypatch):
     for t in th:
         t.join(timeout=120)
     assert len(errs) == 2 and all("out of range" in e for e in errs)
+
+
+def _local_device_random(world, n, k, seed):
+    """random_dfa slices generated on the device per rank; returns the whole
+    canonical partition (gathered) and (nb, passes) of every rank."""
+    import torch
+    _group_id[0] += 1
+    group = f"d{_group_id[0]}"
+    res = [None] * world
+    err = []
+
+    def worker(r):
+        try:
+            import ctypes as C
+            se = ShardedEngine(0, r, world, "local", group)
+            lo, hi = se.bounds(n)
+            d = torch.empty((k, max(hi - lo, 1)), dtype=torch.int32, device="cuda")
+            a = torch.empty(max(hi - lo, 1), dtype=torch.uint8, device="cuda")
+            f = se.lib.dfm_random_dfa_slice_dev
+            f.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, C.c_uint64,
+                          C.c_uint64, C.c_void_p, C.c_void_p]
+            assert f(se.handle, n, k, seed, 0.5, lo, hi - lo, d.data_ptr(), a.data_ptr()) == 0
+            d, a = d[:, :hi - lo].contiguous(), a[:hi - lo]
+            out = torch.empty(max(hi - lo, 1), dtype=torch.int32, device="cuda")
+            nb, st = se.sort_pr_device(d, a, n, out)
+            torch.cuda.synchronize()
+            res[r] = (lo, out[:hi - lo].cpu().numpy().view(np.uint32), nb, st.iterations)
+            del d, a, out
+            se.close()
+        except Exception as e:  # pragma: no cover
+            err.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    assert not err, err
+    full = np.concatenate([x[1] for x in sorted(res, key=lambda x: x[0])])
+    return full, {(x[2], x[3]) for x in res}
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_blocked_shard_keys_match_single_engine(eng, monkeypatch, world):
+    """32-bit id passes through the blocked builder over each rank's rows (targets =
+    all states): same partition and pass count as the single-GPU engine."""
+    import torch
+    monkeypatch.setenv("DFM_SHARD_PROTOCOL", "1")
+    n, k = 12_000_000, 4
+    dd = eng.random_dfa_device(n, k, 41, 0.5)
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    nb, st = eng.run_device(dfm.Algo.sort, dd, block_out_ptr=out.data_ptr())
+    ref = out.cpu().numpy().view(np.uint32)
+    dd.free()
+    full, stats = _local_device_random(world, n, k, 41)
+    assert stats == {(nb, st.iterations)}
+    assert (full == ref).all()
+
+
+def test_blocked_shards_north_star_record(monkeypatch):
+    """random_dfa(1e8, 4, 1) over 2 local ranks through the blocked shard builder
+    against the reference's recorded result (tests/golden/config_vectors.json)."""
+    monkeypatch.setenv("DFM_SHARD_PROTOCOL", "1")
+    with open(os.path.join(os.path.dirname(__file__), "golden", "config_vectors.json")) as f:
+        rec = {v["name"]: v for v in json.load(f)["vectors"]}["ns_random_1e8_k4_s1"]["sort"]
+    full, stats = _local_device_random(2, 100_000_000, 4, 1)
+    assert stats == {(rec["num_blocks"], rec["iterations"])}
+    assert digest(full) == rec["sha256"]
