@@ -337,7 +337,8 @@ int dfm_sort_pr_sharded(dfm_ctx* ctx, uint64_t n_total, const dfm_dfa* local, in
                         uint32_t* block_out, uint32_t* num_blocks_out, int64_t timeout_ms,
                         dfm_stats* stats);
 /* Device-resident shard: delta_dev k rows of n_local u32, acc_dev n_local u8,
- * block_out_dev n_local u32 (canonical labels of the owned states). */
+ * block_out_dev n_local u32 (canonical labels of the owned states).  Targets are
+ * trusted (< n_total), like dfm_run_algorithm_dev; the host entry checks them. */
 int dfm_sort_pr_sharded_dev(dfm_ctx* ctx, uint64_t n_total, uint32_t n_local, uint32_t k,
                             const void* delta_dev, const void* acc_dev, void* block_out_dev,
                             uint32_t* num_blocks_out, int64_t timeout_ms, dfm_stats* stats);

@@ -253,7 +253,7 @@ inline uint64_t shard_size(uint64_t n, int world) {
 // `loc` = the owned rows (n = owned states, GLOBAL targets); canonical labels of the
 // owned states into canon_dev (device, loc.n entries)
 AlgoOut run_sort_pr_sharded(Ctx& ctx, uint64_t n_total, const DevDfa& loc, const Deadline& dl,
-                            uint32_t* canon_dev, bool force_protocol);
+                            uint32_t* canon_dev, bool force_protocol, bool validate = true);
 // device random_dfa
 void random_dfa_dev(Ctx& ctx, DevDfa& d, uint32_t n, uint32_t k, uint64_t seed, double p);
 

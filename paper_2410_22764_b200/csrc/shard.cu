@@ -115,19 +115,40 @@ __device__ __forceinline__ uint64_t cell_of(unsigned long long key, int level) {
   return (key >> (level == 0 ? 64 - kCellBits : 8)) & ((1ull << kCellBits) - 1);
 }
 
+// L2 policies as in the single-GPU engine's filter: keys stream with evict_first, the
+// 64 MB filter is kept with evict_last, the second bit is a fire-and-forget reduction
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long ld_key(const unsigned long long* a, uint64_t pol) {
+  unsigned long long v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 __global__ void __launch_bounds__(256) gfilt_set_kernel(const unsigned long long* __restrict__ keys,
                                                         uint64_t count, uint32_t* F, int level,
                                                         const uint32_t* __restrict__ slot_of) {
+  const uint64_t pf = pol_first(), pl = pol_last();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     if (level > 0 && slot_of[i] == kUniq) continue;
-    const uint64_t c = cell_of(keys[i], level);
+    const uint64_t c = cell_of(ld_key(keys + i, pf), level);
     const uint32_t bit = (uint32_t)(c & 15) * 2;
-    // test before set: heavily repeated keys (early passes) would serialise their
-    // atomics on a few cells; a cell already marked "seen twice" needs no update
-    if (((*reinterpret_cast<volatile uint32_t*>(&F[c >> 4]) >> bit) & 3u) == 3u) continue;
-    const uint32_t old = atomicOr(&F[c >> 4], 1u << bit);
-    if ((old >> bit) & 1u) atomicOr(&F[c >> 4], 2u << bit);
+    uint32_t* w = &F[c >> 4];
+    uint32_t old;
+    asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
+                 : "=r"(old) : "l"(w), "r"(1u << bit), "l"(pl) : "memory");
+    if (((old >> bit) & 3u) == 1u)
+      asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(w), "r"(2u << bit),
+                   "l"(pl) : "memory");
   }
 }
 
@@ -135,11 +156,12 @@ __global__ void __launch_bounds__(256) gfilt_mark_kernel(const unsigned long lon
                                                          uint64_t count, const uint32_t* __restrict__ F,
                                                          int level, uint32_t* __restrict__ slot_of,
                                                          unsigned long long* dups) {
+  const uint64_t pf = pol_first();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint32_t mine = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     if (level > 0 && slot_of[i] == kUniq) continue;
-    const uint64_t c = cell_of(keys[i], level);
+    const uint64_t c = cell_of(ld_key(keys + i, pf), level);
     const bool dup = (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
     slot_of[i] = dup ? 0u : kUniq;
     mine += dup ? 1u : 0u;
@@ -220,6 +242,21 @@ __global__ void __launch_bounds__(256) group_insert_kernel(const unsigned long l
       }
     }
     __syncthreads();
+  }
+}
+
+// filtered passes: only the filter's candidates (a few % of mostly-distinct keys)
+// reach the table, each straight to the global table (no per-tile shared-memory
+// aggregation: their keys rarely repeat inside a tile)
+__global__ void __launch_bounds__(256) group_insert_cand_kernel(
+    const unsigned long long* __restrict__ keys, uint64_t count, GSlot* slots, uint64_t cap,
+    uint32_t* __restrict__ slot_of) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (slot_of[i] == kUniq) continue;
+    const uint64_t g = global_insert(slots, cap, keys[i]);
+    atomicMax(&slots[g].rep, ~(uint32_t)i);
+    slot_of[i] = (uint32_t)g;
   }
 }
 
@@ -321,6 +358,24 @@ __global__ void __launch_bounds__(256) direct_set_kernel(const unsigned long lon
   }
 }
 
+// small key spaces (<= 2^16 keys: the early passes, a handful of keys over all
+// items): each CTA ORs its keys into a shared bitmap, then one global OR per word
+__global__ void __launch_bounds__(256) direct_set_small_kernel(
+    const unsigned long long* __restrict__ keys, uint64_t count, uint32_t* bits, uint32_t words) {
+  extern __shared__ uint32_t s_bits[];
+  for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) s_bits[w] = 0;
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t key = keys[i] - 1;
+    const uint32_t m = 1u << (key & 31);
+    if ((s_bits[key >> 5] & m) == 0) atomicOr(&s_bits[key >> 5], m);
+  }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < words; w += blockDim.x)
+    if (s_bits[w]) atomicOr(&bits[w], s_bits[w]);
+}
+
 struct DirPopIn {
   const uint32_t* bits;
   __device__ uint32_t operator()(uint64_t w) const { return __popc(bits[w]); }
@@ -400,7 +455,11 @@ void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key
   ProfScope p(ctx, "group", count * 16ull + words * 12);
   DFM_CUDA(cudaMemsetAsync(bits, 0, words * 4, ctx.stream));
   const auto* k = static_cast<const unsigned long long*>(keys);
-  if (count) {
+  if (count && words <= 2048) {
+    direct_set_small_kernel<<<grid_for(ctx, count), 256, words * 4, ctx.stream>>>(
+        k, count, bits, (uint32_t)words);
+    DFM_LAUNCH_CHECK();
+  } else if (count) {
     direct_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(k, count, bits);
     DFM_LAUNCH_CHECK();
   }
@@ -449,10 +508,14 @@ void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, ui
       const uint64_t cap = std::max<uint64_t>(1024, dups * 5 / 2);  // load <= 0.4
       auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
       DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
-      group_insert_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(count, kTileItems),
-                                                         ctx.num_sms * 8ull),
-                            256, 0, ctx.stream>>>(
-          static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
+      if (dups < count)  // filtered: candidates only
+        group_insert_cand_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+            static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
+      else
+        group_insert_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(count, kTileItems),
+                                                           ctx.num_sms * 8ull),
+                              256, 0, ctx.stream>>>(
+            static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
       DFM_LAUNCH_CHECK();
       group_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
           count, slots, slot_of, static_cast<const uint32_t*>(sig), words,
