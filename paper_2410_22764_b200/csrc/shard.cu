@@ -345,23 +345,24 @@ __global__ void random_slice_kernel(uint32_t* __restrict__ delta, uint8_t* __res
 // Direct grouping of exact packed keys from a small key space (2^bits keys): a
 // presence bitmap (L2-resident) and the key's rank among the present keys as its
 // dense group id — one atomic per warp-distinct key, no table, no probing.
+// bitmap words interleaved with their exclusive popcounts: word w of the bitmap at
+// [2w], its prefix at [2w+1] — a key's rank is one 8-byte read
 __global__ void __launch_bounds__(256) direct_set_kernel(const unsigned long long* __restrict__ keys,
-                                                         uint64_t count, uint32_t* bits) {
+                                                         uint64_t count, uint32_t* bp) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint64_t key = keys[i] - 1;  // packed keys are stored + 1
-    const uint32_t peers = __match_any_sync(__activemask(), key);
-    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
-      const uint32_t m = 1u << (key & 31);
-      if ((bits[key >> 5] & m) == 0) atomicOr(&bits[key >> 5], m);
-    }
+    const uint32_t m = 1u << (key & 31);
+    uint32_t* w = bp + 2 * (key >> 5);
+    // test before set: most keys of a dense pass repeat
+    if ((*reinterpret_cast<volatile uint32_t*>(w) & m) == 0) atomicOr(w, m);
   }
 }
 
 // small key spaces (<= 2^16 keys: the early passes, a handful of keys over all
 // items): each CTA ORs its keys into a shared bitmap, then one global OR per word
 __global__ void __launch_bounds__(256) direct_set_small_kernel(
-    const unsigned long long* __restrict__ keys, uint64_t count, uint32_t* bits, uint32_t words) {
+    const unsigned long long* __restrict__ keys, uint64_t count, uint32_t* bp, uint32_t words) {
   extern __shared__ uint32_t s_bits[];
   for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) s_bits[w] = 0;
   __syncthreads();
@@ -373,27 +374,27 @@ __global__ void __launch_bounds__(256) direct_set_small_kernel(
   }
   __syncthreads();
   for (uint32_t w = threadIdx.x; w < words; w += blockDim.x)
-    if (s_bits[w]) atomicOr(&bits[w], s_bits[w]);
+    if (s_bits[w]) atomicOr(&bp[2 * w], s_bits[w]);
 }
 
 struct DirPopIn {
-  const uint32_t* bits;
-  __device__ uint32_t operator()(uint64_t w) const { return __popc(bits[w]); }
+  const uint32_t* bp;
+  __device__ uint32_t operator()(uint64_t w) const { return __popc(bp[2 * w]); }
 };
 struct DirPopOut {
-  uint32_t* prefix;
-  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { prefix[w] = excl; }
+  uint32_t* bp;
+  __device__ void operator()(uint64_t w, uint32_t excl, uint32_t) const { bp[2 * w + 1] = excl; }
 };
 
 __global__ void __launch_bounds__(256) direct_label_kernel(const unsigned long long* __restrict__ keys,
                                                            uint64_t count,
-                                                           const uint32_t* __restrict__ bits,
-                                                           const uint32_t* __restrict__ prefix,
+                                                           const uint32_t* __restrict__ bp,
                                                            uint32_t* __restrict__ label) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint64_t key = keys[i] - 1;
-    label[i] = prefix[key >> 5] + __popc(bits[key >> 5] & ((1u << (key & 31)) - 1u));
+    const uint2 wp = *reinterpret_cast<const uint2*>(bp + 2 * (key >> 5));
+    label[i] = wp.y + __popc(wp.x & ((1u << (key & 31)) - 1u));
   }
 }
 
@@ -449,24 +450,23 @@ void shard_group_direct(Ctx& ctx, const void* keys, uint64_t count, uint32_t key
   if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "too many items for one rank");
   if (key_bits > 32) throw Error(DFM_ERR_INVALID, "direct grouping needs <= 32 key bits");
   const uint64_t words = ceil_div(1ull << key_bits, 32);
-  uint32_t* bits = ctx.slot_t<uint32_t>("shard.dbits", words);
-  uint32_t* prefix = ctx.slot_t<uint32_t>("shard.dpref", words);
+  uint32_t* bp = ctx.slot_t<uint32_t>("shard.dbits", 2 * words);  // {bitmap, prefix} pairs
   uint64_t* total = ctx.d_scalars + 48;
   ProfScope p(ctx, "group", count * 16ull + words * 12);
-  DFM_CUDA(cudaMemsetAsync(bits, 0, words * 4, ctx.stream));
+  DFM_CUDA(cudaMemsetAsync(bp, 0, 2 * words * 4, ctx.stream));
   const auto* k = static_cast<const unsigned long long*>(keys);
   if (count && words <= 2048) {
     direct_set_small_kernel<<<grid_for(ctx, count), 256, words * 4, ctx.stream>>>(
-        k, count, bits, (uint32_t)words);
+        k, count, bp, (uint32_t)words);
     DFM_LAUNCH_CHECK();
   } else if (count) {
-    direct_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(k, count, bits);
+    direct_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(k, count, bp);
     DFM_LAUNCH_CHECK();
   }
-  prims::lookback_scan(ctx, "shard.dscan", words, DirPopIn{bits}, DirPopOut{prefix}, total);
+  prims::lookback_scan(ctx, "shard.dscan", words, DirPopIn{bp}, DirPopOut{bp}, total);
   if (count) {
     direct_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-        k, count, bits, prefix, static_cast<uint32_t*>(label_out));
+        k, count, bp, static_cast<uint32_t*>(label_out));
     DFM_LAUNCH_CHECK();
   }
   DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 48, total, 8, cudaMemcpyDeviceToHost, ctx.stream));
