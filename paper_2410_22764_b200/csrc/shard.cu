@@ -11,6 +11,7 @@
 //   sort_pairs      : the onesweep radix sort (routing by destination rank)
 //   random slice    : bit-exact random_dfa rows for an owned state range
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "prims.cuh"
@@ -19,6 +20,13 @@ namespace dfm {
 namespace {
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+// DFM_SHARD_WEAK_HASH=<bits> (tests): hashed keys of passes under the first seed are
+// truncated so that distinct signatures collide and the void-and-retry path runs
+constexpr uint64_t kShardSeed0 = 0x5EED0001ull;
+__device__ unsigned long long g_shard_weak_mask = ~0ull;
+__device__ __forceinline__ unsigned long long shard_weak(unsigned long long h, uint64_t seed) {
+  return seed == kShardSeed0 ? (h & g_shard_weak_mask) : h;
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -70,6 +78,7 @@ __global__ void __launch_bounds__(256) shard_sig_kernel_w(
       row[a + 1] = s;
       h = mix64(h + kGolden + s);
     }
+    h = shard_weak(h, seed);
     keys[i] = h | 1ull;
     dest[i] = (uint32_t)__umul64hi(mix64(h ^ 0xD1B54A32D192ED03ull), ranks);
   }
@@ -408,10 +417,22 @@ unsigned grid_for(const Ctx& ctx, uint64_t items) {
 
 
 namespace dfm {
+void shard_weak_hash_setup() {
+  static unsigned long long set = ~0ull;
+  const char* e = getenv("DFM_SHARD_WEAK_HASH");
+  const unsigned long long mask =
+      e ? ((1ull << std::min(63ul, strtoul(e, nullptr, 10))) - 1) : ~0ull;
+  if (mask != set) {
+    DFM_CUDA(cudaMemcpyToSymbol(g_shard_weak_mask, &mask, sizeof(mask)));
+    set = mask;
+  }
+}
+
 void shard_signature(Ctx& ctx, const void* delta_local, uint64_t n_local, uint32_t k,
                      const void* block_full, uint32_t id_bits, uint64_t lo, uint64_t seed,
                      uint32_t ranks, uint32_t pack_bits, void* keys_out, void* sig_out,
                      void* dest_out) {
+  shard_weak_hash_setup();
   if (ranks == 0) throw Error(DFM_ERR_INVALID, "ranks must be >= 1");
   if (id_bits != 1 && id_bits != 2 && id_bits != 4 && id_bits != 8 && id_bits != 16 && id_bits != 32)
     throw Error(DFM_ERR_INVALID, "id_bits must be 1, 2, 4, 8, 16 or 32");

@@ -231,3 +231,15 @@ def test_blocked_shards_north_star_record(monkeypatch):
     full, stats = _local_device_random(2, 100_000_000, 4, 1)
     assert stats == {(rec["num_blocks"], rec["iterations"])}
     assert digest(full) == rec["sha256"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_forced_hash_collisions_retry_exactly(world, monkeypatch):
+    """DFM_SHARD_WEAK_HASH truncates the first seed's hashed keys: distinct signatures
+    collide, the rows disagree on some rank, every rank voids the pass and redoes it
+    under a new seed — the result is still the oracle's."""
+    monkeypatch.setenv("DFM_SHARD_PROTOCOL", "1")
+    monkeypatch.setenv("DFM_SHARD_WEAK_HASH", "6")
+    for delta, acc in (O.vlts_dfa(200, 20_000, 10), O.random_dfa(30_000, 6, 13, 0.5)):
+        ref = O.sort_pr(delta, acc)
+        _check(_local(world, delta, acc, gather_all=True), ref)
