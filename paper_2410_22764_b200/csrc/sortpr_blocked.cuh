@@ -39,8 +39,10 @@ struct Layout {
   // soon as its rows are in HBM (pipelined upload); one chunk = plain range-major
   uint32_t Wc = 0, nC = 0;
   uint64_t n = 0, T = 0;
-  uint64_t nt = 0;  // target states: == n on one GPU; the global count for a shard's rows
   uint32_t k = 0;
+  // target states: == n on one GPU; the global count for a shard's rows (u32: fills
+  // the padding after k, so the struct — a kernel parameter — keeps its size)
+  uint32_t nt = 0;
   uint16_t* tgt = nullptr;
   uint16_t* lsf = nullptr;
   uint32_t* eidx = nullptr;    // [T] bucket position of each window-flattened transition
@@ -120,13 +122,21 @@ __global__ void __launch_bounds__(512) lay_count_kernel(const uint32_t* __restri
     }
     uint32_t tot;
     uint32_t run = prims::block_exclusive_sum<512>(sum, s_warp, &tot);
+    // stage the in-window prefixes in shared memory (after the counts in s_h) so that
+    // both rows leave with coalesced stores (a thread's 8 consecutive entries would
+    // touch 8 sectors per warp instruction)
+    uint16_t* s_pre_w = reinterpret_cast<uint16_t*>(s_h + L.R);
 #pragma unroll
     for (uint32_t u = 0; u < kPer; ++u)
       if (j0 + u < L.R) {
-        cnt_w[(uint64_t)w * L.R + j0 + u] = c[u];
-        L.pre[(uint64_t)w * L.R + j0 + u] = (uint16_t)run;
+        s_pre_w[j0 + u] = (uint16_t)run;
         run += c[u];
       }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < L.R; j += blockDim.x) {
+      cnt_w[(uint64_t)w * L.R + j] = s_h[j];
+      L.pre[(uint64_t)w * L.R + j] = s_pre_w[j];
+    }
     __syncthreads();
   }
 }
@@ -175,25 +185,24 @@ struct LayOffOut {
 // every tgt goes to its bucket position off(w, j) + rank.
 __device__ __forceinline__ void lay_stage(uint32_t t, uint32_t a, uint32_t x, uint32_t W,
                                           uint32_t* s_cur, const uint32_t* s_pre,
-                                          uint16_t* s_tgt, uint16_t* s_lsf, uint16_t* s_j) {
+                                          uint32_t* s_tj, uint16_t* s_lsf) {
   const uint32_t j = t / kRs;
   const uint32_t f = s_pre[j] + atomicAdd(&s_cur[j], 1u);
-  s_tgt[f] = (uint16_t)(t - j * kRs);
+  s_tj[f] = (t - j * kRs) | (j << 16);  // target offset (16 bits) and range (< 4096)
   s_lsf[f] = (uint16_t)(a * W + x);
-  s_j[f] = (uint16_t)j;
 }
 
 __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __restrict__ delta,
                                                            Layout L, uint32_t w_begin,
                                                            uint32_t w_end) {
-  // s_cur[R], s_off[R], s_pre[R+1], then u16 s_lsf[E], s_tgt[E], s_j[E]
+  // s_cur[R], s_off[R], s_pre[R+1], then u32 s_tj[E] (target offset | range << 16),
+  // u16 s_lsf[E]: two shared stores per staged transition
   extern __shared__ uint32_t s_lay[];
   uint32_t* s_cur = s_lay;
   uint32_t* s_off = s_lay + L.R;
   uint32_t* s_pre = s_lay + 2 * L.R;
-  uint16_t* s_lsf = reinterpret_cast<uint16_t*>(s_lay + 3 * L.R + 1);
-  uint16_t* s_tgt = s_lsf + L.E;
-  uint16_t* s_j = s_tgt + L.E;
+  uint32_t* s_tj = s_lay + 3 * L.R + 1;
+  uint16_t* s_lsf = reinterpret_cast<uint16_t*>(s_tj + L.E);
   const uint64_t pol = policy_evict_first();
   // the next window's sub-run starts are loaded while the current one is written out
   constexpr uint32_t kPf = kMaxRanges / 1024;
@@ -242,10 +251,10 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
           const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
           if (e < ew4) {
             const uint32_t a = e / w4, x = 4 * (e - a * w4);
-            lay_stage(t[u].x, a, x, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
-            lay_stage(t[u].y, a, x + 1, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
-            lay_stage(t[u].z, a, x + 2, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
-            lay_stage(t[u].w, a, x + 3, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+            lay_stage(t[u].x, a, x, L.W, s_cur, s_pre, s_tj, s_lsf);
+            lay_stage(t[u].y, a, x + 1, L.W, s_cur, s_pre, s_tj, s_lsf);
+            lay_stage(t[u].z, a, x + 2, L.W, s_cur, s_pre, s_tj, s_lsf);
+            lay_stage(t[u].w, a, x + 3, L.W, s_cur, s_pre, s_tj, s_lsf);
           }
         }
       }
@@ -263,7 +272,7 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
           const uint32_t e = e0 + u * blockDim.x + threadIdx.x;
           if (e < ew) {
             const uint32_t a = e / wn;
-            lay_stage(t[u], a, e - a * wn, L.W, s_cur, s_pre, s_tgt, s_lsf, s_j);
+            lay_stage(t[u], a, e - a * wn, L.W, s_cur, s_pre, s_tj, s_lsf);
           }
         }
       }
@@ -275,10 +284,11 @@ __global__ void __launch_bounds__(1024) lay_scatter_kernel(const uint32_t* __res
     __syncthreads();
     const uint64_t fb = (uint64_t)w * L.E;
     for (uint32_t f = threadIdx.x; f < ew; f += blockDim.x) {
-      const uint32_t e = s_off[s_j[f]] + f;
+      const uint32_t tj = s_tj[f];
+      const uint32_t e = s_off[tj >> 16] + f;
       L.lsf[fb + f] = s_lsf[f];
       L.eidx[fb + f] = e;
-      L.tgt[e] = s_tgt[f];
+      L.tgt[e] = (uint16_t)(tj & 0xFFFFu);
     }
     __syncthreads();
   }
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32
     const uint32_t j0 = g * c, j1 = min(L.R, j0 + c);
     // id slice of states [j0*kRs, min(n, j1*kRs)): words of the packed mirror
     const uint64_t st0 = (uint64_t)j0 * kRs;
-    const uint64_t st1 = min(L.nt, (uint64_t)j1 * kRs);
+    const uint64_t st1 = min((uint64_t)L.nt, (uint64_t)j1 * kRs);
     const uint64_t w0 = st0 * kIdBits / 32, w1 = (st1 * kIdBits + 31) / 32;
     const uint32_t nwords = (uint32_t)(w1 - w0);
     const uint4* src4 = reinterpret_cast<const uint4*>(ids + w0);  // 16-byte aligned: kRs*bits/8
@@ -350,26 +360,54 @@ __global__ void __launch_bounds__(1024) lay_gather_kernel(Layout L, const uint32
                     : (ch + 1 < L.nC ? (ch + 1) * L.Wc * L.E : (uint32_t)L.T);
       }
       __syncthreads();
-      // range by range (no per-element range search); 8 targets per thread-step
+      // range by range (no per-element range search).  The aligned body moves 8
+      // targets per 16-byte load and 8 ids per vector store (two groups in flight
+      // per thread); the unaligned head and tail go element by element
       for (uint32_t r = 0; r < j1 - j0; ++r) {
         const uint32_t start = s_bound[r], end = s_bound[r + 1];
         const uint32_t* sl = s_slice;
         const uint32_t sb = r * kRs;
-        for (uint32_t e0 = start + threadIdx.x; e0 < end; e0 += 8 * blockDim.x) {
-          uint32_t t[8];
+        const uint32_t g0 = (start + 7) / 8, g1 = end / 8;  // whole 8-element groups
+        const uint32_t head_end = g0 < g1 ? g0 * 8 : end;
+        for (uint32_t e = start + threadIdx.x; e < head_end; e += blockDim.x)
+          vout[e] = (V)slice_id<kIdBits>(sl, sb + L.tgt[e]);
+        if (g0 < g1) {
+          for (uint32_t e = g1 * 8 + threadIdx.x; e < end; e += blockDim.x)
+            vout[e] = (V)slice_id<kIdBits>(sl, sb + L.tgt[e]);
+          const uint4* t4 = reinterpret_cast<const uint4*>(L.tgt);
+          for (uint32_t g = g0 + threadIdx.x; g < g1; g += 2 * blockDim.x) {
+            uint4 tv[2];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t e = e0 + u * blockDim.x;
-            uint32_t x = 0;
-            if (e < end)
-              asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
-                  : "=r"(x) : "l"(L.tgt + e), "l"(pol));
-            t[u] = x;
-          }
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t gg = g + u * blockDim.x;
+              if (gg < g1)
+                asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                    : "=r"(tv[u].x), "=r"(tv[u].y), "=r"(tv[u].z), "=r"(tv[u].w)
+                    : "l"(t4 + gg), "l"(pol));
+            }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint32_t e = e0 + u * blockDim.x;
-            if (e < end) vout[e] = (V)slice_id<kIdBits>(sl, sb + t[u]);
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t gg = g + u * blockDim.x;
+              if (gg >= g1) continue;
+              const uint32_t w4[4] = {tv[u].x, tv[u].y, tv[u].z, tv[u].w};
+              uint32_t id[8];
+#pragma unroll
+              for (int b = 0; b < 8; ++b)
+                id[b] = slice_id<kIdBits>(sl, sb + ((w4[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu));
+              if (sizeof(V) == 4) {
+                uint4* o = reinterpret_cast<uint4*>(vout) + 2 * (uint64_t)gg;
+                o[0] = make_uint4(id[0], id[1], id[2], id[3]);
+                o[1] = make_uint4(id[4], id[5], id[6], id[7]);
+              } else if (sizeof(V) == 2) {
+                reinterpret_cast<uint4*>(vout)[gg] =
+                    make_uint4(id[0] | id[1] << 16, id[2] | id[3] << 16, id[4] | id[5] << 16,
+                               id[6] | id[7] << 16);
+              } else {
+                reinterpret_cast<uint2*>(vout)[gg] =
+                    make_uint2(id[0] | id[1] << 8 | id[2] << 16 | id[3] << 24,
+                               id[4] | id[5] << 8 | id[6] << 16 | id[7] << 24);
+              }
+            }
           }
         }
       }
@@ -395,10 +433,6 @@ struct SigParams {
   uint32_t* present;  // direct keys: bitmap of the keys present, words interleaved with
                       // their exclusive popcounts (rank-compacted table)
   uint32_t tile_bytes;  // shared tile size (16-byte multiple)
-  // uniqueness filter of a filtered pass (null: none): the level-0 set is done here,
-  // on the key still in registers, instead of a separate sweep over the keys
-  uint32_t* filt = nullptr;
-  bool filt_hashed = false;
 };
 
 // ---- per pass P: one CTA per window, streamed ids -> smem tile -> keys
@@ -467,15 +501,13 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
     for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
       const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
       const uint32_t x = (uint32_t)(q - q0);
-      unsigned long long stored;
       const uint32_t b = p.block[q];
       if (!kHashed) {
         unsigned long long key = b;
 #pragma unroll
         for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
           key = (key << p.w) | tget(a * L.W + x);
-        stored = p.vals ? mix64(key ^ p.seed) : key;
-        p.keys[i] = stored;
+        p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
         if (p.present) {  // test before set: most keys of a dense pass are repeats
           const uint32_t bit = 1u << (key & 31);
           uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
@@ -491,19 +523,9 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
           row[a + 1] = s;
           h = mix64(h + kGolden + s);
         }
-        stored = weak(h, p.seed);
-        p.keys[i] = stored;
+        p.keys[i] = weak(h, p.seed);
       }
       if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
-      if (p.filt) {  // = filt_set_kernel level 0 on keys[i]
-        const uint64_t c =
-            (table_hash(stored, p.filt_hashed, p.seed) >> (64 - kFilterCellBits)) &
-            ((1ull << kFilterCellBits) - 1);
-        const uint32_t bb = (uint32_t)(c & 15) * 2;
-        const uint64_t pol_keep = policy_evict_last();
-        const uint32_t old = atom_or_keep(&p.filt[c >> 4], 1u << bb, pol_keep);
-        if (((old >> bb) & 3u) == 1u) red_or_keep(&p.filt[c >> 4], 2u << bb, pol_keep);
-      }
     }
     __syncthreads();
   }

@@ -939,22 +939,14 @@ __global__ void __launch_bounds__(256) direct_keys_kernel(
   }
 }
 
-// opt-in (DFM_SORTPR_DIRECT=1): measured slower on random_dfa(1e8, 4) — 2.0 ms for the
-// 4e8 gathers from the 66.7 MB 5-bit mirror while the layout streams beside it, vs
-// 1.7 ms for the blocked pass (profiles/r02c)
-// opt-in (DFM_SORTPR_FILT_FUSED=1): the level-0 filter set inside lay_sig is exact but
-// measured slower — lay_sig 6.7 -> 8.1 ms of the step with the L2 atomics in it,
-// against the 0.95 ms filt_set sweep it replaces (random_dfa(1e8, 4); profiles/r02f)
 bool pass_timing() {
   const char* e = getenv("DFM_SORTPR_PASS_TIMING");
   return e != nullptr && e[0] == '1';
 }
 
-bool filt_fused_enabled() {
-  const char* e = getenv("DFM_SORTPR_FILT_FUSED");
-  return e != nullptr && e[0] == '1';
-}
-
+// opt-in (DFM_SORTPR_DIRECT=1): measured slower on random_dfa(1e8, 4) — 2.0 ms for the
+// 4e8 gathers from the 66.7 MB 5-bit mirror while the layout streams beside it, vs
+// 1.7 ms for the blocked pass (profiles/r02c)
 bool pass_direct_enabled() {
   const char* e = getenv("DFM_SORTPR_DIRECT");
   return e != nullptr && e[0] == '1';
@@ -1207,7 +1199,7 @@ uint32_t layout_window(uint64_t n, uint32_t k) {
 // layout buffers and geometry; chunks of wc windows (0: one chunk)
 void layout_init(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t wc, uint64_t nt = 0) {
   L.n = d.n;
-  L.nt = nt ? nt : d.n;
+  L.nt = (uint32_t)(nt ? nt : d.n);
   L.k = d.k;
   L.T = L.n * L.k;
   L.R = (uint32_t)ceil_div(L.nt, kRs);
@@ -1239,7 +1231,7 @@ void layout_chunk(Ctx& ctx, const DevDfa& d, Layout& L, uint32_t ch) {
   // delta read twice + tgt/lsf/eidx writes + the count/offset matrices
   ProfScope ps(ctx, "layout", ct * (4ull + 4 + 2 + 2 + 4) + cells * (4ull * 4 + 2 * 2));
   const unsigned grid = (unsigned)std::min<uint64_t>(wc, (uint64_t)ctx.num_sms * 4);
-  lay_count_kernel<<<grid, 512, L.R * 4, ctx.stream>>>(d.delta, L, cnt_w, w0, w1);
+  lay_count_kernel<<<grid, 512, L.R * 6 + 16, ctx.stream>>>(d.delta, L, cnt_w, w0, w1);
   DFM_LAUNCH_CHECK();
   lay_transpose_kernel<<<dim3((unsigned)ceil_div(L.R, 32), (unsigned)ceil_div(wc, 32)),
                          dim3(32, 8), 0, ctx.stream>>>(cnt_w + (uint64_t)w0 * L.R,
@@ -1343,7 +1335,7 @@ void layout_keys_bits(Ctx& ctx, const Layout& L, const uint32_t* ids, const SigP
 void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const uint32_t* act,
                  uint64_t m, const uint32_t* block, int w, bool hashed, uint64_t seed,
                  unsigned long long* keys, uint32_t* sig, uint32_t row, uint32_t* vals,
-                 const uint8_t* lead, uint32_t* present, uint32_t* filt = nullptr) {
+                 const uint8_t* lead, uint32_t* present) {
   if (act) {
     ProfScope ps(ctx, "scan", m * 4 + L.nW * 4ull);
     lay_wstart_kernel<<<grid_for(ctx, m + 1), 256, 0, ctx.stream>>>(act, m, L.W, L.nW, L.wstart);
@@ -1352,8 +1344,6 @@ void layout_keys(Ctx& ctx, Layout& L, int mirror_bits, const void* ids, const ui
   const uint64_t idb = (uint64_t)std::max(8, mirror_bits) / 8;
   SigParams sp{L,   act ? L.wstart : nullptr, act, block, w, seed, keys, hashed ? sig : nullptr,
                row, vals, lead, present};
-  sp.filt = filt;
-  sp.filt_hashed = hashed;
   // per transition: tgt 2 + id write + lsf 2 + eidx 4 + id read; id slices once; per active
   // state: act 4 + own id 4 + key 8 (+ signature row)
   ProfScope ps(ctx, "sig", L.T * (8 + 2 * idb) + L.n * (uint64_t)mirror_bits / 8 +
@@ -1638,7 +1628,6 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       const bool part = blocked && part_on && !force_global && !(direct && table <= kSmallTable) &&
                         m >= kPartMinStates && m < (1ull << 31);
       force_global = false;
-      bool filt_preset = false;  // the level-0 filter was set by the key kernel
       // narrow exact passes (ids <= 8 bits): keys by direct gathers from an L2-resident
       // packed mirror; the blocked layout keeps building on the side stream for the
       // 32-bit passes
@@ -1707,15 +1696,8 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           present = ctx.slot_t<uint32_t>("sh.present", 2 * words);
           DFM_CUDA(cudaMemsetAsync(present, 0, 2 * words * 4, ctx.stream));
         }
-        // a filtered pass's level-0 filter is set inside the key kernel
-        uint32_t* F0 = nullptr;
-        if (!part && !direct && m >= kFilterMinStates && filt_fused_enabled()) {
-          F0 = ctx.slot_t<uint32_t>("sh.filter", 1ull << (kFilterCellBits - 4));
-          DFM_CUDA(cudaMemsetAsync(F0, 0, 1ull << (kFilterCellBits - 2), ctx.stream));
-        }
         layout_keys(ctx, lay, mirror_bits, ids, act, m, block, w, !packed, seed, keys, sig, row,
-                    vals, lead, present, F0);
-        filt_preset = F0 != nullptr;
+                    vals, lead, present);
         if (part) {
           group_partitioned(ctx, m, act, keys, vals, packed ? nullptr : sig, k + 1, row, B, block,
                             flag, lead, sc);
@@ -1750,12 +1732,10 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           ProfScope p(ctx, "insert", (1ull << (kFilterCellBits - 2)) + dups * (8ull + 8 + 4));
           DFM_CUDA(cudaMemsetAsync(sc + 6, 0, 8, ctx.stream));
           const uint32_t* cin = level == 0 ? nullptr : cand;
-          if (!(level == 0 && filt_preset)) {  // (level 0 set by the key kernel)
-            DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kFilterCellBits - 2), ctx.stream));
-            filt_set_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(keys, dups, !packed,
-                                                                         seed, F, level, cin);
-            DFM_LAUNCH_CHECK();
-          }
+          DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kFilterCellBits - 2), ctx.stream));
+          filt_set_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(keys, dups, !packed, seed,
+                                                                       F, level, cin);
+          DFM_LAUNCH_CHECK();
           filt_mark_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(
               keys, dups, !packed, seed, F, slot_of, level, cin);
           DFM_LAUNCH_CHECK();
