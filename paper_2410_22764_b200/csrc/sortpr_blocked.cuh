@@ -498,34 +498,50 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
     __syncthreads();
     const uint64_t i0 = p.wstart ? p.wstart[w] : q0;
     const uint64_t i1 = p.wstart ? p.wstart[w + 1] : q0 + wn;
-    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-      const uint32_t q = p.act ? p.act[i] : (uint32_t)i;
-      const uint32_t x = (uint32_t)(q - q0);
-      const uint32_t b = p.block[q];
-      if (!kHashed) {
-        unsigned long long key = b;
+    // KU states per thread: their own-block loads are in flight together (one state
+    // at a time left every warp waiting a full memory latency per state)
+    constexpr int KU = kHashed ? 1 : 4;
+    for (uint64_t ib = i0 + threadIdx.x; ib < i1; ib += KU * blockDim.x) {
+      uint32_t qq[KU], bb[KU];
 #pragma unroll
-        for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
-          key = (key << p.w) | tget(a * L.W + x);
-        p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
-        if (p.present) {  // test before set: most keys of a dense pass are repeats
-          const uint32_t bit = 1u << (key & 31);
-          uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
-          if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
-        }
-      } else {
-        uint32_t* row = p.sig + i * (uint64_t)p.row;
-        row[0] = b;
-        unsigned long long h = mix64(p.seed * kGolden + b);
-#pragma unroll
-        for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a) {
-          const uint32_t s = tget(a * L.W + x);
-          row[a + 1] = s;
-          h = mix64(h + kGolden + s);
-        }
-        p.keys[i] = weak(h, p.seed);
+      for (int u = 0; u < KU; ++u) {
+        const uint64_t i = ib + (uint64_t)u * blockDim.x;
+        qq[u] = i < i1 ? (p.act ? p.act[i] : (uint32_t)i) : 0u;
       }
-      if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
+#pragma unroll
+      for (int u = 0; u < KU; ++u) bb[u] = ib + (uint64_t)u * blockDim.x < i1 ? p.block[qq[u]] : 0u;
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const uint64_t i = ib + (uint64_t)u * blockDim.x;
+        if (i >= i1) break;
+        const uint32_t q = qq[u];
+        const uint32_t x = (uint32_t)(q - q0);
+        const uint32_t b = bb[u];
+        if (!kHashed) {
+          unsigned long long key = b;
+#pragma unroll
+          for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a)
+            key = (key << p.w) | tget(a * L.W + x);
+          p.keys[i] = p.vals ? mix64(key ^ p.seed) : key;
+          if (p.present) {  // test before set: most keys of a dense pass are repeats
+            const uint32_t bit = 1u << (key & 31);
+            uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
+            if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
+          }
+        } else {
+          uint32_t* row = p.sig + i * (uint64_t)p.row;
+          row[0] = b;
+          unsigned long long h = mix64(p.seed * kGolden + b);
+#pragma unroll
+          for (uint32_t a = 0; a < (kK > 0 ? (uint32_t)kK : k); ++a) {
+            const uint32_t s = tget(a * L.W + x);
+            row[a + 1] = s;
+            h = mix64(h + kGolden + s);
+          }
+          p.keys[i] = weak(h, p.seed);
+        }
+        if (p.vals) p.vals[i] = (uint32_t)i | ((uint32_t)p.lead[q] << 31);
+      }
     }
     __syncthreads();
   }

@@ -270,7 +270,6 @@ __global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
     unsigned long long key[2] = {0, 0};
     bool valid[2];
     bool merge[2] = {!kHashed, !kHashed};  // slot needs the aggregated rep/info update
-#pragma unroll
     uint64_t idx[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {

@@ -1,5 +1,5 @@
 set -u
-OUT=gpurun_out/r02o; mkdir -p $OUT
+OUT=gpurun_out/${1:-r02q}; mkdir -p $OUT
 timeout 1500 python -m pytest tests/test_gpu_configs.py tests/test_gpu_parity.py tests/test_gpu_pipeline.py tests/test_gpu_sharded_driver.py -q -p no:cacheprovider -x > $OUT/tests.txt 2>&1; echo "rc=$?" >> $OUT/tests.txt; tail -3 $OUT/tests.txt
 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench.json 2>&1
 python - $OUT/bench.json <<'PY'
