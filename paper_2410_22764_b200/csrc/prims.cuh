@@ -165,6 +165,113 @@ void lookback_scan(Ctx& ctx, const char* slot, uint64_t count, In in, Out out,
   DFM_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------------ flag compaction
+// Ordered compaction of 0/1 flags with decoupled look-back: pred(i) -> bool is
+// evaluated STRIPED (item u of thread t is tile_base + u*256 + t: every load is
+// warp-coalesced) and ranked with ballots; out(i, rank, flag) gets the number of set
+// flags before i, so the flagged i leave in ascending order.
+template <class Pred, class Out>
+__global__ void __launch_bounds__(kScanThreads) lookback_flags_kernel(Pred pred, Out out,
+                                                                      uint64_t count,
+                                                                      uint64_t* status,
+                                                                      uint32_t* ticket,
+                                                                      uint64_t* total_out) {
+  constexpr int kWarps = kScanThreads / 32;
+  static_assert(kScanItems * kWarps == 64, "two (item, warp) counts per lane");
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_cnt[kScanItems * kWarps];
+  __shared__ uint32_t s_agg;
+  __shared__ uint64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t tb = tile * kScanTile;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  uint32_t bal[kScanItems];
+#pragma unroll
+  for (int u = 0; u < kScanItems; ++u) {
+    const uint64_t idx = tb + (uint64_t)u * kScanThreads + threadIdx.x;
+    bal[u] = __ballot_sync(0xffffffffu, idx < count && pred(idx));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < kScanItems; ++u) s_cnt[u * kWarps + warp] = __popc(bal[u]);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 64 (item, warp) counts, slot-major
+    const uint32_t a = s_cnt[2 * lane], b = s_cnt[2 * lane + 1];
+    uint32_t incl = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t ex = incl - a - b;
+    s_cnt[2 * lane] = ex;
+    s_cnt[2 * lane + 1] = ex + a;
+    if (lane == 31) s_agg = incl;
+  }
+  __syncthreads();
+  const uint32_t agg = s_agg;
+  if (warp == 0) {
+    uint64_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile(status, kFlagInc | agg);
+    } else {
+      if (lane == 0) st_volatile(status + tile, kFlagAgg | agg);
+      int64_t pos = (int64_t)tile - 1 - lane;
+      while (true) {
+        uint64_t s = 0;
+        if (pos >= 0) {
+          do {
+            s = ld_volatile(status + pos);
+          } while ((s & ~kValMask) == 0);
+        } else {
+          s = kFlagInc;
+        }
+        const uint32_t inc_mask = __ballot_sync(0xffffffffu, (s & kFlagInc) != 0);
+        const int stop = inc_mask ? __ffs(inc_mask) - 1 : 31;
+        uint64_t val = ((int)lane <= stop) ? (s & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc_mask) break;
+        pos -= 32;
+      }
+      if (lane == 0) st_volatile(status + tile, kFlagInc | (prefix + agg));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int u = 0; u < kScanItems; ++u) {
+    const uint64_t idx = tb + (uint64_t)u * kScanThreads + threadIdx.x;
+    if (idx < count)
+      out(idx, (uint32_t)s_prefix + s_cnt[u * kWarps + warp] + __popc(bal[u] & lt),
+          (bal[u] >> lane) & 1u);
+  }
+  if (total_out != nullptr && threadIdx.x == 0 && (tile + 1) * kScanTile >= count)
+    *total_out = s_prefix + agg;
+}
+
+template <class Pred, class Out>
+void lookback_flags(Ctx& ctx, const char* slot, uint64_t count, Pred pred, Out out,
+                    uint64_t* total_dev) {
+  if (count == 0) {
+    if (total_dev) DFM_CUDA(cudaMemsetAsync(total_dev, 0, 8, ctx.stream));
+    return;
+  }
+  const uint64_t tiles = ceil_div(count, kScanTile);
+  uint8_t* scratch = ctx.slot_t<uint8_t>(slot, 16 + tiles * 8);
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(scratch);
+  uint64_t* status = reinterpret_cast<uint64_t*>(scratch + 16);
+  DFM_CUDA(cudaMemsetAsync(scratch, 0, 16 + tiles * 8, ctx.stream));
+  lookback_flags_kernel<Pred, Out><<<(unsigned)tiles, kScanThreads, 0, ctx.stream>>>(
+      pred, out, count, status, ticket, total_dev);
+  DFM_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ radix sort
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;

@@ -506,6 +506,47 @@ __global__ void __launch_bounds__(256) filt_mark_kernel(const unsigned long long
   }
 }
 
+// mark + compact in one look-back pass (prims::lookback_flags): a key alone in its
+// cell leaves — as a singleton block right away under relabel-in-place (id B + i,
+// its own leader; rip_hashed_cand_kernel then visits the table states only), else
+// slot_of = kUnique — and the others stay candidates, in ascending state order
+struct FiltPred {
+  const unsigned long long* keys;
+  const uint32_t* F;
+  const uint32_t* cand;  // nullptr: the identity list 0..m-1
+  uint64_t seed;
+  bool hashed;
+  int shift;
+  __device__ bool operator()(uint64_t j) const {
+    const uint64_t i = cand ? cand[j] : j;
+    const uint64_t c = (table_hash(ld_key_stream(keys + i, policy_evict_first()), hashed, seed) >>
+                        shift) & ((1ull << kFilterCellBits) - 1);
+    return (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
+  }
+};
+struct FiltOut {
+  const uint32_t* cand;
+  uint32_t* out;
+  uint32_t* slot_of;  // plain passes
+  uint32_t* ids;      // relabel-in-place passes (non-null): ids, lead, flag
+  uint8_t* lead;
+  uint8_t* flag;
+  uint32_t B;
+  __device__ void operator()(uint64_t j, uint32_t rank, uint32_t dup) const {
+    const uint32_t i = cand ? cand[j] : (uint32_t)j;
+    if (dup) {
+      out[rank] = i;
+      if (!ids) slot_of[i] = 0u;
+    } else if (ids) {
+      ids[i] = B + i;
+      lead[i] = 1;
+      flag[i] = 0;
+    } else {
+      slot_of[i] = kUnique;
+    }
+  }
+};
+
 // candidates in ascending state order (look-back scan over the previous list)
 struct CandIn {
   const uint32_t* cand;  // nullptr: the identity list 0..m-1
@@ -755,6 +796,26 @@ __global__ void __launch_bounds__(256) rip_hashed_kernel(uint64_t m,
     const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
     const uint32_t rep_i = ~sl.x;
     if (rep_i != (uint32_t)i && sig != nullptr && rows_differ(sig, row, words, i, rep_i))
+      atomicOr(collision, 1ull);
+    ids[i] = B + (uint32_t)m + s;
+    flag[i] = (sl.y & 0x7FFFFFFFu) >= 2 ? 1 : 0;
+  }
+}
+
+// the table states of a filtered relabel-in-place pass (FiltOut labelled the rest)
+__global__ void __launch_bounds__(256) rip_hashed_cand_kernel(
+    uint64_t nc, const uint32_t* __restrict__ cand, uint64_t m,
+    const uint32_t* __restrict__ slot_of, const Slot* __restrict__ slots,
+    const uint32_t* __restrict__ sig, uint32_t words, uint32_t row,
+    unsigned long long* collision, uint32_t B, uint32_t* __restrict__ ids,
+    uint8_t* __restrict__ flag) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += stride) {
+    const uint32_t i = cand[j];
+    const uint32_t s = slot_of[i];
+    const uint2 sl = *reinterpret_cast<const uint2*>(&slots[s].rep);
+    const uint32_t rep_i = ~sl.x;
+    if (rep_i != i && sig != nullptr && rows_differ(sig, row, words, i, rep_i))
       atomicOr(collision, 1ull);
     ids[i] = B + (uint32_t)m + s;
     flag[i] = (sl.y & 0x7FFFFFFFu) >= 2 ? 1 : 0;
@@ -1167,6 +1228,13 @@ int run_small(Ctx& ctx, const DevDfa& d, const Deadline& dl, unsigned grid, uint
 }
 
 // partitioned grouping (sortpr_group.cuh) is opt-in until its radix passes beat the
+// filter mark fused with its candidate compaction (DFM_SORTPR_FILT_FUSED=0: the
+// separate mark kernel + scan, for A/B runs)
+bool filt_fused() {
+  const char* e = getenv("DFM_SORTPR_FILT_FUSED");
+  return !(e && e[0] == '0');
+}
+
 // global table: DFM_SORTPR_PARTITION=1
 bool partition_enabled() {
   const char* e = getenv("DFM_SORTPR_PARTITION");
@@ -1606,6 +1674,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     uint64_t rip_bound = 0;  // its id bound: the direct table's size
     const Slot* rip_slots = nullptr;
     bool hrip = false;        // filtered pass relabelled in place (ids into res, swapped in)
+    bool hrip_pre = false;    // ... with its singletons labelled by the filter itself
     uint64_t hrip_table = 0;  // states that reached its table
     bool act_scanned = false;  // the partitioned path compacts inside the pass
     if (m > 0) {
@@ -1727,6 +1796,10 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         uint64_t dups = m;
         // a second level on independent hash bits re-tests only the first level's
         // candidates: ~31 % -> ~4 % of the keys reach the table at 1e8 distinct keys
+        // relabel-in-place over all states (decided before the filter: the table's
+        // capacity is at most max(1024, 5m/2)): the filter labels its singletons
+        hrip_pre = rip_on && act == nullptr &&
+                   (uint64_t)B + m + std::max<uint64_t>(1024, m * 5 / 2) < (1ull << 32);
         for (int level = 0; level < 2 && dups >= kFilterMinStates; ++level) {
           ProfScope p(ctx, "insert", (1ull << (kFilterCellBits - 2)) + dups * (8ull + 8 + 4));
           DFM_CUDA(cudaMemsetAsync(sc + 6, 0, 8, ctx.stream));
@@ -1735,11 +1808,19 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           filt_set_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(keys, dups, !packed, seed,
                                                                        F, level, cin);
           DFM_LAUNCH_CHECK();
-          filt_mark_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(
-              keys, dups, !packed, seed, F, slot_of, level, cin);
-          DFM_LAUNCH_CHECK();
-          prims::lookback_scan(ctx, "sc.cand", dups, CandIn{cin, slot_of},
-                               CandOut{cin, cbuf[level]}, sc + 6);
+          if (filt_fused()) {
+            prims::lookback_flags(
+                ctx, "sc.cand", dups,
+                FiltPred{keys, F, cin, seed, !packed, level == 0 ? 64 - kFilterCellBits : 8},
+                FiltOut{cin, cbuf[level], slot_of, hrip_pre ? res : nullptr, lead, flag, B},
+                sc + 6);
+          } else {
+            filt_mark_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(
+                keys, dups, !packed, seed, F, slot_of, level, cin);
+            DFM_LAUNCH_CHECK();
+            prims::lookback_scan(ctx, "sc.cand", dups, CandIn{cin, slot_of},
+                                 CandOut{cin, cbuf[level]}, sc + 6);
+          }
           DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 6, sc + 6, 8, cudaMemcpyDeviceToHost,
                                    ctx.stream));
           ctx.sync();
@@ -1767,6 +1848,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       ip.ids_out = rip ? block : nullptr;
       ip.id_off = rip_off;
       hrip = rip_on && filtered && act == nullptr && (uint64_t)B + m + cap < (1ull << 32);
+      hrip_pre = hrip_pre && filtered && filt_fused();  // (implies hrip)
       hrip_table = ncand;
       if (blocked) {
         ProfScope p(ctx, "insert", m * (8ull + 4 + 1 + 4 + 16 + 4));
@@ -1812,10 +1894,16 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
       if (hrip) {
         {
           // slot_of 4 + id 4 + flag 1 (+ lead 1 for unique states) + slot 8 for table states
-          ProfScope p(ctx, "scan", m * 10ull + ncand * 8ull);
-          rip_hashed_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
-              m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
-              reinterpret_cast<unsigned long long*>(sc + 2), B, res, lead, flag);
+          ProfScope p(ctx, "scan", (hrip_pre ? 0 : m * 10ull) + ncand * 8ull);
+          if (hrip_pre) {
+            rip_hashed_cand_kernel<<<grid_for(ctx, ncand), 256, 0, ctx.stream>>>(
+                ncand, cand, m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
+                reinterpret_cast<unsigned long long*>(sc + 2), B, res, flag);
+          } else {
+            rip_hashed_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+                m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
+                reinterpret_cast<unsigned long long*>(sc + 2), B, res, lead, flag);
+          }
           DFM_LAUNCH_CHECK();
         }
         ProfScope p(ctx, "scan", cap * 8ull);
