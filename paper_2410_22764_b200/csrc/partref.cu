@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
     // the previous pass's "changed" flag is read here and tested after this pass's
     // election, off the critical path: a pass after a stable one changes nothing
     const uint32_t prev_changed =
-        p > 0 ? *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) : 1u;
+        p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
     bool any = false;
     if (kCas) {
       for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kPersistThreads) persistent_kernel(PersistentA
     sel ^= 1;
     ++p;
   }
-  if (!stable && p > 0 && *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u)
+  if (!stable && p > 0 && prims::ld_relaxed_u32(&a.changed[p - 1]) == 0u)
     stable = true;
   if (first == 0) {
     a.out[0] = p;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
     const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
     unsigned long long* ccur = (pass & 1) ? a.cells1 : a.cells0;
     const uint32_t prev_changed =
-        p > 0 ? *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) : 1u;
+        p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
     bool any = false;
     for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
       const uint64_t qi = qb + (threadIdx.x & 31);
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
     sel ^= 1;
     ++p;
   }
-  if (!stable && p > 0 && *reinterpret_cast<volatile uint32_t*>(&a.changed[p - 1]) == 0u)
+  if (!stable && p > 0 && prims::ld_relaxed_u32(&a.changed[p - 1]) == 0u)
     stable = true;
   if (first == 0) {
     a.out[0] = p;

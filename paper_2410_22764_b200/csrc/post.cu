@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(512) bfs_kernel(BfsArgs a) {
                    clr_c = (uint32_t)((lvl + 2) % 3);
     const uint32_t* cur_f = (lvl & 1) ? a.f1 : a.f0;
     uint32_t* nxt_f = (lvl & 1) ? a.f0 : a.f1;
-    const uint32_t size = *reinterpret_cast<volatile uint32_t*>(&a.cnt[cur_c]);
+    const uint32_t size = prims::ld_relaxed_u32(&a.cnt[cur_c]);
     if (size == 0) {
       done = true;
       break;

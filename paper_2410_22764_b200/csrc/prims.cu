@@ -35,7 +35,7 @@ __global__ void radix_bucket_scan_kernel(const uint32_t* __restrict__ hist,
 }
 
 template <bool kIdentVals>
-__global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
+__global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t count, int shift,
     const uint32_t* __restrict__ bucket_base, uint64_t* status, uint32_t* ticket) {
@@ -45,13 +45,13 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
   uint32_t* s_cnt = s_vals + kRsTile;         // [warp][digit]
   uint32_t* s_start = s_cnt + kRsWarps * 256;  // tile-local digit start
   uint32_t* s_glob = s_start + 256;            // global destination base per digit
-  uint32_t* s_misc = s_glob + 256;             // [0] tile id, [1..9] warp sums
-  uint32_t* s_hist = s_misc + 16;              // tile digit histogram (published early)
+  uint32_t* s_misc = s_glob + 256;             // [0] tile id, [1..kRsWarps+1] warp sums
+  uint32_t* s_hist = s_misc + 32;              // tile digit histogram (published early)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_misc[0] = atomicAdd(ticket, 1u);
   for (int i = tid; i < kRsWarps * 256; i += kRsThreads) s_cnt[i] = 0;
-  s_hist[tid] = 0;
+  if (tid < 256) s_hist[tid] = 0;
   __syncthreads();
   const uint32_t tile = s_misc[0];
   const uint64_t tile_base = (uint64_t)tile * kRsTile;
@@ -76,8 +76,10 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
   for (int j = 0; j < kRsItems; ++j)
     if (dig[j] < 256) atomicAdd(&s_hist[dig[j]], 1u);
   __syncthreads();
-  if (tile == 0) st_volatile(status + tid, kFlagInc | s_hist[tid]);
-  else st_volatile(status + (uint64_t)tile * 256 + tid, kFlagAgg | s_hist[tid]);
+  if (tid < 256) {
+    if (tile == 0) st_volatile(status + tid, kFlagInc | s_hist[tid]);
+    else st_volatile(status + (uint64_t)tile * 256 + tid, kFlagAgg | s_hist[tid]);
+  }
   uint32_t* my_cnt = s_cnt + warp * 256;
 #pragma unroll
   for (int j = 0; j < kRsItems; ++j) {
@@ -94,8 +96,8 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
   __syncthreads();
   // per digit: exclusive prefix across warps (stability: warp chunks are in order)
   uint32_t total = 0;
-  {
-    const int d = tid;  // kRsThreads == 256 digits
+  if (tid < 256) {
+    const int d = tid;  // one digit per thread of the first 256
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
@@ -107,21 +109,30 @@ __global__ void __launch_bounds__(kRsThreads, 4) onesweep_kernel(
   }
   uint32_t tile_total;
   const uint32_t start = block_exclusive_sum<kRsThreads>(total, s_misc + 1, &tile_total);
-  s_start[tid] = start;
+  if (tid < 256) s_start[tid] = start;
   // decoupled look-back, one digit per thread
-  {
+  if (tid < 256) {
     const int d = tid;
     uint64_t prefix = 0;
     if (tile > 0) {
+      // kLb predecessors per step: their loads are in flight together (a walk over
+      // tiles that published only aggregates costs one L2 round trip per kLb tiles)
+      constexpr int kLb = 4;
       int64_t t = (int64_t)tile - 1;
-      while (t >= 0) {
-        uint64_t s;
-        do {
-          s = ld_volatile(status + (uint64_t)t * 256 + d);
-        } while ((s & ~kValMask) == 0);
-        prefix += s & kValMask;
-        if (s & kFlagInc) break;
-        --t;
+      bool done = false;
+      while (!done) {
+        uint64_t s[kLb];
+#pragma unroll
+        for (int u = 0; u < kLb; ++u)
+          s[u] = t - u >= 0 ? ld_volatile(status + (uint64_t)(t - u) * 256 + d) : kFlagInc;
+#pragma unroll
+        for (int u = 0; u < kLb; ++u) {
+          if (done) break;
+          while ((s[u] & ~kValMask) == 0) s[u] = ld_volatile(status + (uint64_t)(t - u) * 256 + d);
+          prefix += s[u] & kValMask;
+          done = (s[u] & kFlagInc) != 0;
+        }
+        t -= kLb;
       }
       st_volatile(status + (uint64_t)tile * 256 + d, kFlagInc | (prefix + total));
     }

@@ -24,13 +24,29 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// look-back status words are single 64-bit words read and written whole: relaxed
+// GPU-scope accesses suffice (ld/st.volatile lower to system-scope STRONG.SYS
+// accesses, which the look-back spins on)
 __device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// test-before-set hint: a weak load at L2 (.cg); a stale 0 only costs a redundant
+// atomicOr
+__device__ __forceinline__ uint32_t ld_hint_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// a flag written by other CTAs before a grid barrier (or polled): GPU scope
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // look-back status word: [63:62] flag, [61:0] value (value + flag in one
@@ -273,11 +289,13 @@ void lookback_flags(Ctx& ctx, const char* slot, uint64_t count, Pred pred, Out o
 }
 
 // ------------------------------------------------------------------ radix sort
-constexpr int kRsThreads = 256;
+constexpr int kRsThreads = 256;   // >= 256: the first 256 threads own one digit each
+constexpr int kRsBlocksPerSm = 4;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsItems = 8;
 constexpr int kRsTile = kRsThreads * kRsItems;  // 4096
-constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 64 + 1024;
+constexpr int kRsSmem = kRsTile * 8 + kRsTile * 4 + kRsWarps * 256 * 4 + 256 * 4 * 2 + 128 + 1024;
+static_assert(kRsWarps + 2 <= 32, "s_misc holds the tile id and the warp sums");
 
 // Sorts (keys, vals) of length count on the low `bits` bits.  ident_vals: the
 // input values are 0..count-1 and `vals` is not read.  Uses alt_keys/alt_vals

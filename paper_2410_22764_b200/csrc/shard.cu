@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(256) direct_set_kernel(const unsigned long lon
     const uint32_t m = 1u << (key & 31);
     uint32_t* w = bp + 2 * (key >> 5);
     // test before set: most keys of a dense pass repeat
-    if ((*reinterpret_cast<volatile uint32_t*>(w) & m) == 0) atomicOr(w, m);
+    if ((prims::ld_hint_u32(w) & m) == 0) atomicOr(w, m);
   }
 }
 

@@ -210,6 +210,45 @@ __global__ void __launch_bounds__(256) scatter_kernel(uint64_t m, const uint32_t
   }
 }
 
+// Sort-back relabel: instead of scattering each sorted position's new id to its
+// state (random 4-byte + 1-byte writes: a DRAM read-modify-write each), pair the
+// new id (| run size >= 2 in bit 31) with the active index and radix-sort the pairs
+// back into active order — streaming passes — then write block/flag in order.
+__global__ void __launch_bounds__(256) unscatter_pairs_kernel(
+    uint64_t m, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ run_of,
+    const uint32_t* __restrict__ runstart, const uint32_t* __restrict__ newid,
+    uint64_t* __restrict__ pkeys, uint32_t* __restrict__ pvals, const uint64_t* scalars) {
+  if (scalars[2] != 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint32_t r = run_of[j];
+    const uint32_t len = runstart[r + 1] - runstart[r];
+    pkeys[j] = vals[j];
+    pvals[j] = newid[r] | (len >= 2 ? 0x80000000u : 0u);
+  }
+}
+__global__ void __launch_bounds__(256) unscatter_apply_kernel(uint64_t m,
+                                                              const uint32_t* __restrict__ pvals,
+                                                              const uint32_t* __restrict__ act,
+                                                              uint32_t* __restrict__ block,
+                                                              uint8_t* __restrict__ flag,
+                                                              const uint64_t* scalars) {
+  if (scalars[2] != 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint32_t v = pvals[i];
+    const uint32_t q = act ? act[i] : (uint32_t)i;
+    block[q] = v & 0x7FFFFFFFu;
+    flag[q] = (uint8_t)(v >> 31);
+  }
+}
+
+// DFM_RADIX_UNSCATTER=0: the plain scatter (A/B runs)
+bool unscatter_enabled() {
+  const char* e = getenv("DFM_RADIX_UNSCATTER");
+  return !(e && e[0] == '0');
+}
+
 struct ActIn {
   const uint32_t* act;
   const uint8_t* flag;
@@ -370,7 +409,26 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
         prims::lookback_scan(ctx, "sc.fresh", m, FreshIn{runblock, runstart, cells, sc, epoch},
                              FreshOut{runblock, newid, sc, B}, sc + 1);
       }
-      {
+      if (unscatter_enabled() && n < (1ull << 31) && m >= (1u << 20)) {
+        // the sorted buffers are dead once the pairs are built: they are the sort's
+        // alternates.  Pairs: run_of 4 + runstart pair 8 + value 4 + new id 4 + key 8 +
+        // value 4; the sort back; apply: value 4 + active id 4 + block 4 + flag 1
+        uint64_t* pk = alt ? keysA : keysB;
+        uint32_t* pv = alt ? valsA : valsB;
+        {
+          ProfScope p(ctx, "relabel", m * 32ull);
+          unscatter_pairs_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+              m, vs, run_of, runstart, newid, pk, pv, sc);
+          DFM_LAUNCH_CHECK();
+        }
+        const bool alt2 = prims::radix_sort_pairs(ctx, pk, pv, const_cast<uint64_t*>(ks),
+                                                  const_cast<uint32_t*>(vs), m,
+                                                  bit_width_u32((uint32_t)(m - 1)), false);
+        ProfScope p(ctx, "relabel", m * 13ull);
+        unscatter_apply_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
+            m, alt2 ? vs : pv, act, block, flag, sc);
+        DFM_LAUNCH_CHECK();
+      } else {
         // run_of 4 + runstart pair 8 + value 4 + active id 4 + new id 4 + block write 4 + flag 1
         ProfScope p(ctx, "relabel", m * 29ull);
         scatter_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, vs, act, run_of, runstart,

@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(1024, (kIdBits <= 16 || kTile24) ? 2 : 1)
           if (p.present) {  // test before set: most keys of a dense pass are repeats
             const uint32_t bit = 1u << (key & 31);
             uint32_t* word = p.present + 2 * (key >> 5);  // (interleaved with the prefixes)
-            if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
+            if (!(prims::ld_hint_u32(word) & bit)) atomicOr(word, bit);
           }
         } else {
           uint32_t* row = p.sig + i * (uint64_t)p.row;

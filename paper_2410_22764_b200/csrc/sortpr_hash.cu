@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(256) direct_keys_kernel(
     keys[i] = key;
     const uint32_t bit = 1u << (key & 31);
     uint32_t* word = present + 2 * (key >> 5);
-    if (!(*reinterpret_cast<volatile uint32_t*>(word) & bit)) atomicOr(word, bit);
+    if (!(prims::ld_hint_u32(word) & bit)) atomicOr(word, bit);
   }
 }
 
