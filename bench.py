@@ -748,17 +748,15 @@ def run_sharded(args, rank: int, world: int, local: int):
                       "rows, the sharded run, D2H of the owned labels); max over ranks"}
     single = None
     if world == 1:
-        # the single-GPU engine on the same DFA, after the sharded context
-        # released its HBM (at 1e9 states both would not fit together)
-        host_d = delta.cpu().numpy().view(np.uint32)
-        host_a = acc.cpu().numpy()
+        # the single-GPU engine on the same DFA, generated on the device by
+        # the same generator exactly as the default (single-engine) line does, after the
+        # sharded context released its HBM (at 1e9 states both would not fit together)
         del delta, acc, out
         se.close()
         torch.cuda.empty_cache()
         e1 = dfm.Engine(local)
         e1.set_stream(stream.cuda_stream)
-        dd = e1.upload(dfm.Dfa(n_total, args.k, host_d, host_a, 0))
-        del host_d, host_a
+        dd = e1.random_dfa_device(n_total, args.k, args.seed, args.p)
         e1.run_device(dfm.Algo.sort, dd)
         sm = []
         for _ in range(max(1, min(args.steps, 5))):

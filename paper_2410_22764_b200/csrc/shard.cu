@@ -142,13 +142,41 @@ __device__ __forceinline__ unsigned long long ld_key(const unsigned long long* a
   return v;
 }
 
-__global__ void __launch_bounds__(256) gfilt_set_kernel(const unsigned long long* __restrict__ keys,
-                                                        uint64_t count, uint32_t* F, int level,
-                                                        const uint32_t* __restrict__ slot_of) {
+// Fused mark + compaction (prims::lookback_flags, as the single-GPU engine's filter):
+// a key alone in its cell is a group of its own and is labelled on the spot — the
+// u-th singleton of the level takes base + u (u = position - candidates before it) —
+// and the others leave as the next level's list, in ascending order.  The table then
+// sees the last list only, and so do the label and member kernels.
+struct GFiltPred {
+  const unsigned long long* keys;
+  const uint32_t* F;
+  const uint32_t* cand;  // nullptr: all items
+  int level;
+  __device__ bool operator()(uint64_t j) const {
+    const uint64_t i = cand ? cand[j] : j;
+    const uint64_t c = cell_of(ld_key(keys + i, pol_first()), level);
+    return (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
+  }
+};
+struct GFiltOut {
+  const uint32_t* cand;
+  uint32_t* out;
+  uint32_t* label;
+  uint32_t base;
+  __device__ void operator()(uint64_t j, uint32_t rank, uint32_t dup) const {
+    const uint32_t i = cand ? cand[j] : (uint32_t)j;
+    if (dup) out[rank] = i;
+    else label[i] = base + (uint32_t)j - rank;
+  }
+};
+
+__global__ void __launch_bounds__(256) gfilt_set_list_kernel(
+    const unsigned long long* __restrict__ keys, uint64_t count, uint32_t* F, int level,
+    const uint32_t* __restrict__ cand) {
   const uint64_t pf = pol_first(), pl = pol_last();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    if (level > 0 && slot_of[i] == kUniq) continue;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+    const uint64_t i = cand ? cand[j] : j;
     const uint64_t c = cell_of(ld_key(keys + i, pf), level);
     const uint32_t bit = (uint32_t)(c & 15) * 2;
     uint32_t* w = &F[c >> 4];
@@ -159,25 +187,6 @@ __global__ void __launch_bounds__(256) gfilt_set_kernel(const unsigned long long
       asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(w), "r"(2u << bit),
                    "l"(pl) : "memory");
   }
-}
-
-__global__ void __launch_bounds__(256) gfilt_mark_kernel(const unsigned long long* __restrict__ keys,
-                                                         uint64_t count, const uint32_t* __restrict__ F,
-                                                         int level, uint32_t* __restrict__ slot_of,
-                                                         unsigned long long* dups) {
-  const uint64_t pf = pol_first();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  uint32_t mine = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    if (level > 0 && slot_of[i] == kUniq) continue;
-    const uint64_t c = cell_of(ld_key(keys + i, pf), level);
-    const bool dup = (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
-    slot_of[i] = dup ? 0u : kUniq;
-    mine += dup ? 1u : 0u;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(dups, (unsigned long long)mine);
 }
 
 // Insert with CTA-level pre-aggregation: a tile's keys first meet in a shared-memory
@@ -254,17 +263,15 @@ __global__ void __launch_bounds__(256) group_insert_kernel(const unsigned long l
   }
 }
 
-// filtered passes: only the filter's candidates (a few % of mostly-distinct keys)
-// reach the table, each straight to the global table (no per-tile shared-memory
-// aggregation: their keys rarely repeat inside a tile)
-__global__ void __launch_bounds__(256) group_insert_cand_kernel(
-    const unsigned long long* __restrict__ keys, uint64_t count, GSlot* slots, uint64_t cap,
-    uint32_t* __restrict__ slot_of) {
+// the filtered list's states: table insert, then label / members as below
+__global__ void __launch_bounds__(256) group_insert_list_kernel(
+    const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ list, uint64_t nl,
+    GSlot* slots, uint64_t cap, uint32_t* __restrict__ slot_of) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-    if (slot_of[i] == kUniq) continue;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += stride) {
+    const uint32_t i = list[j];
     const uint64_t g = global_insert(slots, cap, keys[i]);
-    atomicMax(&slots[g].rep, ~(uint32_t)i);
+    atomicMax(&slots[g].rep, ~i);
     slot_of[i] = (uint32_t)g;
   }
 }
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(256) group_insert_cand_kernel(
 // a member is the representative of its group if it is alone (filter) or the table's
 // minimum; representatives take an id from one atomic per CTA step
 __global__ void __launch_bounds__(256) group_label_kernel(uint64_t count, GSlot* slots,
+                                                          const uint32_t* __restrict__ list,
                                                           const uint32_t* __restrict__ slot_of,
                                                           const uint32_t* __restrict__ sig,
                                                           uint32_t words, uint32_t* __restrict__ label,
@@ -282,10 +290,11 @@ __global__ void __launch_bounds__(256) group_label_kernel(uint64_t count, GSlot*
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < count; base += stride) {
-    const uint64_t i = base + threadIdx.x;
+    const uint64_t j = base + threadIdx.x;
+    const uint64_t i = j < count ? (list ? list[j] : j) : 0;
     bool rep = false;
     uint32_t s = kUniq;
-    if (i < count) {
+    if (j < count) {
       s = slot_of[i];
       if (s == kUniq) {
         rep = true;
@@ -324,10 +333,12 @@ __global__ void __launch_bounds__(256) group_label_kernel(uint64_t count, GSlot*
 }
 
 __global__ void group_members_kernel(uint64_t count, const GSlot* __restrict__ slots,
+                                     const uint32_t* __restrict__ list,
                                      const uint32_t* __restrict__ slot_of,
                                      uint32_t* __restrict__ label) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+    const uint32_t i = list ? list[j] : (uint32_t)j;
     const uint32_t s = slot_of[i];
     if (s == kUniq) continue;
     if (~slots[s].rep != (uint32_t)i) label[i] = slots[s].gid;
@@ -505,47 +516,71 @@ void shard_group(Ctx& ctx, const void* keys, const void* sig, uint32_t words, ui
       uint64_t dups = count;
       ProfScope p(ctx, "group", count * (8ull + 16 + 4 + 4 + 4 + 4ull * words));
       // the filter pays off for hashed keys (late, mostly-distinct passes); exact packed
-      // keys belong to the early passes, where a few keys repeat over all items
-      if (count >= kFilterMin && words > 0) {
+      // keys belong to the early passes, where a few keys repeat over all items.  Above
+      // one key per cell (2^28) nearly every key shares its cell: straight to the table
+      if (count >= kFilterMin && count <= (1ull << kCellBits) && words > 0) {
+        // filtered: singletons labelled by the fused mark, the table sees the last list
         uint32_t* F = ctx.slot_t<uint32_t>("shard.filter", 1ull << (kCellBits - 4));
-        for (int level = 0; level < 2 && dups >= kFilterMin; ++level) {
+        uint32_t* lbuf[2] = {ctx.slot_t<uint32_t>("shard.cand0", count),
+                             ctx.slot_t<uint32_t>("shard.cand1", count)};
+        uint32_t* label = static_cast<uint32_t*>(label_out);
+        const uint32_t* list = nullptr;
+        uint64_t nl = count, singles = 0;
+        for (int level = 0; level < 2 && nl >= kFilterMin; ++level) {
           DFM_CUDA(cudaMemsetAsync(F, 0, 1ull << (kCellBits - 2), ctx.stream));
-          DFM_CUDA(cudaMemsetAsync(sc + 2, 0, 8, ctx.stream));
-          gfilt_set_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-              static_cast<const unsigned long long*>(keys), count, F, level, slot_of);
+          gfilt_set_list_kernel<<<grid_for(ctx, nl), 256, 0, ctx.stream>>>(
+              static_cast<const unsigned long long*>(keys), nl, F, level, list);
           DFM_LAUNCH_CHECK();
-          gfilt_mark_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-              static_cast<const unsigned long long*>(keys), count, F, level, slot_of,
-              reinterpret_cast<unsigned long long*>(sc + 2));
-          DFM_LAUNCH_CHECK();
+          prims::lookback_flags(
+              ctx, "shard.fscan", nl,
+              GFiltPred{static_cast<const unsigned long long*>(keys), F, list, level},
+              GFiltOut{list, lbuf[level], label, (uint32_t)singles}, sc + 2);
           DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 50, sc + 2, 8, cudaMemcpyDeviceToHost,
                                    ctx.stream));
           ctx.sync();
-          dups = ctx.h_scalars[50];
+          const uint64_t d = ctx.h_scalars[50];
+          singles += nl - d;
+          nl = d;
+          list = lbuf[level];
+        }
+        const uint64_t cap = std::max<uint64_t>(1024, nl * 5 / 2);  // load <= 0.4
+        auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
+        DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
+        // table groups are numbered after the singletons
+        ctx.h_scalars[51] = singles;
+        DFM_CUDA(cudaMemcpyAsync(sc, ctx.h_scalars + 51, 8, cudaMemcpyHostToDevice, ctx.stream));
+        if (nl) {
+          group_insert_list_kernel<<<grid_for(ctx, nl), 256, 0, ctx.stream>>>(
+              static_cast<const unsigned long long*>(keys), list, nl, slots, cap, slot_of);
+          DFM_LAUNCH_CHECK();
+          group_label_kernel<<<grid_for(ctx, nl), 256, 0, ctx.stream>>>(
+              nl, slots, list, slot_of, static_cast<const uint32_t*>(sig), words, label,
+              reinterpret_cast<unsigned long long*>(sc),
+              reinterpret_cast<unsigned long long*>(sc + 1));
+          DFM_LAUNCH_CHECK();
+          group_members_kernel<<<grid_for(ctx, nl), 256, 0, ctx.stream>>>(nl, slots, list,
+                                                                            slot_of, label);
+          DFM_LAUNCH_CHECK();
         }
       } else {
         DFM_CUDA(cudaMemsetAsync(slot_of, 0, count * 4, ctx.stream));
-      }
-      const uint64_t cap = std::max<uint64_t>(1024, dups * 5 / 2);  // load <= 0.4
-      auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
-      DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
-      if (dups < count)  // filtered: candidates only
-        group_insert_cand_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-            static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
-      else
+        const uint64_t cap = std::max<uint64_t>(1024, dups * 5 / 2);  // load <= 0.4
+        auto* slots = static_cast<GSlot*>(ctx.slot("shard.table", cap * sizeof(GSlot)));
+        DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(GSlot), ctx.stream));
         group_insert_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(count, kTileItems),
                                                            ctx.num_sms * 8ull),
                               256, 0, ctx.stream>>>(
             static_cast<const unsigned long long*>(keys), count, slots, cap, slot_of);
-      DFM_LAUNCH_CHECK();
-      group_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-          count, slots, slot_of, static_cast<const uint32_t*>(sig), words,
-          static_cast<uint32_t*>(label_out), reinterpret_cast<unsigned long long*>(sc),
-          reinterpret_cast<unsigned long long*>(sc + 1));
-      DFM_LAUNCH_CHECK();
-      group_members_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
-          count, slots, slot_of, static_cast<uint32_t*>(label_out));
-      DFM_LAUNCH_CHECK();
+        DFM_LAUNCH_CHECK();
+        group_label_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+            count, slots, nullptr, slot_of, static_cast<const uint32_t*>(sig), words,
+            static_cast<uint32_t*>(label_out), reinterpret_cast<unsigned long long*>(sc),
+            reinterpret_cast<unsigned long long*>(sc + 1));
+        DFM_LAUNCH_CHECK();
+        group_members_kernel<<<grid_for(ctx, count), 256, 0, ctx.stream>>>(
+            count, slots, nullptr, slot_of, static_cast<uint32_t*>(label_out));
+        DFM_LAUNCH_CHECK();
+      }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 48, sc, 16, cudaMemcpyDeviceToHost, ctx.stream));
     ctx.sync();

@@ -29,7 +29,10 @@
 
 constexpr uint32_t kRs = 49152;          // states per target range (16-bit offsets)
 constexpr uint32_t kMaxRanges = 4096;    // n <= 2.01e8 on the blocked path
-constexpr uint32_t kWinElems = 32768;    // transitions per source window (u16 tile slots)
+#ifndef DFM_WIN_ELEMS  // (build-variant experiments: tools/build_variant.sh)
+#define DFM_WIN_ELEMS 32768
+#endif
+constexpr uint32_t kWinElems = DFM_WIN_ELEMS;  // transitions per source window (u16 tile slots)
 constexpr uint32_t kSliceBytes = 192u << 10;
 
 struct Layout {

@@ -442,7 +442,10 @@ __global__ void __launch_bounds__(256) insert_small_kernel(InsertParams p, uint3
 // L2-resident footprint (tools/l2_bench.cu: ~190 G atomics/s vs ~21-25 G/s for
 // a > L2 table).  Keys alone in their cell are singleton groups and skip the
 // global table; only the rest (true duplicates + cell collisions) is inserted.
-constexpr int kFilterCellBits = 28;
+#ifndef DFM_FILTER_CELL_BITS  // (build-variant experiments)
+#define DFM_FILTER_CELL_BITS 28
+#endif
+constexpr int kFilterCellBits = DFM_FILTER_CELL_BITS;
 
 __device__ __forceinline__ unsigned long long table_hash(unsigned long long key, bool hashed,
                                                          uint64_t seed) {
