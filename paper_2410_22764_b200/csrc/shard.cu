@@ -112,8 +112,8 @@ struct GSlot {
 };
 
 // Grouping of the received keys (64-bit signature hashes, never 0) — the hash
-// engine's recipe (sortpr_hash.cu): a two-level uniqueness filter (2-bit cells,
-// 64 MB, L2-resident) lets keys that are alone in their cell skip the table;
+// engine's recipe (sortpr_hash.cu): a two-level uniqueness filter ("seen" and "seen
+// twice" bitmaps of 2^28 cells, 64 MB, L2-resident) lets keys alone in their cell skip the table;
 // the rest goes through an open-addressing table at load <= 0.4; group ids come
 // from one atomic per CTA step (no global scan).
 constexpr uint32_t kUniq = 0xFFFFFFFFu;
@@ -155,7 +155,7 @@ struct GFiltPred {
   __device__ bool operator()(uint64_t j) const {
     const uint64_t i = cand ? cand[j] : j;
     const uint64_t c = cell_of(ld_key(keys + i, pol_first()), level);
-    return (F[c >> 4] >> ((uint32_t)(c & 15) * 2 + 1)) & 1u;
+    return (F[(1ull << (kCellBits - 5)) + (c >> 5)] >> (uint32_t)(c & 31)) & 1u;
   }
 };
 struct GFiltOut {
@@ -177,15 +177,16 @@ __global__ void __launch_bounds__(256) gfilt_set_list_kernel(
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
     const uint64_t i = cand ? cand[j] : j;
+    // "seen" bitmap (first 2^28 bits) and "seen twice" bitmap (next 2^28 bits)
     const uint64_t c = cell_of(ld_key(keys + i, pf), level);
-    const uint32_t bit = (uint32_t)(c & 15) * 2;
-    uint32_t* w = &F[c >> 4];
+    const uint32_t bit = 1u << (uint32_t)(c & 31);
     uint32_t old;
     asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
-                 : "=r"(old) : "l"(w), "r"(1u << bit), "l"(pl) : "memory");
-    if (((old >> bit) & 3u) == 1u)
-      asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(w), "r"(2u << bit),
-                   "l"(pl) : "memory");
+                 : "=r"(old) : "l"(&F[c >> 5]), "r"(bit), "l"(pl) : "memory");
+    if (old & bit)
+      asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(
+                       &F[(1ull << (kCellBits - 5)) + (c >> 5)]),
+                   "r"(bit), "l"(pl) : "memory");
   }
 }
 
