@@ -244,6 +244,12 @@ void shard_layout_free(ShardLayout* s);
 void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* full,
                        const uint32_t* own, uint64_t m, int w, bool hashed, uint64_t seed,
                        unsigned long long* keys, uint32_t* sig, uint32_t row);
+// the same builder for the radix engine (sort_pr.cu) over the whole DFA: keys of the
+// m active states (ascending act, or all states) in active order
+ShardLayout* radix_layout_build(Ctx& ctx, const DevDfa& d);
+void radix_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* ids,
+                       const uint32_t* act, uint64_t m, const uint32_t* block, int w, bool hashed,
+                       uint64_t seed, unsigned long long* keys, uint32_t* sig, uint32_t row);
 // contiguous shards of S = ceil(n/world) rounded up to a multiple of 32 states (a
 // rank's slice of a bit-packed id vector is whole words): rank r owns
 // [r*S, min(n, (r+1)*S))

@@ -34,6 +34,9 @@ __global__ void radix_bucket_scan_kernel(const uint32_t* __restrict__ hist,
   base[blockIdx.x * 256 + threadIdx.x] = e;
 }
 
+#ifndef DFM_RS_BALLOT_RANK  // digit peers from 9 ballots (1) or match.any (0): sort 28.4 -> 26.7 ms
+#define DFM_RS_BALLOT_RANK 1
+#endif
 template <bool kIdentVals>
 __global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
@@ -84,7 +87,17 @@ __global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
 #pragma unroll
   for (int j = 0; j < kRsItems; ++j) {
     const uint32_t d = dig[j];
+#if DFM_RS_BALLOT_RANK
+    // lanes holding the same 9-bit value (digit, or 256 = no item): one ballot per bit
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+#else
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#endif
     const uint32_t lt = __popc(peers & lanemask_lt());
     uint32_t base = 0;
     if (d < 256) base = my_cnt[d];

@@ -20,6 +20,8 @@
 // keep_kernel / fresh scan / scatter_kernel, active-list compaction scan,
 // K5 canonicalize (canon.cu).
 #include <algorithm>
+#include <cstdlib>
+#include <memory>
 #include <vector>
 
 #include "prims.cuh"
@@ -338,6 +340,12 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
   uint32_t epoch = 0;
   uint64_t seed = 0x5EED0001ull;
   std::vector<uint32_t> trace_buf;
+  struct LayFree {
+    void operator()(ShardLayout* s) const { shard_layout_free(s); }
+  };
+  std::unique_ptr<ShardLayout, LayFree> lay;
+  const char* le = getenv("DFM_RADIX_LAYOUT");  // 0: the gather kernel on every pass
+  bool lay_enabled = !(le && le[0] == '0');
 
   while (true) {
     if (dl.expired()) {
@@ -366,7 +374,16 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
         DFM_LAUNCH_CHECK();
       }
       SigParams sp{d.delta, n, k, block, act, m, w, seed, keysA, sig, mirror};
-      {
+      // ids wider than 4 bits (B > 16) over most states: the blocked builder of
+      // the hash engine (no random HBM gathers; built once, delta is pass-invariant)
+      if (mb >= 8 && m >= n / 4 && lay_enabled && !lay) {
+        lay.reset(radix_layout_build(ctx, d));
+        lay_enabled = lay != nullptr;
+      }
+      if (mb >= 8 && m >= n / 4 && lay) {
+        radix_layout_keys(ctx, lay.get(), mb, mb < 32 ? mirror : block, act, m, block, w,
+                          !packed, seed, reinterpret_cast<unsigned long long*>(keysA), sig, k + 1);
+      } else {
         // delta stream 4k + successor-block gather 4k + own block 4 + active id 4 + key 8
         // (+ signature row 4(k+1) when hashed) per active state
         ProfScope p(ctx, "sig",

@@ -1540,6 +1540,14 @@ void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* fu
               nullptr, nullptr, nullptr);
 }
 
+ShardLayout* radix_layout_build(Ctx& ctx, const DevDfa& d) { return shard_layout_build(ctx, d, d.n); }
+void radix_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* ids,
+                       const uint32_t* act, uint64_t m, const uint32_t* block, int w, bool hashed,
+                       uint64_t seed, unsigned long long* keys, uint32_t* sig, uint32_t row) {
+  layout_keys(ctx, s->L, id_bits, ids, act, m, block, w, hashed, seed, keys, sig, row, nullptr,
+              nullptr, nullptr);
+}
+
 AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_trace* trace) {
   AlgoOut out;
   const uint64_t n = d.n;
