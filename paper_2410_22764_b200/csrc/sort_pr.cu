@@ -121,8 +121,9 @@ struct HeadIn {
     if (j == 0) return 1u;
     if (keys[j] != keys[j - 1]) return 1u;
     if (sig != nullptr) {
-      const uint32_t* a = sig + (uint64_t)vals[j] * words;
-      const uint32_t* b = sig + (uint64_t)vals[j - 1] * words;
+      // (bit 31 of a value may carry the item's leader flag)
+      const uint32_t* a = sig + (uint64_t)(vals[j] & 0x7FFFFFFFu) * words;
+      const uint32_t* b = sig + (uint64_t)(vals[j - 1] & 0x7FFFFFFFu) * words;
       for (uint32_t i = 0; i < words; ++i) {
         if (a[i] != b[i]) {
           atomicOr(collision, 1ull);
@@ -245,6 +246,127 @@ __global__ void __launch_bounds__(256) unscatter_apply_kernel(uint64_t m,
   }
 }
 
+// ---- leader-flag relabel (n < 2^30, >= 2^20 active states).  Every block keeps a
+// leader flag on its minimum state (as the hash engine does).  The sort values carry
+// it in bit 31, so a run holds its old block's leader iff one of its items has the
+// bit: that run keeps the block's id (read from the leader's block entry — one
+// gather per old block) and every other run takes a fresh id.  No per-run atomics on
+// the old blocks' cells (1e8 singleton runs contending for 3e4 cells took 5.3 ms).
+// A fresh run's leader is its head (a stable sort of ascending active states puts
+// the minimum state first); a kept run's stays.  The new flags ride the sort back.
+__global__ void lead_min_kernel(const uint8_t* __restrict__ acc, uint64_t n,
+                                uint32_t* __restrict__ mins) {
+  uint32_t la = 0xFFFFFFFFu, lr = 0xFFFFFFFFu;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride) {
+    if (acc[q]) la = min(la, (uint32_t)q);
+    else lr = min(lr, (uint32_t)q);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    la = min(la, __shfl_xor_sync(0xffffffffu, la, o));
+    lr = min(lr, __shfl_xor_sync(0xffffffffu, lr, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (la != 0xFFFFFFFFu) atomicMin(&mins[0], la);
+    if (lr != 0xFFFFFFFFu) atomicMin(&mins[1], lr);
+  }
+}
+__global__ void lead_init_kernel(uint64_t n, const uint32_t* __restrict__ mins,
+                                 uint8_t* __restrict__ lead) {
+  const uint32_t a = mins[0], r = mins[1];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += stride)
+    lead[q] = (q == a || q == r) ? 1 : 0;
+}
+// the sort's input values: active index | leader flag << 31
+__global__ void lead_vals_kernel(uint64_t m, const uint32_t* __restrict__ act,
+                                 const uint8_t* __restrict__ lead, uint32_t* __restrict__ vals) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
+    vals[i] = (uint32_t)i | ((uint32_t)lead[act ? act[i] : (uint32_t)i] << 31);
+}
+// the run holding an old block's leader keeps the block's id
+__global__ void lead_keep_kernel(uint64_t m, const uint32_t* __restrict__ vals,
+                                 const uint32_t* __restrict__ act, const uint32_t* __restrict__ run_of,
+                                 const uint32_t* __restrict__ block, uint32_t* __restrict__ newid,
+                                 uint8_t* __restrict__ kept, const uint64_t* scalars) {
+  if (scalars[2] != 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint32_t v = vals[j];
+    if (!(v >> 31)) continue;
+    const uint32_t i = v & 0x7FFFFFFFu;
+    const uint32_t r = run_of[j];
+    newid[r] = block[act ? act[i] : i];
+    kept[r] = 1;
+  }
+}
+struct LeadFreshIn {
+  const uint8_t* kept;
+  const uint64_t* scalars;
+  __device__ uint32_t operator()(uint64_t r) const {
+    if (r >= scalars[0] || scalars[2] != 0) return 0u;
+    return kept[r] ? 0u : 1u;
+  }
+};
+struct LeadFreshOut {
+  uint32_t* newid;
+  const uint64_t* scalars;
+  uint32_t B;
+  __device__ void operator()(uint64_t r, uint32_t excl, uint32_t v) const {
+    if (r < scalars[0] && v) newid[r] = B + excl;
+  }
+};
+// pairs (active index, new id | run >= 2 << 31 | new leader << 30) for the sort back
+__global__ void __launch_bounds__(256) lead_pairs_kernel(
+    uint64_t m, const uint32_t* __restrict__ vals, const uint32_t* __restrict__ run_of,
+    const uint32_t* __restrict__ runstart, const uint32_t* __restrict__ newid,
+    const uint8_t* __restrict__ kept, uint64_t* __restrict__ pkeys, uint32_t* __restrict__ pvals,
+    const uint64_t* scalars) {
+  if (scalars[2] != 0) return;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
+    const uint32_t v = vals[j];
+    const uint32_t r = run_of[j];
+    const uint32_t s0 = runstart[r];
+    const uint32_t len = runstart[r + 1] - s0;
+    const uint32_t nl = kept[r] ? (v >> 31) : ((uint32_t)j == s0 ? 1u : 0u);
+    pkeys[j] = v & 0x7FFFFFFFu;
+    pvals[j] = newid[r] | (len >= 2 ? 0x80000000u : 0u) | (nl << 30);
+  }
+}
+// The pairs' keys are a permutation of 0..m-1: after a stable sort on bits [11, ..)
+// only, window x (positions [2048x, 2048x + 2048)) holds exactly the keys of that
+// range, so one CTA per window finishes the order in shared memory and applies the
+// values in active order (two digit passes fewer than a full sort at m <= 2^27).
+constexpr int kPlaceBits = 11;
+__global__ void __launch_bounds__(1024) lead_place_apply_kernel(
+    uint64_t m, const uint64_t* __restrict__ pkeys, const uint32_t* __restrict__ pvals,
+    const uint32_t* __restrict__ act, uint32_t* __restrict__ block, uint8_t* __restrict__ flag,
+    uint8_t* __restrict__ lead, const uint64_t* scalars) {
+  __shared__ uint32_t s_v[1u << kPlaceBits];
+  if (scalars[2] != 0) return;
+  const uint64_t nwin = (m + (1u << kPlaceBits) - 1) >> kPlaceBits;
+  for (uint64_t x = blockIdx.x; x < nwin; x += gridDim.x) {
+    const uint64_t b = x << kPlaceBits;
+    const uint64_t rem = m - b;
+    const uint32_t len = rem < (1u << kPlaceBits) ? (uint32_t)rem : (1u << kPlaceBits);
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x)
+      s_v[(uint32_t)(pkeys[b + t] - b)] = pvals[b + t];
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint32_t v = s_v[t];
+      const uint64_t i = b + t;
+      const uint32_t q = act ? act[i] : (uint32_t)i;
+      block[q] = v & 0x3FFFFFFFu;
+      flag[q] = (uint8_t)(v >> 31);
+      lead[q] = (uint8_t)((v >> 30) & 1u);
+    }
+    __syncthreads();
+  }
+}
+
 // DFM_RADIX_UNSCATTER=0: the plain scatter (A/B runs)
 bool unscatter_enabled() {
   const char* e = getenv("DFM_RADIX_UNSCATTER");
@@ -333,6 +455,22 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
     init_block_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, split, block);
     DFM_LAUNCH_CHECK();
   }
+  // leader flags (the minimum state of each block) for the leader-flag relabel; ids
+  // then travel in 30 bits
+  const bool lead_ok = n >= (1u << 20) && n < (1ull << 30);
+  uint8_t* lead = nullptr;
+  uint8_t* kept = nullptr;
+  if (lead_ok) {
+    lead = ctx.slot_t<uint8_t>("sp.lead", n);
+    kept = ctx.slot_t<uint8_t>("sp.kept", n);
+    uint32_t* mins = reinterpret_cast<uint32_t*>(sc + 6);
+    ProfScope p(ctx, "init", n * 2ull);
+    DFM_CUDA(cudaMemsetAsync(mins, 0xFF, 8, ctx.stream));
+    lead_min_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(d.acc, n, mins);
+    DFM_LAUNCH_CHECK();
+    lead_init_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(n, mins, lead);
+    DFM_LAUNCH_CHECK();
+  }
 
   const uint32_t* act = nullptr;  // identity: every state active at pass 1
   int act_sel = 0;
@@ -405,7 +543,15 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
 #undef DFM_SIG
         DFM_LAUNCH_CHECK();
       }
-      const bool alt = prims::radix_sort_pairs(ctx, keysA, valsA, keysB, valsB, m, bits, true);
+      // leader-flag relabel (see lead_keep_kernel) for large active sets
+      const bool lead_path = lead_ok && unscatter_enabled() && m >= (1u << 20);
+      if (lead_path) {
+        ProfScope p(ctx, "relabel", m * 9ull);  // active id 4 + flag 1 + value 4
+        lead_vals_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, act, lead, valsA);
+        DFM_LAUNCH_CHECK();
+      }
+      const bool alt =
+          prims::radix_sort_pairs(ctx, keysA, valsA, keysB, valsB, m, bits, !lead_path);
       const uint64_t* ks = alt ? keysB : keysA;
       const uint32_t* vs = alt ? valsB : valsA;
       {
@@ -415,6 +561,43 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
                                     reinterpret_cast<unsigned long long*>(sc + 2)},
                              HeadOut{run_of, runstart, m}, sc + 0);
       }
+      if (lead_path) {
+        // the sorted buffers are dead once the pairs are built: they are the sort's
+        // alternates
+        uint64_t* pk = alt ? keysA : keysB;
+        uint32_t* pv = alt ? valsA : valsB;
+        {
+          ProfScope p(ctx, "relabel", m * 5ull);  // value 4 + kept flag 1 (+ per old block)
+          DFM_CUDA(cudaMemsetAsync(kept, 0, m, ctx.stream));
+          lead_keep_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, vs, act, run_of, block,
+                                                                    newid, kept, sc);
+          DFM_LAUNCH_CHECK();
+        }
+        {
+          ProfScope p(ctx, "scan", m * 5ull);  // kept flag 1 + new id 4 per run
+          prims::lookback_scan(ctx, "sc.fresh", m, LeadFreshIn{kept, sc},
+                               LeadFreshOut{newid, sc, B}, sc + 1);
+        }
+        {
+          // value 4 + run_of 4 + runstart pair 8 + new id 4 + kept 1 + key 8 + value 4
+          ProfScope p(ctx, "relabel", m * 33ull);
+          lead_pairs_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, vs, run_of, runstart, newid,
+                                                                     kept, pk, pv, sc);
+          DFM_LAUNCH_CHECK();
+        }
+        // the sort back on the bits above the 2048-key windows, then the windows
+        const int hb = bit_width_u32((uint32_t)(m - 1));
+        const bool alt2 = prims::radix_sort_pairs_bits(ctx, pk, pv, const_cast<uint64_t*>(ks),
+                                                       const_cast<uint32_t*>(vs), m, kPlaceBits,
+                                                       hb - kPlaceBits, false);
+        // key 8 + value 4 + active id 4 + block 4 + flag 1 + lead 1
+        ProfScope p(ctx, "relabel", m * 22ull);
+        lead_place_apply_kernel<<<(unsigned)std::min<uint64_t>(
+                                      ceil_div(m, 1u << kPlaceBits), (uint64_t)ctx.num_sms * 2),
+                                  1024, 0, ctx.stream>>>(m, alt2 ? ks : pk, alt2 ? vs : pv, act,
+                                                         block, flag, lead, sc);
+        DFM_LAUNCH_CHECK();
+      } else {
       {
         ProfScope p(ctx, "relabel");
         keep_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(runstart, vs, act, block, runblock,
@@ -451,6 +634,7 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
         scatter_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(m, vs, act, run_of, runstart,
                                                                  newid, block, flag, sc);
         DFM_LAUNCH_CHECK();
+      }
       }
       {
         ProfScope p(ctx, "scan", m * 9ull);  // active id 4 + flag 1 + survivor id 4
