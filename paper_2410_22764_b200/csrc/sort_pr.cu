@@ -556,7 +556,7 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
       const uint32_t* vs = alt ? valsB : valsA;
       {
         ProfScope p(ctx, "scan", m * 16ull);  // key 8 + run_of 4 + runstart 4
-        prims::lookback_scan(ctx, "sc.heads", m,
+        prims::lookback_flags(ctx, "sc.heads", m,
                              HeadIn{ks, vs, packed ? nullptr : sig, k + 1,
                                     reinterpret_cast<unsigned long long*>(sc + 2)},
                              HeadOut{run_of, runstart, m}, sc + 0);
@@ -575,7 +575,7 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
         }
         {
           ProfScope p(ctx, "scan", m * 5ull);  // kept flag 1 + new id 4 per run
-          prims::lookback_scan(ctx, "sc.fresh", m, LeadFreshIn{kept, sc},
+          prims::lookback_flags(ctx, "sc.fresh", m, LeadFreshIn{kept, sc},
                                LeadFreshOut{newid, sc, B}, sc + 1);
         }
         {
@@ -606,7 +606,7 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
       }
       {
         ProfScope p(ctx, "scan");
-        prims::lookback_scan(ctx, "sc.fresh", m, FreshIn{runblock, runstart, cells, sc, epoch},
+        prims::lookback_flags(ctx, "sc.fresh", m, FreshIn{runblock, runstart, cells, sc, epoch},
                              FreshOut{runblock, newid, sc, B}, sc + 1);
       }
       if (unscatter_enabled() && n < (1ull << 31) && m >= (1u << 20)) {
@@ -638,7 +638,7 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
       }
       {
         ProfScope p(ctx, "scan", m * 9ull);  // active id 4 + flag 1 + survivor id 4
-        prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+        prims::lookback_flags(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
       }
     }
     DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars, sc, 4 * 8, cudaMemcpyDeviceToHost, ctx.stream));

@@ -1798,7 +1798,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           group_partitioned(ctx, m, act, keys, vals, packed ? nullptr : sig, k + 1, row, B, block,
                             flag, lead, sc);
           ProfScope p(ctx, "scan", m * 9ull);
-          prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+          prims::lookback_flags(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
           act_scanned = true;
         }
       }
@@ -1846,7 +1846,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
             filt_mark_kernel<<<grid_for(ctx, dups), 256, 0, ctx.stream>>>(
                 keys, dups, !packed, seed, F, slot_of, level, cin);
             DFM_LAUNCH_CHECK();
-            prims::lookback_scan(ctx, "sc.cand", dups, CandIn{cin, slot_of},
+            prims::lookback_flags(ctx, "sc.cand", dups, CandIn{cin, slot_of},
                                  CandOut{cin, cbuf[level]}, sc + 6);
           }
           DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 6, sc + 6, 8, cudaMemcpyDeviceToHost,
@@ -2027,7 +2027,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
     if (!act_scanned && m > 0 && ctx.h_scalars[8] != 0) {
       // some states became singletons: compact the active list (ascending q)
       ProfScope p(ctx, "scan", m * 9ull);
-      prims::lookback_scan(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
+      prims::lookback_flags(ctx, "sc.act", m, ActIn{act, flag}, ActOut{act, act_next}, sc + 3);
       DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 3, sc + 3, 8, cudaMemcpyDeviceToHost, ctx.stream));
       ctx.sync();
       act_scanned = true;
@@ -2049,7 +2049,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   } else {
     uint32_t* cob = ctx.slot_t<uint32_t>("sh.cob", std::max<uint64_t>(n, B));
     ProfScope p(ctx, "canon", n * 13ull);
-    prims::lookback_scan(ctx, "sc.canon", n, LeadIn{lead}, LeadOut{block, cob}, sc + 5);
+    prims::lookback_flags(ctx, "sc.canon", n, LeadIn{lead}, LeadOut{block, cob}, sc + 5);
     canon_gather_kernel<<<grid_for(ctx, n), 256, 0, ctx.stream>>>(block, n, cob, out.canon_dev);
     DFM_LAUNCH_CHECK();
     out.num_blocks = nb;  // one leader per block
