@@ -247,6 +247,8 @@ void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* fu
 // the same builder for the radix engine (sort_pr.cu) over the whole DFA: keys of the
 // m active states (ascending act, or all states) in active order
 ShardLayout* radix_layout_build(Ctx& ctx, const DevDfa& d);
+// DFM_SORTPR_WEAK_HASH (tests): truncated hashed keys under the first seed
+void sortpr_weak_hash_setup();
 void radix_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* ids,
                        const uint32_t* act, uint64_t m, const uint32_t* block, int w, bool hashed,
                        uint64_t seed, unsigned long long* keys, uint32_t* sig, uint32_t row);

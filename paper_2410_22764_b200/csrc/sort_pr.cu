@@ -83,6 +83,11 @@ __global__ void __launch_bounds__(256) riota_kernel(uint32_t* __restrict__ out, 
     out[q] = (uint32_t)q;
 }
 
+// first seed of every run; DFM_SORTPR_WEAK_HASH=<bits> (tests) truncates the hashed
+// keys under it so that distinct signatures collide and the void-and-retry path runs
+constexpr uint64_t kRadixSeed0 = 0x5EED0001ull;
+__device__ unsigned long long g_radix_weak_mask = ~0ull;
+
 // K1: signature gather + key build, one thread per active state.  delta rows
 // are read coalesced (active list is ascending in q); block[] is gathered.
 template <bool kHashed, int kBits>
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(256) sig_kernel(SigParams p) {
         row[a + 1] = s;
         h = mix64(h + kGolden + s);
       }
-      p.keys[i] = h;
+      p.keys[i] = p.seed == kRadixSeed0 ? (h & g_radix_weak_mask) : h;
     }
   }
 }
@@ -476,7 +481,18 @@ AlgoOut run_sort_pr(Ctx& ctx, const DevDfa& d, const Deadline& dl, const dfm_tra
   int act_sel = 0;
   uint64_t m = n;
   uint32_t epoch = 0;
-  uint64_t seed = 0x5EED0001ull;
+  uint64_t seed = kRadixSeed0;
+  {
+    sortpr_weak_hash_setup();  // (the blocked builder's keys)
+    static unsigned long long mask_set = ~0ull;
+    const char* e = getenv("DFM_SORTPR_WEAK_HASH");
+    const unsigned long long mask =
+        e ? ((1ull << std::min(63ul, strtoul(e, nullptr, 10))) - 1) : ~0ull;
+    if (mask != mask_set) {
+      DFM_CUDA(cudaMemcpyToSymbol(g_radix_weak_mask, &mask, sizeof(mask)));
+      mask_set = mask;
+    }
+  }
   std::vector<uint32_t> trace_buf;
   struct LayFree {
     void operator()(ShardLayout* s) const { shard_layout_free(s); }

@@ -1541,6 +1541,19 @@ void shard_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* fu
 }
 
 ShardLayout* radix_layout_build(Ctx& ctx, const DevDfa& d) { return shard_layout_build(ctx, d, d.n); }
+
+// DFM_SORTPR_WEAK_HASH=<bits> (tests): the hashed keys of passes under the first seed
+// (both engines' blocked builder) keep only that many bits
+void sortpr_weak_hash_setup() {
+  static unsigned long long mask_set = ~0ull;
+  const char* e = getenv("DFM_SORTPR_WEAK_HASH");
+  const unsigned long long mask =
+      e ? ((1ull << std::min(63ul, strtoul(e, nullptr, 10))) - 1) : ~0ull;
+  if (mask != mask_set) {
+    DFM_CUDA(cudaMemcpyToSymbol(g_weak_mask, &mask, sizeof(mask)));
+    mask_set = mask;
+  }
+}
 void radix_layout_keys(Ctx& ctx, ShardLayout* s, int id_bits, const uint32_t* ids,
                        const uint32_t* act, uint64_t m, const uint32_t* block, int w, bool hashed,
                        uint64_t seed, unsigned long long* keys, uint32_t* sig, uint32_t row) {
@@ -1670,16 +1683,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
   int act_sel = 0;
   uint64_t m = n;
   uint64_t seed = kSeed0;
-  {
-    static unsigned long long mask_set = ~0ull;
-    const char* e = getenv("DFM_SORTPR_WEAK_HASH");
-    const unsigned long long mask =
-        e ? ((1ull << std::min(63ul, strtoul(e, nullptr, 10))) - 1) : ~0ull;
-    if (mask != mask_set) {
-      DFM_CUDA(cudaMemcpyToSymbol(g_weak_mask, &mask, sizeof(mask)));
-      mask_set = mask;
-    }
-  }
+  sortpr_weak_hash_setup();
   std::vector<uint32_t> trace_buf;
   bool prog_pending = d.nready > 0;  // pipelined upload: rows still landing chunk by chunk
 

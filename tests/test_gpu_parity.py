@@ -436,11 +436,14 @@ def test_host_loop_relabel_in_place_vs_oracle(eng, monkeypatch):
             assert (x.partition.block == ref.block).all()
 
 
+@pytest.mark.parametrize("engine", ["hash", "radix"])
 @pytest.mark.parametrize("n,k,seed", [(200_000, 4, 3), (12_000_000, 4, 3)])
-def test_forced_hash_collisions_retry_exactly(eng, monkeypatch, n, k, seed):
+def test_forced_hash_collisions_retry_exactly(eng, eng_radix, monkeypatch, n, k, seed, engine):
     """DFM_SORTPR_WEAK_HASH truncates the first seed's hashed keys to 10 bits: every
     hashed pass collides, is voided and redone under the next seed (direct passes,
-    the filtered relabel-in-place pass included) — same result as without."""
+    the filtered relabel-in-place pass, the radix engine's gather and blocked-builder
+    keys and its leader-flag relabel included) — same result as without."""
+    eng = eng if engine == "hash" else eng_radix
     monkeypatch.setenv("DFM_SORTPR_SMALL", "0")
     dd = eng.random_dfa_device(n, k, seed, 0.5)
     nb, it, lab = _device_labels(eng, dd, n)
