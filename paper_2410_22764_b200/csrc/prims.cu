@@ -37,11 +37,31 @@ __global__ void radix_bucket_scan_kernel(const uint32_t* __restrict__ hist,
 #ifndef DFM_RS_BALLOT_RANK  // digit peers from 9 ballots (1) or match.any (0): sort 28.4 -> 26.7 ms
 #define DFM_RS_BALLOT_RANK 1
 #endif
-template <bool kIdentVals>
+// per-(tile, digit) look-back words: 64-bit, or 32-bit (flags in bits 31:30) while the
+// item count stays below 2^30 — half the status traffic and memset
+template <class S>
+struct LbStatus;
+template <>
+struct LbStatus<uint64_t> {
+  static constexpr uint64_t kAgg = kFlagAgg, kInc = kFlagInc, kVal = kValMask;
+  __device__ static uint64_t ld(const uint64_t* p) { return ld_volatile(p); }
+  __device__ static void st(uint64_t* p, uint64_t v) { st_volatile(p, v); }
+};
+template <>
+struct LbStatus<uint32_t> {
+  static constexpr uint32_t kAgg = 1u << 30, kInc = 2u << 30, kVal = (1u << 30) - 1;
+  __device__ static uint32_t ld(const uint32_t* p) { return ld_relaxed_u32(p); }
+  __device__ static void st(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  }
+};
+
+template <bool kIdentVals, class S>
 __global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
     const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t count, int shift,
-    const uint32_t* __restrict__ bucket_base, uint64_t* status, uint32_t* ticket) {
+    const uint32_t* __restrict__ bucket_base, S* status, uint32_t* ticket) {
+  using St = LbStatus<S>;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* s_keys = reinterpret_cast<uint64_t*>(smem);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kRsTile);
@@ -80,8 +100,8 @@ __global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
     if (dig[j] < 256) atomicAdd(&s_hist[dig[j]], 1u);
   __syncthreads();
   if (tid < 256) {
-    if (tile == 0) st_volatile(status + tid, kFlagInc | s_hist[tid]);
-    else st_volatile(status + (uint64_t)tile * 256 + tid, kFlagAgg | s_hist[tid]);
+    if (tile == 0) St::st(status + tid, St::kInc | (S)s_hist[tid]);
+    else St::st(status + (uint64_t)tile * 256 + tid, St::kAgg | (S)s_hist[tid]);
   }
   uint32_t* my_cnt = s_cnt + warp * 256;
 #pragma unroll
@@ -134,20 +154,20 @@ __global__ void __launch_bounds__(kRsThreads, kRsBlocksPerSm) onesweep_kernel(
       int64_t t = (int64_t)tile - 1;
       bool done = false;
       while (!done) {
-        uint64_t s[kLb];
+        S s[kLb];
 #pragma unroll
         for (int u = 0; u < kLb; ++u)
-          s[u] = t - u >= 0 ? ld_volatile(status + (uint64_t)(t - u) * 256 + d) : kFlagInc;
+          s[u] = t - u >= 0 ? St::ld(status + (uint64_t)(t - u) * 256 + d) : St::kInc;
 #pragma unroll
         for (int u = 0; u < kLb; ++u) {
           if (done) break;
-          while ((s[u] & ~kValMask) == 0) s[u] = ld_volatile(status + (uint64_t)(t - u) * 256 + d);
-          prefix += s[u] & kValMask;
-          done = (s[u] & kFlagInc) != 0;
+          while ((s[u] & ~St::kVal) == 0) s[u] = St::ld(status + (uint64_t)(t - u) * 256 + d);
+          prefix += s[u] & St::kVal;
+          done = (s[u] & St::kInc) != 0;
         }
         t -= kLb;
       }
-      st_volatile(status + (uint64_t)tile * 256 + d, kFlagInc | (prefix + total));
+      St::st(status + (uint64_t)tile * 256 + d, St::kInc | (S)(prefix + total));
     }
     s_glob[d] = bucket_base[d] + (uint32_t)prefix;
   }
@@ -187,10 +207,14 @@ bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* a
   if (count >= (1ull << 32)) throw Error(DFM_ERR_INVALID, "radix_sort_pairs: count >= 2^32");
   int dev = 0;
   DFM_CUDA(cudaGetDevice(&dev));
-  per_device_memo((const void*)onesweep_kernel<true>, dev, [](const void*) {
-    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<true>,
+  per_device_memo((const void*)onesweep_kernel<true, uint64_t>, dev, [](const void*) {
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<true, uint64_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
-    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<false>,
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<false, uint64_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<true, uint32_t>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
+    DFM_CUDA(cudaFuncSetAttribute(onesweep_kernel<false, uint32_t>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
     return 1;
   });
@@ -199,7 +223,9 @@ bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* a
   uint32_t* hist = ctx.slot_t<uint32_t>("rs.hist", 2 * 8 * 256 + 16);
   uint32_t* base = hist + 8 * 256;
   uint32_t* tickets = base + 8 * 256;
-  uint64_t* status = ctx.slot_t<uint64_t>("rs.status", tiles * 256);
+  const bool narrow = count < (1ull << 30);  // 32-bit look-back words
+  const size_t sbytes = tiles * 256 * (narrow ? 4 : 8);
+  void* status = ctx.slot("rs.status", sbytes);
   DFM_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (2 * 8 * 256 + 16), ctx.stream));
   {
     ProfScope p(ctx, "sort", count * 8ull);  // one read of the keys for all digit histograms
@@ -215,17 +241,28 @@ bool radix_sort_pairs_bits(Ctx& ctx, uint64_t* keys, uint32_t* vals, uint64_t* a
   uint64_t* kout = alt_keys;
   uint32_t* vout = alt_vals;
   for (int p = 0; p < passes; ++p) {
-    DFM_CUDA(cudaMemsetAsync(status, 0, tiles * 256 * 8, ctx.stream));
+    DFM_CUDA(cudaMemsetAsync(status, 0, sbytes, ctx.stream));
     {
       ProfScope ps(ctx, "sort", count * 24ull);  // (key 8 + value 4) read + written
-      if (p == 0 && ident_vals)
-        onesweep_kernel<true><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
-            kin, nullptr, kout, vout, (uint32_t)count, lo_bit + 8 * p, base + p * 256, status,
-            tickets + p);
-      else
-        onesweep_kernel<false><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
-            kin, vin, kout, vout, (uint32_t)count, lo_bit + 8 * p, base + p * 256, status,
-            tickets + p);
+      const bool iv = p == 0 && ident_vals;
+      const int sh = lo_bit + 8 * p;
+      if (narrow) {
+        auto* st = static_cast<uint32_t*>(status);
+        if (iv)
+          onesweep_kernel<true, uint32_t><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+              kin, nullptr, kout, vout, (uint32_t)count, sh, base + p * 256, st, tickets + p);
+        else
+          onesweep_kernel<false, uint32_t><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+              kin, vin, kout, vout, (uint32_t)count, sh, base + p * 256, st, tickets + p);
+      } else {
+        auto* st = static_cast<uint64_t*>(status);
+        if (iv)
+          onesweep_kernel<true, uint64_t><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+              kin, nullptr, kout, vout, (uint32_t)count, sh, base + p * 256, st, tickets + p);
+        else
+          onesweep_kernel<false, uint64_t><<<(unsigned)tiles, kRsThreads, kRsSmem, ctx.stream>>>(
+              kin, vin, kout, vout, (uint32_t)count, sh, base + p * 256, st, tickets + p);
+      }
       DFM_LAUNCH_CHECK();
     }
     std::swap(kin, kout);
