@@ -186,6 +186,7 @@ class ShardedResult:
     num_blocks: int
     iterations: int
     retries: int
+    converged: bool = True  # False: stopped at max_passes before the fixpoint
 
 
 def shard_bounds(n_total: int, world: int, rank: int):
@@ -213,6 +214,7 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
     B = 2 if split else 1
     seed = 0x5EED0001
     iterations = retries = 0
+    converged = False
     while True:
         if max_passes is not None and iterations >= max_passes:
             break
@@ -249,16 +251,18 @@ def sharded_sort_pr(delta_local: torch.Tensor, acc_local: torch.Tensor, n_total:
         iterations += 1
         block = new_block
         if B_new == B:  # fixpoint, min_sort.hpp:111-117
+            converged = True
             break
         B = B_new
         if B == n_total:
             # every block is a singleton: the next pass sees n distinct keys (each holds
             # its own block id), grows nothing and ends the loop — count it, skip it
             iterations += 1
+            converged = True
             break
     block_full = comm.all_gather(block, sizes)
     canon, nb = ops.canonicalize(block_full)
-    return ShardedResult(canon[lo:lo + n_local].clone(), nb, iterations, retries)
+    return ShardedResult(canon[lo:lo + n_local].clone(), nb, iterations, retries, converged)
 
 
 class ShardedEngine:

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cases, weak, q):
+def _worker(rank, world, port, cases, weak, q, max_passes=None):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from paper_2410_22764_b200.sharded import Comm, shard_bounds, sharded_sort_pr
@@ -37,17 +37,19 @@ def _worker(rank, world, port, cases, weak, q):
         # of the early passes cannot collide)
         r = sharded_sort_pr(torch.from_numpy(delta[:, lo:hi].astype(np.int32)),
                             torch.from_numpy(acc[lo:hi]), n, lo, Comm(), CpuShardOps(weak),
-                            allow_packed=not weak)
-        out.append((lo, r.block_local.numpy().copy(), r.num_blocks, r.iterations, r.retries))
+                            max_passes=max_passes, allow_packed=not weak)
+        out.append((lo, r.block_local.numpy().copy(), r.num_blocks, r.iterations, r.retries,
+                    r.converged))
     q.put((rank, out))
     dist.destroy_process_group()
 
 
-def _run(world, cases, weak=False):
+def _run(world, cases, weak=False, max_passes=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, weak, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cases, weak, q, max_passes))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in range(world))
@@ -70,9 +72,10 @@ def test_sharded_matches_oracle(world):
         ref = O.sort_pr(delta, acc)
         full = np.empty(acc.size, np.int64)
         for r in range(world):
-            lo, blk, nb, it, _ = res[r][ci]
+            lo, blk, nb, it, _, conv = res[r][ci]
             full[lo:lo + blk.size] = blk
             assert (nb, it) == (ref.num_blocks, ref.iterations), (ci, r)
+            assert conv, (ci, r)
         assert (full == ref.block).all(), ci
 
 
@@ -83,7 +86,17 @@ def test_sharded_collision_retry_is_exact():
         ref = O.sort_pr(delta, acc)
         full = np.empty(acc.size, np.int64)
         for r in range(2):
-            lo, blk, nb, it, retries = res[r][ci]
+            lo, blk, nb, it, retries, _ = res[r][ci]
             full[lo:lo + blk.size] = blk
             assert it == ref.iterations and retries >= 1
         assert (full == ref.block).all()
+
+
+def test_sharded_max_passes_reports_not_converged():
+    """A run cut at max_passes before the fixpoint says so (ShardedResult.converged)."""
+    delta, acc = O.fib_dfa(9)
+    assert O.sort_pr(delta, acc).iterations > 2
+    res = _run(2, [(delta, acc)], max_passes=2)
+    for r in range(2):
+        _, _, _, it, _, conv = res[r][0]
+        assert it == 2 and not conv
