@@ -439,6 +439,99 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
 }
 
 // ---------------------------------------------------------------------------
+// Lane groups for large alphabets: kG lanes per state, each comparing the letters
+// a = g, g + kG, ... (kPer of them per round, all loads of a round in flight), so a
+// stable state costs one round of two dependent gathers instead of k/4 rounds
+// (min_partref.hpp:93-97's early exit only helps the states that split).  The
+// group's first lane writes the label, elects and marks as fused_pr_kernel does;
+// same per-pass semantics and pass count.
+template <int kPolicy, int kG>
+__global__ void __launch_bounds__(kPersistThreads) fused_group_kernel(FusedArgs a) {
+  constexpr int kPer = 4;
+  cg::grid_group g = cg::this_grid();
+  const uint32_t lane = threadIdx.x & 31, sub = lane % kG;
+  const uint32_t gmask = ((1u << kG) - 1u) << (lane - sub);  // (kG < 32)
+  const uint64_t spw = 32 / kG;  // states per warp step
+  const uint64_t warp_id = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  int sel = a.start_sel;
+  uint32_t p = 0;
+  bool stable = false;
+  while (p < a.max_passes) {
+    const uint32_t pass = a.pass0 + p + 1;
+    const uint32_t* Lm = sel ? a.lab1 : a.lab0;
+    uint32_t* Lw = sel ? a.lab0 : a.lab1;
+    const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
+    unsigned long long* ccur = (pass & 1) ? a.cells1 : a.cells0;
+    const uint32_t prev_changed = p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
+    bool any = false;
+    for (uint64_t qb = warp_id * spw; qb < a.n; qb += nwarps * spw) {
+      const uint64_t qi = qb + lane / kG;
+      const bool valid = qi < a.n;
+      const uint32_t q = (uint32_t)qi;
+      uint32_t lw = 0, leader = 0;
+      bool eval = false;
+      if (valid) {
+        lw = Lm[q];
+        leader = label_on_the_fly(lw, cprev);
+        eval = q != leader;
+        if (eval && a.mark != nullptr && pass > a.dirty_from && !(lw & kSplitBit))
+          eval = a.mark[q] >= pass || a.mark[leader] >= pass;
+      }
+      bool spl = false;
+      if (eval) {
+        for (uint64_t a0 = sub; a0 < a.letters && !spl; a0 += (uint64_t)kG * kPer) {
+          uint32_t tq[kPer], tl[kPer], lq[kPer], ll[kPer];
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const uint64_t aa = a0 + (uint64_t)u * kG;
+            if (aa < a.letters) {
+              tq[u] = a.rows[aa * a.n + q];
+              tl[u] = a.rows[aa * a.n + leader];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kPer; ++u)
+            if (a0 + (uint64_t)u * kG < a.letters) {
+              lq[u] = Lm[tq[u]];
+              ll[u] = Lm[tl[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < kPer; ++u)
+            if (a0 + (uint64_t)u * kG < a.letters)
+              spl |= label_on_the_fly(lq[u], cprev) != label_on_the_fly(ll[u], cprev);
+        }
+      }
+      const bool sp = (__ballot_sync(0xffffffffu, spl) & gmask) != 0;
+      const bool head = valid && sub == 0;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, head);
+      if (head) {
+        Lw[q] = leader | (sp ? kSplitBit : 0u);
+        any |= sp;
+        elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
+      }
+      if (sp && valid && a.mark != nullptr)  // the group marks q's predecessors
+        for (uint32_t e = a.pred_off[q] + sub, e1 = a.pred_off[q + 1]; e < e1; e += kG)
+          a.mark[a.pred_src[e]] = pass + 1;
+    }
+    if (prev_changed == 0u) {  // pass p was stable: this pass rewrote the same labels
+      stable = true;
+      break;
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) a.changed[p] = 1u;
+    g.sync();
+    sel ^= 1;
+    ++p;
+  }
+  if (!stable && p > 0 && prims::ld_relaxed_u32(&a.changed[p - 1]) == 0u) stable = true;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.out[0] = p;
+    a.out[1] = stable ? 1u : 0u;
+    a.out[2] = (uint32_t)sel;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Cluster variant for tiny inputs (rings and chains of a few thousand states run
 // n-1 passes): the whole working set — successor rows, both label buffers,
 // election cells, split flags — lives in the (distributed) shared memory of a
@@ -696,6 +789,16 @@ uint64_t fused_max_states(const Ctx& ctx, const void* kern) {
   return (uint64_t)per_sm * ctx.num_sms * kPersistThreads;
 }
 
+// DFM_NAIVE_GROUP (opt-in): 1 = lane groups for >= 8 letters when the thread-per-
+// state variant does not hold all states, 2 = always (tests).  Off by default:
+// measured on vlts(1000, 1e6, 20) (602 passes) 49.3 ms -> 114.5 ms — with the
+// work-efficient marks most states only run the skip test, which the groups
+// replicate kG times (`profiles/r03q`)
+int group_mode() {
+  const char* e = getenv("DFM_NAIVE_GROUP");
+  return e == nullptr ? 0 : (int)strtol(e, nullptr, 10);
+}
+
 bool fused_enabled() {
   const char* e = getenv("DFM_NAIVE_FUSED");
   return e == nullptr || e[0] != '0';
@@ -815,13 +918,22 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
                                    : fused_pr_kernel<DFM_POLICY_ARBITRARY, true>;
     // a thread per state when the kOne variant holds all n resident
     const bool one = n <= fused_max_states(ctx, (const void*)kern_one);
+    const int gm = group_mode();
+    const int lanes = (letters >= 8 && ((gm == 1 && !one) || gm == 2)) ? (letters >= 16 ? 8 : 4) : 1;
     void (*kern)(FusedArgs) =
-        one ? kern_one
+        lanes == 8 ? (policy == DFM_POLICY_MIN   ? fused_group_kernel<DFM_POLICY_MIN, 8>
+                      : policy == DFM_POLICY_MAX ? fused_group_kernel<DFM_POLICY_MAX, 8>
+                                                 : fused_group_kernel<DFM_POLICY_ARBITRARY, 8>)
+        : lanes == 4 ? (policy == DFM_POLICY_MIN   ? fused_group_kernel<DFM_POLICY_MIN, 4>
+                        : policy == DFM_POLICY_MAX ? fused_group_kernel<DFM_POLICY_MAX, 4>
+                                                   : fused_group_kernel<DFM_POLICY_ARBITRARY, 4>)
+        : one ? kern_one
         : policy == DFM_POLICY_MIN ? fused_pr_kernel<DFM_POLICY_MIN, false>
         : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, false>
                                    : fused_pr_kernel<DFM_POLICY_ARBITRARY, false>;
-    const unsigned pgrid = (unsigned)std::min<uint64_t>(
-        ceil_div(n, kPersistThreads), fused_max_states(ctx, (const void*)kern) / kPersistThreads);
+    const unsigned pgrid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>(ceil_div(n * lanes, kPersistThreads),
+                              fused_max_states(ctx, (const void*)kern) / kPersistThreads));
     const uint32_t *pred_off = nullptr, *pred_src = nullptr;
     uint32_t* mark = nullptr;
     uint32_t dirty_from = 0;

@@ -511,3 +511,28 @@ def test_naive_work_efficient_passes(eng, monkeypatch, name, pair):
     assert rt.stats.iterations == ref_t.iterations and (rt.partition.block == ref_t.block).all()
     assert (eng.naive_pr(d, dfm.PrOptions(policy=ARB)).partition.block ==
             O.naive_pr(delta, acc, "min").block).all()
+
+
+@pytest.mark.parametrize("name,pair", [
+    ("vlts_k12", lambda: O.vlts_dfa(300, 60_000, 12)),
+    ("vlts_k20", lambda: O.vlts_dfa(200, 40_000, 20)),
+    ("random_k9", lambda: O.random_dfa(20_000, 9, 77, 0.5)),
+    ("random_k33", lambda: O.random_dfa(5_000, 33, 5, 0.5)),
+])
+def test_naive_lane_groups(eng, monkeypatch, name, pair):
+    """4 or 8 lanes per state (fused_group_kernel, forced with DFM_NAIVE_GROUP=2 on
+    inputs the thread-per-state kernel would take): the reference's partition and pass
+    count under min / max, with and without the work-efficient marks; transPR too."""
+    delta, acc = pair()
+    d = to_dfa((delta, acc))
+    monkeypatch.setenv("DFM_NAIVE_GROUP", "2")
+    for pol, name_ in ((MIN, "min"), (MAX, "max")):
+        ref = O.naive_pr(delta, acc, name_)
+        for flag in ("1", "0"):
+            monkeypatch.setenv("DFM_NAIVE_DIRTY", flag)
+            r = eng.naive_pr(d, dfm.PrOptions(policy=pol))
+            assert r.stats.iterations == ref.iterations, (name, name_, flag)
+            assert (r.partition.block == ref.block).all(), (name, name_, flag)
+    rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+    ref_t = O.trans_pr(delta, acc, "min")
+    assert rt.stats.iterations == ref_t.iterations and (rt.partition.block == ref_t.block).all()
