@@ -333,7 +333,14 @@ struct FusedArgs {
   uint32_t* mark;
   uint32_t dirty_from;  // first pass that writes marks (it evaluates every state)
   bool own_label;       // kOne: keep the state's own label word in a register
+  // letter masks (the kMask kernels; <= 32 letters, n < 2^21): `mark` is then three
+  // arrays of n, pass P reads mask[P % 3] — the letters whose successor changed in
+  // P-1 — writes mask[(P+1) % 3] and clears mask[(P+2) % 3].  A state evaluated only
+  // through the marks compares just the letters in mask[q] | mask[leader(q)]: every
+  // other letter compares two labels unchanged since an evaluation that found them
+  // equal.  pred_src then packs (source | letter << 21).
 };
+constexpr uint32_t kPredSrcBits = 21;
 
 // label words carry the previous pass's split flag in bit 31 (state ids < 2^31), so
 // one gather yields both the label and whether it must be corrected
@@ -342,7 +349,10 @@ __device__ __forceinline__ uint32_t label_on_the_fly(uint32_t w, const unsigned 
   return (w & kSplitBit) ? (uint32_t)cprev[w & ~kSplitBit] : w;
 }
 
-template <int kPolicy, bool kOne>
+// kMask: the letter-mask variant (launched once the masks exist; the plain variants
+// keep their code: the extra paths doubled the latency-bound C1 kernel's SASS and
+// slowed it 43 %)
+template <int kPolicy, bool kOne, bool kMask = false>
 __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) {
   cg::grid_group g = cg::this_grid();
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -382,15 +392,53 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       const uint32_t leader = label_on_the_fly(lw, cprev);
       bool sp = false;
       bool eval = q != leader;
-      if (eval && a.mark != nullptr && pass > a.dirty_from && !(lw & kSplitBit))
-        eval = a.mark[q] >= pass || a.mark[leader] >= pass;
-      if (one && leader != cl && eval) {
+      uint32_t lm = 0xFFFFFFFFu;  // letters to compare
+      if (eval && a.mark != nullptr && pass > a.dirty_from && !(lw & kSplitBit)) {
+        if constexpr (kMask) {
+          const uint32_t* mc = a.mark + (uint64_t)(pass % 3) * a.n;
+          lm = mc[q] | mc[leader];
+          eval = lm != 0;
+        } else {
+          eval = a.mark[q] >= pass || a.mark[leader] >= pass;
+        }
+      }
+      if constexpr (kMask)  // (read in pass - 1, written in pass + 1)
+        if (pass >= a.dirty_from) a.mark[(uint64_t)((pass + 2) % 3) * a.n + q] = 0;
+      if (one && leader != cl && eval && (!kMask || lm == 0xFFFFFFFFu)) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if ((uint64_t)u < a.letters) crow[u] = a.rows[(uint64_t)u * a.n + leader];
         cl = leader;
       }
-      if (eval) {
+      if (kMask && eval && lm != 0xFFFFFFFFu) {  // only the letters whose successors changed
+        uint32_t rem = lm;
+        while (rem != 0u && !sp) {
+          uint32_t al[4], tq[4], tl[4], lq[4], ll[4];
+          int c = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (rem != 0u) {
+              al[u] = (uint32_t)__ffs(rem) - 1u;
+              rem &= rem - 1u;
+              c = u + 1;
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < c) {
+              tq[u] = a.rows[(uint64_t)al[u] * a.n + q];
+              tl[u] = a.rows[(uint64_t)al[u] * a.n + leader];
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < c) {
+              lq[u] = Lm[tq[u]];
+              ll[u] = Lm[tl[u]];
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < c) sp |= label_on_the_fly(lq[u], cprev) != label_on_the_fly(ll[u], cprev);
+        }
+      } else if (eval) {
         for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
           uint32_t tq[4], tl[4], lq[4], ll[4];
 #pragma unroll
@@ -415,10 +463,19 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       if (one) myw = leader | (sp ? kSplitBit : 0u);
       any |= sp;
       elect_cell<kPolicy>(ccur, leader, q, pass, sp, vmask);
-      if (sp && a.mark != nullptr)  // q's label changes: its predecessors re-evaluate
+      if (sp && a.mark != nullptr) {  // q's label changes: its predecessors re-evaluate
         // (pass >= dirty_from always holds here: marks exist only from that launch on)
-        for (uint32_t e = a.pred_off[q], e1 = a.pred_off[q + 1]; e < e1; ++e)
-          a.mark[a.pred_src[e]] = pass + 1;
+        if constexpr (kMask) {
+          uint32_t* mn = a.mark + (uint64_t)((pass + 1) % 3) * a.n;
+          for (uint32_t e = a.pred_off[q], e1 = a.pred_off[q + 1]; e < e1; ++e) {
+            const uint32_t ps = a.pred_src[e];
+            atomicOr(&mn[ps & ((1u << kPredSrcBits) - 1u)], 1u << (ps >> kPredSrcBits));
+          }
+        } else {
+          for (uint32_t e = a.pred_off[q], e1 = a.pred_off[q + 1]; e < e1; ++e)
+            a.mark[a.pred_src[e]] = pass + 1;
+        }
+      }
     }
     if (prev_changed == 0u) {  // pass p was stable: this pass rewrote the same labels
       stable = true;
@@ -749,10 +806,14 @@ __global__ void pred_count_kernel(const uint32_t* __restrict__ rows, uint64_t n,
     atomicAdd(&deg[rows[j]], 1u);
 }
 __global__ void pred_fill_kernel(const uint32_t* __restrict__ rows, uint64_t n, uint64_t letters,
-                                 uint32_t* __restrict__ cursor, uint32_t* __restrict__ src) {
+                                 uint32_t* __restrict__ cursor, uint32_t* __restrict__ src,
+                                 bool with_letter) {
   const uint64_t total = n * letters, stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride)
-    src[atomicAdd(&cursor[rows[j]], 1u)] = (uint32_t)(j % n);
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += stride) {
+    const uint32_t s = (uint32_t)(j % n);
+    src[atomicAdd(&cursor[rows[j]], 1u)] =
+        with_letter ? s | (uint32_t)(j / n) << kPredSrcBits : s;
+  }
 }
 struct DegIn {
   const uint32_t* deg;
@@ -797,6 +858,12 @@ uint64_t fused_max_states(const Ctx& ctx, const void* kern) {
 int group_mode() {
   const char* e = getenv("DFM_NAIVE_GROUP");
   return e == nullptr ? 0 : (int)strtol(e, nullptr, 10);
+}
+
+// DFM_NAIVE_LMASK=0: work-efficient passes re-compare every letter of a marked state
+bool lmask_enabled() {
+  const char* e = getenv("DFM_NAIVE_LMASK");
+  return e == nullptr || e[0] != '0';
 }
 
 bool fused_enabled() {
@@ -937,6 +1004,8 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
     const uint32_t *pred_off = nullptr, *pred_src = nullptr;
     uint32_t* mark = nullptr;
     uint32_t dirty_from = 0;
+    const bool use_lmask = lanes == 1 && letters <= 32 && n < (1ull << kPredSrcBits) &&
+                           lmask_enabled();
     // the predecessor lists pay off only over many passes: built once a run has gone
     // 64 passes without converging (transPR's few-pass runs never build them)
     auto build_dirty = [&]() {
@@ -953,7 +1022,11 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
       pred_count_kernel<<<g2, 256, 0, ctx.stream>>>(rows, n, letters, deg);
       DFM_LAUNCH_CHECK();
       prims::lookback_scan(ctx, "pr.degscan", n + 1, DegIn{deg}, DegOut{off, cur}, nullptr);
-      pred_fill_kernel<<<g2, 256, 0, ctx.stream>>>(rows, n, letters, cur, src);
+      if (use_lmask) {  // the marks become three letter-mask arrays
+        mark = ctx.slot_t<uint32_t>("pr.lmask", 3 * n);
+        DFM_CUDA(cudaMemsetAsync(mark, 0, 3 * n * 4, ctx.stream));
+      }
+      pred_fill_kernel<<<g2, 256, 0, ctx.stream>>>(rows, n, letters, cur, src, use_lmask);
       DFM_LAUNCH_CHECK();
       pred_off = off;
       pred_src = src;
@@ -971,9 +1044,26 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
                    own_label_on()};
       chunk = std::min(kChunkMax, chunk * 2);
       void* args[] = {&fa};
+      // once the letter masks exist: the kMask variant (its own occupancy and kOne test)
+      const void* lk = (const void*)kern;
+      unsigned lgrid = pgrid;
+      if (mark != nullptr && use_lmask) {
+        void (*mk_one)(FusedArgs) =
+            policy == DFM_POLICY_MIN   ? fused_pr_kernel<DFM_POLICY_MIN, true, true>
+            : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, true, true>
+                                       : fused_pr_kernel<DFM_POLICY_ARBITRARY, true, true>;
+        void (*mk)(FusedArgs) =
+            (one && n <= fused_max_states(ctx, (const void*)mk_one)) ? mk_one
+            : policy == DFM_POLICY_MIN ? fused_pr_kernel<DFM_POLICY_MIN, false, true>
+            : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, false, true>
+                                       : fused_pr_kernel<DFM_POLICY_ARBITRARY, false, true>;
+        lk = (const void*)mk;
+        lgrid = (unsigned)std::max<uint64_t>(
+            1, std::min<uint64_t>(ceil_div(n, kPersistThreads),
+                                  fused_max_states(ctx, lk) / kPersistThreads));
+      }
       ProfScope prof(ctx, "elect", 0);
-      DFM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, pgrid, kPersistThreads, args, 0,
-                                           ctx.stream));
+      DFM_CUDA(cudaLaunchCooperativeKernel(lk, lgrid, kPersistThreads, args, 0, ctx.stream));
       DFM_LAUNCH_CHECK();
       prof.stop();
       DFM_CUDA(cudaMemcpyAsync(ctx.h_scalars + 20, pout, 12, cudaMemcpyDeviceToHost, ctx.stream));
