@@ -860,6 +860,12 @@ int group_mode() {
   return e == nullptr ? 0 : (int)strtol(e, nullptr, 10);
 }
 
+// passes before the predecessor lists are built (DFM_NAIVE_DIRTY_AFTER, default 64)
+uint32_t dirty_after() {
+  const char* e = getenv("DFM_NAIVE_DIRTY_AFTER");
+  return e ? (uint32_t)strtoul(e, nullptr, 10) : 64u;
+}
+
 // DFM_NAIVE_LMASK=0: work-efficient passes re-compare every letter of a marked state
 bool lmask_enabled() {
   const char* e = getenv("DFM_NAIVE_LMASK");
@@ -1037,7 +1043,7 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
         out.status = DFM_STATUS_TIMEOUT;
         return out;
       }
-      if (mark == nullptr && pass >= 64 && dirty_enabled(n, letters)) build_dirty();
+      if (mark == nullptr && pass >= dirty_after() && dirty_enabled(n, letters)) build_dirty();
       DFM_CUDA(cudaMemsetAsync(chg, 0, chunk * 4, ctx.stream));
       FusedArgs fa{rows, n,     letters, lab[0], lab[1], cells,    cells1,   chg,
                    pass, chunk, sel,     pout,   pred_off, pred_src, mark,   dirty_from,
