@@ -25,6 +25,7 @@
 // back to a CPU path.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -32,8 +33,13 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
+
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
 
 #include "dfm.h"
 
@@ -212,6 +218,39 @@ struct View {
   }
 };
 
+// The partition vector a MinResult returns (core.hpp: Partition::block).  A value-
+// initialised std::vector of 1e8 labels page-faults 400 MB of fresh mmap'd memory on
+// one thread (~200 ms, more than the whole GPU minimization); for large partitions the
+// pages are advised as huge pages and faulted in by several threads first, so
+// resize() only runs its memset over resident memory (measured ~50 ms at 1e8).
+inline std::vector<std::uint32_t> partition_buffer(std::size_t n) {
+  std::vector<std::uint32_t> v;
+  constexpr std::size_t kParallelBytes = std::size_t(64) << 20;
+  if (n * sizeof(std::uint32_t) >= kParallelBytes) {
+    v.reserve(n);
+    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(v.data());
+    const std::uintptr_t e = b + n * sizeof(std::uint32_t);
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+    const std::uintptr_t kHuge = std::uintptr_t(2) << 20;
+    const std::uintptr_t hb = (b + kHuge - 1) & ~(kHuge - 1), he = e & ~(kHuge - 1);
+    if (he > hb) madvise(reinterpret_cast<void*>(hb), he - hb, MADV_HUGEPAGE);
+#endif
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    auto touch = [b, e, T](unsigned t) {
+      const std::uintptr_t span = e - b;
+      std::uintptr_t lo = b + (span * t / T + 4095) / 4096 * 4096;
+      const std::uintptr_t hi = b + span * (t + 1) / T;
+      for (; lo < hi; lo += 4096) *reinterpret_cast<volatile char*>(lo) = 0;
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(touch, t);
+    touch(0);
+    for (auto& x : th) x.join();
+  }
+  v.resize(n);
+  return v;
+}
+
 inline MinResult result(std::vector<std::uint32_t>&& block, std::uint32_t nb, const dfm_stats& s) {
   MinResult r;
   r.stats.iterations = s.iterations;
@@ -253,7 +292,7 @@ inline void on_pr_pass(void* user, std::uint64_t, const std::uint32_t* raw, std:
 inline MinResult sort_pr(const Dfa& d, const SortOptions& opt = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block(d.num_states);
+  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_sort_pass, opt.trace};
@@ -271,7 +310,7 @@ inline MinResult sort_pr(const Dfa& d, std::int64_t timeout_ms) {
 inline MinResult naive_pr(const Dfa& d, const PrOptions& opt = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block(d.num_states);
+  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_pr_pass, opt.trace};
@@ -291,7 +330,7 @@ inline MinResult naive_pr_cas(const Dfa& d, std::int64_t timeout_ms = 300'000,
                               PrTrace* trace = nullptr) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block(d.num_states);
+  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_pr_pass, trace};
@@ -335,7 +374,7 @@ inline ExpandedDfa expand_alphabet(const Dfa& d, const Limits& limits = {}) {
 inline MinResult trans_pr(const Dfa& d, const PrOptions& opt = {}, const Limits& limits = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block(d.num_states);
+  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   const dfm_limits lim{limits.max_memory_bytes, opt.timeout_ms};
@@ -361,7 +400,7 @@ inline MinResult trans_minimize(const Dfa& d, const Limits& limits = {},
   Engine& e = Engine::thread_default();
   detail::View v(d);
   const std::size_t n = d.num_states;
-  std::vector<std::uint32_t> block(n);
+  std::vector<std::uint32_t> block = detail::partition_buffer(n);
   std::uint32_t nb = 0;
   dfm_stats st{};
   const dfm_limits lim{limits.max_memory_bytes, limits.timeout_ms};
@@ -512,7 +551,7 @@ inline MinResult sort_pr(const Dfa& d, ShardedEngine& se, const SortOptions& opt
   local.delta = rows.empty() ? nullptr : rows.data();
   local.accepting = d.accepting.data() + lo;
   local.initial = 0;
-  std::vector<std::uint32_t> block(d.num_states);
+  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   se.check(dfm_sort_pr_sharded(se.get(), d.num_states, &local, 1, block.data(), &nb,
