@@ -374,8 +374,23 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       if ((uint64_t)u < a.letters) qrow[u] = a.rows[(uint64_t)u * a.n + first];
   }
   const bool own_label_enabled = a.own_label;
+  // masked passes above the resident threads: each CTA owns a contiguous range and its
+  // warps take rows of 32 states from a shared counter, so a warp that drew cheap rows
+  // (skip tests) takes more instead of waiting at the grid barrier for the warp that
+  // drew full evaluations (ncu, C2: 44 % of the stall samples were that barrier)
+  constexpr bool dyn = kMask && !kOne;
+  __shared__ uint32_t s_row[2];
+  uint64_t dlo = 0, dhi = 0;
+  if (dyn) {
+    const uint64_t per = ((a.n + gridDim.x - 1) / gridDim.x + 31) & ~31ull;
+    dlo = (uint64_t)blockIdx.x * per;
+    dhi = dlo + per < a.n ? dlo + per : a.n;
+    if (threadIdx.x < 2) s_row[threadIdx.x] = 0;
+    __syncthreads();
+  }
   while (p < a.max_passes) {
     const uint32_t pass = a.pass0 + p + 1;
+    if (dyn && threadIdx.x == 0) s_row[(p + 1) & 1] = 0;  // last used in pass p - 1
     const uint32_t* Lm = sel ? a.lab1 : a.lab0;
     uint32_t* Lw = sel ? a.lab0 : a.lab1;
     const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
@@ -383,10 +398,17 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
     const uint32_t prev_changed =
         p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
     bool any = false;
-    for (uint64_t qb = first - (threadIdx.x & 31); qb < a.n; qb += nth) {
+    const uint64_t qend = dyn ? dhi : a.n;
+    for (uint64_t qb = dyn ? 0 : first - (threadIdx.x & 31);; qb += nth) {
+      if (dyn) {
+        uint32_t r = 0;
+        if ((threadIdx.x & 31) == 0) r = atomicAdd(&s_row[p & 1], 1u);
+        qb = dlo + 32ull * __shfl_sync(0xffffffffu, r, 0);
+      }
+      if (qb >= qend) break;
       const uint64_t qi = qb + (threadIdx.x & 31);
-      const uint32_t vmask = __ballot_sync(0xffffffffu, qi < a.n);
-      if (qi >= a.n) continue;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, qi < qend);
+      if (qi >= qend) continue;
       const uint32_t q = (uint32_t)qi;
       const uint32_t lw = (one && p > 0 && own_label_enabled) ? myw : Lm[q];
       const uint32_t leader = label_on_the_fly(lw, cprev);
@@ -489,6 +511,191 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
   if (!stable && p > 0 && prims::ld_relaxed_u32(&a.changed[p - 1]) == 0u)
     stable = true;
   if (first == 0) {
+    a.out[0] = p;
+    a.out[1] = stable ? 1u : 0u;
+    a.out[2] = (uint32_t)sel;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Queued masked passes (letter masks on, n above the resident threads).  The grid-
+// stride loop of fused_pr_kernel<kMask> walks ~n / resident-threads states per thread
+// one after another, each a chain of dependent L2 round trips (label word -> cell ->
+// masks -> rows -> labels -> cells), although most states stop at the skip test.
+// Here a pass runs in rounds of kQueue states per CTA: stage A evaluates the skip test
+// of three states per thread with all their loads in flight and writes the unchanged
+// labels at once; the states that must compare letters go to a shared-memory queue,
+// which stage B drains one entry per thread.  The queue breaks the lane = q order the
+// warp-aggregated election relies on, so the group's candidate is found with a
+// min / max reduction over its lanes.  Same per-pass semantics as fused_pr_kernel.
+constexpr int kQueuePer = 3;  // states per thread per round (static smem: 36 KB)
+constexpr int kQueue = kQueuePer * kPersistThreads;
+template <int kPolicy>
+__device__ __forceinline__ void elect_cell_any(unsigned long long* cells, uint32_t leader,
+                                               uint32_t q, uint32_t pass, bool sp,
+                                               uint32_t vmask) {
+  const uint32_t spm = __ballot_sync(vmask, sp);
+  if (!sp) return;
+  const uint32_t peers = __match_any_sync(spm, leader);
+  if (kPolicy == DFM_POLICY_MIN) {
+    if (__reduce_min_sync(peers, q) == q)
+      atomicMin(&cells[leader], ((unsigned long long)(~pass) << 32) | q);
+  } else if (kPolicy == DFM_POLICY_MAX) {
+    if (__reduce_max_sync(peers, q) == q)
+      atomicMax(&cells[leader], ((unsigned long long)pass << 32) | q);
+  } else if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+    *reinterpret_cast<volatile unsigned long long*>(&cells[leader]) =
+        ((unsigned long long)pass << 32) | q;
+  }
+}
+
+template <int kPolicy>
+__global__ void __launch_bounds__(kPersistThreads) queue_pr_kernel(FusedArgs a) {
+  cg::grid_group g = cg::this_grid();
+  __shared__ uint32_t s_q[kQueue], s_l[kQueue], s_m[kQueue];
+  __shared__ uint32_t s_cnt;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t per = (a.n + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = (uint64_t)blockIdx.x * per;
+  const uint64_t hi = lo + per < a.n ? lo + per : a.n;
+  int sel = a.start_sel;
+  uint32_t p = 0;
+  bool stable = false;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  while (p < a.max_passes) {
+    const uint32_t pass = a.pass0 + p + 1;
+    const uint32_t* Lm = sel ? a.lab1 : a.lab0;
+    uint32_t* Lw = sel ? a.lab0 : a.lab1;
+    const unsigned long long* cprev = (pass & 1) ? a.cells0 : a.cells1;
+    unsigned long long* ccur = (pass & 1) ? a.cells1 : a.cells0;
+    const uint32_t prev_changed = p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
+    const uint32_t* mc = a.mark + (uint64_t)(pass % 3) * a.n;
+    uint32_t* mn = a.mark + (uint64_t)((pass + 1) % 3) * a.n;
+    uint32_t* mz = a.mark + (uint64_t)((pass + 2) % 3) * a.n;
+    const bool masks_valid = pass > a.dirty_from;
+    bool any = false;
+    for (uint64_t rb = lo; rb < hi; rb += kQueue) {
+      // stage A: skip tests, kQueuePer states per thread, loads batched
+      uint32_t lw[kQueuePer], ld[kQueuePer], lm[kQueuePer];
+#pragma unroll
+      for (int u = 0; u < kQueuePer; ++u) {
+        const uint64_t qi = rb + (uint64_t)u * kPersistThreads + threadIdx.x;
+        lw[u] = qi < hi ? Lm[qi] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kQueuePer; ++u) {
+        const uint64_t qi = rb + (uint64_t)u * kPersistThreads + threadIdx.x;
+        ld[u] = qi < hi ? label_on_the_fly(lw[u], cprev) : (uint32_t)qi;
+      }
+#pragma unroll
+      for (int u = 0; u < kQueuePer; ++u) {
+        const uint64_t qi = rb + (uint64_t)u * kPersistThreads + threadIdx.x;
+        const bool ev = qi < hi && (uint32_t)qi != ld[u];
+        lm[u] = 0u;
+        if (ev) lm[u] = (masks_valid && !(lw[u] & kSplitBit)) ? (mc[qi] | mc[ld[u]]) : 0xFFFFFFFFu;
+        if (qi < hi) mz[qi] = 0u;  // (read in pass - 1, written in pass + 1)
+      }
+#pragma unroll
+      for (int u = 0; u < kQueuePer; ++u) {
+        const uint64_t qi = rb + (uint64_t)u * kPersistThreads + threadIdx.x;
+        const bool push = lm[u] != 0u;
+        if (qi < hi && !push) Lw[qi] = ld[u];
+        const uint32_t bm = __ballot_sync(0xffffffffu, push);
+        uint32_t base = 0;
+        if (lane == 0 && bm) base = atomicAdd(&s_cnt, (uint32_t)__popc(bm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (push) {
+          const uint32_t slot = base + __popc(bm & ((1u << lane) - 1u));
+          s_q[slot] = (uint32_t)qi;
+          s_l[slot] = ld[u];
+          s_m[slot] = lm[u];
+        }
+      }
+      __syncthreads();
+      const uint32_t cnt = s_cnt;
+      // stage B: the queued states compare their letters
+      for (uint32_t ib = threadIdx.x - lane; ib < cnt; ib += kPersistThreads) {
+        const uint32_t i = ib + lane;
+        const bool valid = i < cnt;
+        const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+        if (!valid) continue;
+        const uint32_t q = s_q[i], leader = s_l[i];
+        uint32_t rem = s_m[i];
+        bool sp = false;
+        if (rem == 0xFFFFFFFFu) {
+          for (uint64_t a0 = 0; a0 < a.letters && !sp; a0 += 4) {
+            uint32_t tq[4], tl[4], lq[4], ll[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (a0 + u < a.letters) {
+                tq[u] = a.rows[(a0 + u) * a.n + q];
+                tl[u] = a.rows[(a0 + u) * a.n + leader];
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (a0 + u < a.letters) {
+                lq[u] = Lm[tq[u]];
+                ll[u] = Lm[tl[u]];
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (a0 + u < a.letters)
+                sp |= label_on_the_fly(lq[u], cprev) != label_on_the_fly(ll[u], cprev);
+          }
+        } else {
+          while (rem != 0u && !sp) {
+            uint32_t al[4], tq[4], tl[4], lq[4], ll[4];
+            int c = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (rem != 0u) {
+                al[u] = (uint32_t)__ffs(rem) - 1u;
+                rem &= rem - 1u;
+                c = u + 1;
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < c) {
+                tq[u] = a.rows[(uint64_t)al[u] * a.n + q];
+                tl[u] = a.rows[(uint64_t)al[u] * a.n + leader];
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < c) {
+                lq[u] = Lm[tq[u]];
+                ll[u] = Lm[tl[u]];
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < c) sp |= label_on_the_fly(lq[u], cprev) != label_on_the_fly(ll[u], cprev);
+          }
+        }
+        Lw[q] = leader | (sp ? kSplitBit : 0u);
+        any |= sp;
+        elect_cell_any<kPolicy>(ccur, leader, q, pass, sp, vmask);
+        if (sp) {  // q's label changes: its predecessors compare that letter next pass
+          for (uint32_t e = a.pred_off[q], e1 = a.pred_off[q + 1]; e < e1; ++e) {
+            const uint32_t ps = a.pred_src[e];
+            atomicOr(&mn[ps & ((1u << kPredSrcBits) - 1u)], 1u << (ps >> kPredSrcBits));
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+    }
+    if (prev_changed == 0u) {  // pass p was stable: this pass rewrote the same labels
+      stable = true;
+      break;
+    }
+    if (__any_sync(0xffffffffu, any) && lane == 0) a.changed[p] = 1u;
+    g.sync();
+    sel ^= 1;
+    ++p;
+  }
+  if (!stable && p > 0 && prims::ld_relaxed_u32(&a.changed[p - 1]) == 0u) stable = true;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out[0] = p;
     a.out[1] = stable ? 1u : 0u;
     a.out[2] = (uint32_t)sel;
@@ -828,6 +1035,14 @@ struct DegOut {
   }
 };
 
+// DFM_NAIVE_QUEUE=1 (opt-in): the masked passes above the resident threads run
+// queue_pr_kernel.  Measured on C2 naive (vlts(1000, 1e6, 20), profiles/r04b): 35.5 vs
+// 33.0 ms for fused_pr_kernel<kMask> — exact, but slower
+bool queue_enabled() {
+  const char* e = getenv("DFM_NAIVE_QUEUE");
+  return e != nullptr && e[0] == '1';
+}
+
 bool own_label_on() {
   const char* e = getenv("DFM_NAIVE_OWN_LABEL");
   return e == nullptr || e[0] != '0';
@@ -1064,6 +1279,10 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
             : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, false, true>
                                        : fused_pr_kernel<DFM_POLICY_ARBITRARY, false, true>;
         lk = (const void*)mk;
+        if (mk != mk_one && queue_enabled())
+          lk = policy == DFM_POLICY_MIN   ? (const void*)queue_pr_kernel<DFM_POLICY_MIN>
+               : policy == DFM_POLICY_MAX ? (const void*)queue_pr_kernel<DFM_POLICY_MAX>
+                                          : (const void*)queue_pr_kernel<DFM_POLICY_ARBITRARY>;
         lgrid = (unsigned)std::max<uint64_t>(
             1, std::min<uint64_t>(ceil_div(n, kPersistThreads),
                                   fused_max_states(ctx, lk) / kPersistThreads));
