@@ -374,17 +374,16 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
       if ((uint64_t)u < a.letters) qrow[u] = a.rows[(uint64_t)u * a.n + first];
   }
   const bool own_label_enabled = a.own_label;
-  // masked passes above the resident threads: each CTA owns a contiguous range and its
-  // warps take rows of 32 states from a shared counter, so a warp that drew cheap rows
+  // masked passes above the resident threads: the warps of a CTA take its rows of 32
+  // states from a shared counter, so a warp that drew cheap rows
   // (skip tests) takes more instead of waiting at the grid barrier for the warp that
   // drew full evaluations (ncu, C2: 44 % of the stall samples were that barrier)
   constexpr bool dyn = kMask && !kOne;
   __shared__ uint32_t s_row[2];
-  uint64_t dlo = 0, dhi = 0;
+  // rows are dealt round-robin (CTA b takes rows b, b + G, b + 2G, ...): every CTA
+  // draws from the whole state range, so contiguous heavy regions spread over the SMs
+  const uint64_t nrows = (a.n + 31) / 32;
   if (dyn) {
-    const uint64_t per = ((a.n + gridDim.x - 1) / gridDim.x + 31) & ~31ull;
-    dlo = (uint64_t)blockIdx.x * per;
-    dhi = dlo + per < a.n ? dlo + per : a.n;
     if (threadIdx.x < 2) s_row[threadIdx.x] = 0;
     __syncthreads();
   }
@@ -398,12 +397,13 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
     const uint32_t prev_changed =
         p > 0 ? prims::ld_relaxed_u32(&a.changed[p - 1]) : 1u;
     bool any = false;
-    const uint64_t qend = dyn ? dhi : a.n;
+    const uint64_t qend = a.n;
     for (uint64_t qb = dyn ? 0 : first - (threadIdx.x & 31);; qb += nth) {
       if (dyn) {
         uint32_t r = 0;
         if ((threadIdx.x & 31) == 0) r = atomicAdd(&s_row[p & 1], 1u);
-        qb = dlo + 32ull * __shfl_sync(0xffffffffu, r, 0);
+        const uint64_t row = blockIdx.x + (uint64_t)gridDim.x * __shfl_sync(0xffffffffu, r, 0);
+        qb = row < nrows ? 32ull * row : qend;
       }
       if (qb >= qend) break;
       const uint64_t qi = qb + (threadIdx.x & 31);
