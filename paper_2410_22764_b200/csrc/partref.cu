@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) 
   // states from a shared counter, so a warp that drew cheap rows
   // (skip tests) takes more instead of waiting at the grid barrier for the warp that
   // drew full evaluations (ncu, C2: 44 % of the stall samples were that barrier)
-  constexpr bool dyn = kMask && !kOne;
+  constexpr bool dyn = !kOne;
   __shared__ uint32_t s_row[2];
   // rows are dealt round-robin (CTA b takes rows b, b + G, b + 2G, ...): every CTA
   // draws from the whole state range, so contiguous heavy regions spread over the SMs

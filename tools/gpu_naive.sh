@@ -8,3 +8,9 @@ for q in ${QS:-1 0}; do
   python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[1], d['ms_per_step'], d['config'].get('passes'), d['config'].get('blocks'))" $OUT/c2_naive_q$q.json
 done
 timeout 300 python tools/host_register_probe.py > $OUT/host_register.txt 2>&1; cat $OUT/host_register.txt
+if [ -n "${MORE:-}" ]; then
+  timeout 600 python bench.py --algo naive --n 100000 --k 2 --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/c1_naive.json 2>&1
+  timeout 600 python bench.py --algo transpr --family comb --n 1000000 --k 2 --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/c3_comb.json 2>&1
+  timeout 600 python bench.py --algo transpr --family chain --n 10000000 --k 1 --steps 3 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/c3_chain.json 2>&1
+  for f in c1_naive c3_comb c3_chain; do python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[1], d['ms_per_step'], d['config'].get('passes'), d['config'].get('blocks'))" $OUT/$f.json; done
+fi
