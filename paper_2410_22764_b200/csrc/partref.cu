@@ -1043,6 +1043,13 @@ bool queue_enabled() {
   return e != nullptr && e[0] == '1';
 }
 
+// DFM_NAIVE_ONE=0 (tests): the grid-stride / dynamic-row kernels even when every
+// state would get its own resident thread
+bool one_enabled() {
+  const char* e = getenv("DFM_NAIVE_ONE");
+  return e == nullptr || e[0] != '0';
+}
+
 bool own_label_on() {
   const char* e = getenv("DFM_NAIVE_OWN_LABEL");
   return e == nullptr || e[0] != '0';
@@ -1205,7 +1212,7 @@ AlgoOut run_leader_election(Ctx& ctx, const DevDfa& d, const uint32_t* rows, uin
         : policy == DFM_POLICY_MAX ? fused_pr_kernel<DFM_POLICY_MAX, true>
                                    : fused_pr_kernel<DFM_POLICY_ARBITRARY, true>;
     // a thread per state when the kOne variant holds all n resident
-    const bool one = n <= fused_max_states(ctx, (const void*)kern_one);
+    const bool one = n <= fused_max_states(ctx, (const void*)kern_one) && one_enabled();
     const int gm = group_mode();
     const int lanes = (letters >= 8 && ((gm == 1 && !one) || gm == 2)) ? (letters >= 16 ? 8 : 4) : 1;
     void (*kern)(FusedArgs) =

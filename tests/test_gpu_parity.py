@@ -515,6 +515,33 @@ def test_naive_work_efficient_passes(eng, monkeypatch, name, pair):
 
 @pytest.mark.parametrize("name,pair", [
     ("vlts_k12", lambda: O.vlts_dfa(300, 60_000, 12)),
+    ("random_k9", lambda: O.random_dfa(20_000, 9, 77, 0.5)),
+    ("random_k2", lambda: O.random_dfa(20_000, 2, 3, 0.5)),
+])
+def test_naive_dynamic_rows_and_queue(eng, monkeypatch, name, pair):
+    """The kernels for inputs above the resident threads — dynamic round-robin rows of
+    fused_pr_kernel (plain and letter-mask instances) and the opt-in queue_pr_kernel —
+    forced on small inputs (DFM_NAIVE_ONE=0, marks from the first pass): the reference's
+    partition and pass count under min and max; transPR too."""
+    delta, acc = pair()
+    d = to_dfa((delta, acc))
+    monkeypatch.setenv("DFM_NAIVE_ONE", "0")
+    for pol, name_ in ((MIN, "min"), (MAX, "max")):
+        ref = O.naive_pr(delta, acc, name_)
+        for dirty, queue in (("0", "0"), ("1", "0"), ("1", "1")):
+            monkeypatch.setenv("DFM_NAIVE_DIRTY", dirty)
+            monkeypatch.setenv("DFM_NAIVE_DIRTY_AFTER", "0")
+            monkeypatch.setenv("DFM_NAIVE_QUEUE", queue)
+            r = eng.naive_pr(d, dfm.PrOptions(policy=pol))
+            assert r.stats.iterations == ref.iterations, (name, name_, dirty, queue)
+            assert (r.partition.block == ref.block).all(), (name, name_, dirty, queue)
+    rt = eng.trans_pr(d, dfm.PrOptions(policy=MIN))
+    ref_t = O.trans_pr(delta, acc, "min")
+    assert rt.stats.iterations == ref_t.iterations and (rt.partition.block == ref_t.block).all()
+
+
+@pytest.mark.parametrize("name,pair", [
+    ("vlts_k12", lambda: O.vlts_dfa(300, 60_000, 12)),
     ("vlts_k20", lambda: O.vlts_dfa(200, 40_000, 20)),
     ("random_k9", lambda: O.random_dfa(20_000, 9, 77, 0.5)),
     ("random_k33", lambda: O.random_dfa(5_000, 33, 5, 0.5)),
