@@ -5,7 +5,9 @@
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -102,19 +104,99 @@ unsigned stage_threads() {
   return std::max(1u, std::min(12u, std::thread::hardware_concurrency() * 3 / 4));
 }
 
-void par_memcpy(void* dst, const void* src, size_t bytes, unsigned T) {
-  if (bytes < (8u << 20) || T <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
+// Persistent host workers for the staging copies.  Spawning the copy threads per
+// memcpy call (one fork-join per letter segment of every chunk) cost a third of the
+// staging throughput: copying random_dfa(1e8, 4)'s rows into a pinned ring took 83 ms
+// with 8 spawned threads per call and 56 ms with 8 persistent workers, one fork-join
+// per chunk (8-core container, /tmp bench in DESIGN.md §1).  One pool per process;
+// concurrent uploads take turns (they share the host's memory bandwidth anyway).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool(stage_threads());
+    return pool;
   }
+  unsigned size() const { return T_; }
+  // f(t) for t in [0, size()): t = 0 on the calling thread
+  void run(const std::function<void(unsigned)>& f) {
+    std::lock_guard<std::mutex> turn(run_mu_);
+    if (T_ == 1) {
+      f(0);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      left_ = T_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return left_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  explicit HostPool(unsigned T) : T_(std::max(1u, T)) {
+    for (unsigned t = 1; t < T_; ++t)
+      th_.emplace_back([this, t] {
+        uint64_t seen = 0;
+        while (true) {
+          const std::function<void(unsigned)>* f;
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            f = job_;
+          }
+          (*f)(t);
+          std::lock_guard<std::mutex> lk(mu_);
+          if (--left_ == 0) done_.notify_one();
+        }
+      });
+  }
+  unsigned T_;
+  std::vector<std::thread> th_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  unsigned left_ = 0;
+  bool stop_ = false;
+};
+
+// dst[0 .. nseg*seg) = the segments srcs[0..nseg) (seg bytes each) back to back,
+// split evenly over the pool (a worker's share may cross segment boundaries)
+void par_memcpy_segs(char* dst, const char* const* srcs, size_t seg, size_t nseg) {
+  const size_t total = seg * nseg;
+  HostPool& pool = HostPool::get();
+  const unsigned T = total < (8u << 20) ? 1u : pool.size();
   auto part = [&](unsigned t) {
-    const size_t lo = (bytes * t / T) & ~size_t(63), hi = t + 1 == T ? bytes : (bytes * (t + 1) / T) & ~size_t(63);
-    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+    size_t lo = (total * t / T) & ~size_t(63);
+    const size_t hi = t + 1 == T ? total : (total * (t + 1) / T) & ~size_t(63);
+    while (lo < hi) {
+      const size_t a = lo / seg, o = lo - a * seg, e = std::min(hi, (a + 1) * seg);
+      std::memcpy(dst + lo, srcs[a] + o, e - lo);
+      lo = e;
+    }
   };
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < T; ++t) th.emplace_back(part, t);
-  part(0);
-  for (auto& x : th) x.join();
+  if (T == 1) part(0);
+  else pool.run(part);
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const char* s = static_cast<const char*>(src);
+  par_memcpy_segs(static_cast<char*>(dst), &s, bytes, 1);
 }
 
 constexpr uint32_t kRing = 3;  // pinned ring slots of one upload chunk each
@@ -151,15 +233,16 @@ class PageableStager final : public ChunkGate {
     try {
       DFM_CUDA(cudaSetDevice(ctx_.device));
       const uint64_t n = d_->num_states, k = d_->alphabet_size;
-      const unsigned T = stage_threads();
       cudaStream_t cs = ctx_.copy();
+      std::vector<const char*> srcs(k);
       for (uint32_t c = 0; c < nc_; ++c) {
         const uint32_t s = c % kRing;
         if (slot_used_[s]) DFM_CUDA(cudaEventSynchronize(slot_ev_[s]));
         char* slot = ring_ + (uint64_t)s * slot_bytes_;
         const uint64_t q0 = (uint64_t)c * chunk_, len = std::min(n, q0 + chunk_) - q0;
         for (uint64_t a = 0; a < k; ++a)
-          par_memcpy(slot + a * len * 4, d_->delta[a] + q0, len * 4, T);
+          srcs[a] = reinterpret_cast<const char*>(d_->delta[a] + q0);
+        par_memcpy_segs(slot, srcs.data(), len * 4, k);
         for (uint64_t a = 0; a < k; ++a)
           DFM_CUDA(cudaMemcpyAsync(dev_ + a * n + q0, slot + a * len * 4, len * 4,
                                    cudaMemcpyHostToDevice, cs));
@@ -213,13 +296,12 @@ struct StageRes {
 // (synchronous for the caller; the DMA runs on `stream`)
 void staged_h2d(Ctx& ctx, void* dst, const void* src, uint64_t bytes, cudaStream_t stream,
                 char* ring, uint64_t slot_bytes, StageRes& res) {
-  const unsigned T = stage_threads();
   uint32_t& s = res.next;  // ring cursor continues across pieces
   for (uint64_t off = 0; off < bytes; off += slot_bytes, s = (s + 1) % kRing) {
     const uint64_t len = std::min(slot_bytes, bytes - off);
     if (res.used[s]) DFM_CUDA(cudaEventSynchronize(res.ev[s]));
     char* slot = ring + (uint64_t)s * slot_bytes;
-    par_memcpy(slot, static_cast<const char*>(src) + off, len, T);
+    par_memcpy(slot, static_cast<const char*>(src) + off, len);
     DFM_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, slot, len, cudaMemcpyHostToDevice,
                              stream));
     DFM_CUDA(cudaEventRecord(res.ev[s], stream));

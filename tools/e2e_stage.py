@@ -19,7 +19,9 @@ dd.free()
 page = dfm.Dfa(n, k, np.ascontiguousarray(host.delta), np.ascontiguousarray(host.accepting), 0)
 out = np.empty(n, np.uint32)
 res = {}
-for T in (4, 8, 12, 16):
+# the staging pool is sized once per process: one T per run (argv[1])
+Ts = [int(a) for a in sys.argv[1:]] or [int(os.environ.get("DFM_STAGE_THREADS", "12"))]
+for T in Ts:
     os.environ["DFM_STAGE_THREADS"] = str(T)
     eng.sort_pr(page, out=out)
     ts = []
