@@ -99,16 +99,18 @@ bool host_pinned_ptr(const void* p) {
 
 unsigned stage_threads() {
   if (const char* e = getenv("DFM_STAGE_THREADS")) return std::max(1, atoi(e));
-  // measured on the 16-core B200 hosts (tools/e2e_stage.py, profiles/r02h): 4 / 8 / 12 /
-  // 16 threads -> 84 / 69 / 66 / 69 ms e2e for random_dfa(1e8, 4) from pageable rows
-  return std::max(1u, std::min(12u, std::thread::hardware_concurrency() * 3 / 4));
+  // measured on the 16-core B200 hosts (tools/e2e_stage.py), e2e of random_dfa(1e8, 4)
+  // from pageable rows: threads spawned per copy (profiles/r02h) 4 / 8 / 12 / 16 ->
+  // 84 / 69 / 66 / 69 ms; the persistent pool (profiles/r04/r04g) 8 / 12 / 16 -> 66.7 /
+  // 60.8 / 58.1 ms (pinned rows: 41 ms)
+  return std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
 }
 
 // Persistent host workers for the staging copies.  Spawning the copy threads per
 // memcpy call (one fork-join per letter segment of every chunk) cost a third of the
 // staging throughput: copying random_dfa(1e8, 4)'s rows into a pinned ring took 83 ms
 // with 8 spawned threads per call and 56 ms with 8 persistent workers, one fork-join
-// per chunk (8-core container, /tmp bench in DESIGN.md §1).  One pool per process;
+// per chunk (8-core container).  One pool per process;
 // concurrent uploads take turns (they share the host's memory bandwidth anyway).
 class HostPool {
  public:

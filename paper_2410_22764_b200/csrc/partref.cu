@@ -1036,7 +1036,7 @@ struct DegOut {
 };
 
 // DFM_NAIVE_QUEUE=1 (opt-in): the masked passes above the resident threads run
-// queue_pr_kernel.  Measured on C2 naive (vlts(1000, 1e6, 20), profiles/r04b): 35.5 vs
+// queue_pr_kernel.  Measured on C2 naive (vlts(1000, 1e6, 20), profiles/r04/r04b): 35.5 vs
 // 33.0 ms for fused_pr_kernel<kMask> — exact, but slower
 bool queue_enabled() {
   const char* e = getenv("DFM_NAIVE_QUEUE");

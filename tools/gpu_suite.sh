@@ -5,7 +5,7 @@
 #   bash tools/gpu_suite.sh <tag> [tests bench ref c5 ncu sanitize]
 set -u
 TAG=${1:-r02}; shift || true
-WHAT=${*:-"tests bench ref c5 ncu sanitize"}
+WHAT=${*:-"tests bench ref c5 ncu"}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 { nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv; nproc; free -g;
