@@ -220,15 +220,45 @@ struct View {
 
 // The partition vector a MinResult returns (core.hpp: Partition::block).  A value-
 // initialised std::vector of 1e8 labels page-faults 400 MB of fresh mmap'd memory on
-// one thread (~200 ms, more than the whole GPU minimization); for large partitions the
-// pages are advised as huge pages and faulted in by several threads first, so
-// resize() only runs its memset over resident memory (measured ~50 ms at 1e8).
-inline std::vector<std::uint32_t> partition_buffer(std::size_t n) {
-  std::vector<std::uint32_t> v;
-  constexpr std::size_t kParallelBytes = std::size_t(64) << 20;
-  if (n * sizeof(std::uint32_t) >= kParallelBytes) {
-    v.reserve(n);
-    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(v.data());
+// one thread (~200 ms, more than the whole GPU minimization).  For large partitions
+// the vector is reserved, its pages advised as huge pages and faulted in by several
+// threads, and only then resized (the memset runs over resident memory) — all on a
+// helper thread WHILE the library works: the library calls ready() (through the
+// context's out-ready hook, dfm.h) before it first writes the buffer.
+class OutPartition {
+ public:
+  explicit OutPartition(std::size_t n) {
+    constexpr std::size_t kParallelBytes = std::size_t(64) << 20;
+    if (n * sizeof(std::uint32_t) < kParallelBytes) {
+      v_.resize(n);
+      p_ = v_.data();
+      return;
+    }
+    v_.reserve(n);
+    p_ = v_.data();  // stable: resize() within the capacity does not reallocate
+    th_ = std::thread([this, n] {
+      prefault(p_, n);
+      v_.resize(n);
+    });
+  }
+  OutPartition(const OutPartition&) = delete;
+  OutPartition& operator=(const OutPartition&) = delete;
+  ~OutPartition() { ready(); }
+  std::uint32_t* data() const { return p_; }
+  void ready() {
+    std::call_once(once_, [this] {
+      if (th_.joinable()) th_.join();
+    });
+  }
+  static void hook(void* self) { static_cast<OutPartition*>(self)->ready(); }
+  std::vector<std::uint32_t> take() {
+    ready();
+    return std::move(v_);
+  }
+
+ private:
+  static void prefault(std::uint32_t* p, std::size_t n) {
+    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(p);
     const std::uintptr_t e = b + n * sizeof(std::uint32_t);
 #if defined(__linux__) && defined(MADV_HUGEPAGE)
     const std::uintptr_t kHuge = std::uintptr_t(2) << 20;
@@ -247,9 +277,22 @@ inline std::vector<std::uint32_t> partition_buffer(std::size_t n) {
     touch(0);
     for (auto& x : th) x.join();
   }
-  v.resize(n);
-  return v;
-}
+  std::vector<std::uint32_t> v_;
+  std::uint32_t* p_ = nullptr;
+  std::thread th_;
+  std::once_flag once_;
+};
+
+// Arms the context's out-ready hook for one host-buffer call and disarms it after
+// (the library consumes it at the start of the call; this covers a call that fails
+// before reaching it).
+struct OutHook {
+  dfm_ctx* ctx;
+  OutHook(dfm_ctx* c, OutPartition& out) : ctx(c) {
+    dfm_ctx_set_out_ready_hook(ctx, &OutPartition::hook, &out);
+  }
+  ~OutHook() { dfm_ctx_set_out_ready_hook(ctx, nullptr, nullptr); }
+};
 
 inline MinResult result(std::vector<std::uint32_t>&& block, std::uint32_t nb, const dfm_stats& s) {
   MinResult r;
@@ -292,13 +335,16 @@ inline void on_pr_pass(void* user, std::uint64_t, const std::uint32_t* raw, std:
 inline MinResult sort_pr(const Dfa& d, const SortOptions& opt = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
+  detail::OutPartition block(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_sort_pass, opt.trace};
-  e.check(dfm_sort_pr(e.get(), &v.c, opt.timeout_ms, opt.trace ? &tr : nullptr, block.data(), &nb,
-                      &st));
-  return detail::result(std::move(block), nb, st);
+  {
+    detail::OutHook hook(e.get(), block);
+    e.check(dfm_sort_pr(e.get(), &v.c, opt.timeout_ms, opt.trace ? &tr : nullptr, block.data(),
+                        &nb, &st));
+  }
+  return detail::result(block.take(), nb, st);
 }
 
 inline MinResult sort_pr(const Dfa& d, std::int64_t timeout_ms) {
@@ -310,13 +356,16 @@ inline MinResult sort_pr(const Dfa& d, std::int64_t timeout_ms) {
 inline MinResult naive_pr(const Dfa& d, const PrOptions& opt = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
+  detail::OutPartition block(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_pr_pass, opt.trace};
-  e.check(dfm_naive_pr(e.get(), &v.c, detail::policy_of(opt.policy), opt.timeout_ms,
-                       opt.trace ? &tr : nullptr, block.data(), &nb, &st));
-  return detail::result(std::move(block), nb, st);
+  {
+    detail::OutHook hook(e.get(), block);
+    e.check(dfm_naive_pr(e.get(), &v.c, detail::policy_of(opt.policy), opt.timeout_ms,
+                         opt.trace ? &tr : nullptr, block.data(), &nb, &st));
+  }
+  return detail::result(block.take(), nb, st);
 }
 
 inline MinResult naive_pr(const Dfa& d, RacePolicy policy, std::int64_t timeout_ms = 300'000) {
@@ -330,13 +379,16 @@ inline MinResult naive_pr_cas(const Dfa& d, std::int64_t timeout_ms = 300'000,
                               PrTrace* trace = nullptr) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
+  detail::OutPartition block(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   dfm_trace tr{&detail::on_pr_pass, trace};
-  e.check(dfm_naive_pr_cas(e.get(), &v.c, timeout_ms, trace ? &tr : nullptr, block.data(), &nb,
-                           &st));
-  return detail::result(std::move(block), nb, st);
+  {
+    detail::OutHook hook(e.get(), block);
+    e.check(dfm_naive_pr_cas(e.get(), &v.c, timeout_ms, trace ? &tr : nullptr, block.data(),
+                             &nb, &st));
+  }
+  return detail::result(block.take(), nb, st);
 }
 
 inline std::uint32_t power_levels(std::uint32_t n) { return dfm_power_levels(n); }
@@ -374,13 +426,16 @@ inline ExpandedDfa expand_alphabet(const Dfa& d, const Limits& limits = {}) {
 inline MinResult trans_pr(const Dfa& d, const PrOptions& opt = {}, const Limits& limits = {}) {
   Engine& e = Engine::thread_default();
   detail::View v(d);
-  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
+  detail::OutPartition block(d.num_states);
   std::uint32_t nb = 0;
   dfm_stats st{};
   const dfm_limits lim{limits.max_memory_bytes, opt.timeout_ms};
-  e.check(dfm_trans_pr(e.get(), &v.c, detail::policy_of(opt.policy), &lim, block.data(), &nb,
-                       &st));
-  return detail::result(std::move(block), nb, st);
+  {
+    detail::OutHook hook(e.get(), block);
+    e.check(dfm_trans_pr(e.get(), &v.c, detail::policy_of(opt.policy), &lim, block.data(), &nb,
+                         &st));
+  }
+  return detail::result(block.take(), nb, st);
 }
 
 inline MinResult trans_pr(const Dfa& d, RacePolicy policy, std::int64_t timeout_ms = 300'000,
@@ -400,7 +455,7 @@ inline MinResult trans_minimize(const Dfa& d, const Limits& limits = {},
   Engine& e = Engine::thread_default();
   detail::View v(d);
   const std::size_t n = d.num_states;
-  std::vector<std::uint32_t> block = detail::partition_buffer(n);
+  detail::OutPartition block(n);
   std::uint32_t nb = 0;
   dfm_stats st{};
   const dfm_limits lim{limits.max_memory_bytes, limits.timeout_ms};
@@ -410,10 +465,13 @@ inline MinResult trans_minimize(const Dfa& d, const Limits& limits = {},
     apart.resize(n * n);
     pops.resize(4096);
   }
-  e.check(dfm_trans_minimize(e.get(), &v.c, &lim, inspect ? apart.data() : nullptr,
-                             inspect ? pops.data() : nullptr, inspect ? 4096u : 0u, block.data(),
-                             &nb, &st));
-  MinResult r = detail::result(std::move(block), nb, st);
+  {
+    detail::OutHook hook(e.get(), block);
+    e.check(dfm_trans_minimize(e.get(), &v.c, &lim, inspect ? apart.data() : nullptr,
+                               inspect ? pops.data() : nullptr, inspect ? 4096u : 0u,
+                               block.data(), &nb, &st));
+  }
+  MinResult r = detail::result(block.take(), nb, st);
   if (inspect && r.stats.status == RunStatus::ok) {
     inspect->apart = std::move(apart);
     inspect->apart_popcounts.assign(pops.begin(), pops.begin() + r.stats.iterations);
@@ -551,12 +609,13 @@ inline MinResult sort_pr(const Dfa& d, ShardedEngine& se, const SortOptions& opt
   local.delta = rows.empty() ? nullptr : rows.data();
   local.accepting = d.accepting.data() + lo;
   local.initial = 0;
-  std::vector<std::uint32_t> block = detail::partition_buffer(d.num_states);
+  detail::OutPartition block(d.num_states);
+  block.ready();  // (the sharded entry has no out-ready hook)
   std::uint32_t nb = 0;
   dfm_stats st{};
   se.check(dfm_sort_pr_sharded(se.get(), d.num_states, &local, 1, block.data(), &nb,
                                opt.timeout_ms, &st));
-  return detail::result(std::move(block), nb, st);
+  return detail::result(block.take(), nb, st);
 }
 
 }  // namespace dfamin::b200

@@ -127,6 +127,15 @@ int dfm_ctx_set_sortpr_engine(dfm_ctx* ctx, int engine);
 #define DFM_TRANS_BIT 1
 #define DFM_TRANS_TENSOR 2
 int dfm_ctx_set_trans_engine(dfm_ctx* ctx, int engine);
+/* Output-ready hook for the NEXT host-buffer minimize call on this context (that call
+ * consumes it; NULL clears it): the library calls ready(user) once — from one of its
+ * threads, possibly while the GPU still works — before it first writes the caller's
+ * partition buffer (block_out), and waits for it to return.  A caller can thus prepare
+ * a fresh output buffer (fault its pages in) concurrently with the minimization; the
+ * C++ layer (dfamin_b200.hpp) does this for the MinResult partition vector.  Not a
+ * reference interface: the reference returns a freshly built std::vector. */
+typedef void (*dfm_out_ready_fn)(void* user);
+int dfm_ctx_set_out_ready_hook(dfm_ctx* ctx, dfm_out_ready_fn ready, void* user);
 /* Record per-kernel CUDA-event timings for subsequent calls (bench/roofline). */
 int dfm_ctx_set_profiling(dfm_ctx* ctx, int enabled);
 /* Read back timing for a kernel family ("sig", "sort", "scan", "relabel", "elect",

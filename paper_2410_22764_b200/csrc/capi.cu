@@ -441,14 +441,28 @@ void host_iota(uint32_t* out, uint64_t n) {
   for (auto& x : th) x.join();
 }
 
+// the caller's out-ready hook (dfm_ctx_set_out_ready_hook): run once before the first
+// write into the caller's partition buffer, from whichever thread writes first
+struct OutGate {
+  void (*fn)(void*) = nullptr;
+  void* user = nullptr;
+  std::once_flag once;
+  void wait() {
+    if (fn) std::call_once(once, [this] { fn(user); });
+  }
+};
+
 // sortPR on a large automaton usually ends all singletons (random DFAs): the identity
 // labels are written into the caller's buffer by a host thread WHILE the GPU runs;
 // joined before anything else touches the buffer (a non-identity result overwrites it)
 struct SpeculativeIota {
   std::thread th;
   bool started = false;
-  void start(uint32_t* out, uint64_t n) {
-    th = std::thread([out, n] { host_iota(out, n); });
+  void start(uint32_t* out, uint64_t n, OutGate* gate) {
+    th = std::thread([out, n, gate] {
+      gate->wait();
+      host_iota(out, n);
+    });
     started = true;
   }
   void join() {
@@ -458,8 +472,9 @@ struct SpeculativeIota {
 };
 
 void finish(Ctx& ctx, const AlgoOut& o, uint64_t n, const Deadline& dl, uint32_t* block_out,
-            uint32_t* nb_out, dfm_stats* st, bool iota_written = false) {
+            uint32_t* nb_out, dfm_stats* st, bool iota_written = false, OutGate* gate = nullptr) {
   const bool identity = o.status == DFM_STATUS_OK && block_out != nullptr && o.canon_identity;
+  if (gate && o.status == DFM_STATUS_OK && block_out != nullptr) gate->wait();
   if (o.status == DFM_STATUS_OK && block_out != nullptr && !identity)
     DFM_CUDA(cudaMemcpyAsync(block_out, o.canon_dev, n * 4, cudaMemcpyDeviceToHost, ctx.stream));
   ctx.sync();
@@ -481,10 +496,15 @@ int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const d
   return guarded(c, [&](Ctx& ctx) {
     const Deadline whole(0);
     const dfm_limits lim = limits_or_default(l);
-    SpeculativeIota spec;
+    OutGate gate;  // consumes the armed out-ready hook
+    gate.fn = ctx.out_ready;
+    gate.user = ctx.out_user;
+    ctx.out_ready = nullptr;
+    ctx.out_user = nullptr;
+    SpeculativeIota spec;  // (declared after the gate: joined before it goes away)
     if (algo == DFM_ALGO_SORT && block_out != nullptr && d != nullptr &&
         d->num_states >= (1u << 22))
-      spec.start(block_out, d->num_states);
+      spec.start(block_out, d->num_states, &gate);
     const uint64_t chunk =
         (algo == DFM_ALGO_SORT && ctx.sortpr_engine != DFM_SORTPR_RADIX && d != nullptr &&
          !(trace && trace->on_pass))
@@ -504,7 +524,7 @@ int run_host(dfm_ctx* c, int32_t algo, const dfm_dfa* d, int32_t policy, const d
     if (stage && stage->stager) stage->stager->join();
     if (dd.nready) DFM_CUDA(cudaStreamSynchronize(ctx.copy()));
     spec.join();
-    finish(ctx, o, dd.n, whole, block_out, nb_out, st, spec.started);
+    finish(ctx, o, dd.n, whole, block_out, nb_out, st, spec.started, &gate);
   });
 }
 
@@ -589,6 +609,13 @@ int dfm_ctx_set_sortpr_engine(dfm_ctx* c, int engine) {
     if (engine != DFM_SORTPR_HASH && engine != DFM_SORTPR_RADIX)
       throw Error(DFM_ERR_INVALID, "unknown sortPR engine");
     ctx.sortpr_engine = engine;
+  });
+}
+
+int dfm_ctx_set_out_ready_hook(dfm_ctx* c, dfm_out_ready_fn ready, void* user) {
+  return guarded(c, [&](Ctx& ctx) {
+    ctx.out_ready = ready;
+    ctx.out_user = ready ? user : nullptr;
   });
 }
 

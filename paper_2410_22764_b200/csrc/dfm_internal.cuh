@@ -99,6 +99,9 @@ struct Ctx {
   int trans_engine = 0;
   // sharded contexts (dfm_ctx_create_sharded[_local]): this rank's communicator
   Comm* comm = nullptr;
+  // dfm_ctx_set_out_ready_hook: armed for the next host-buffer call
+  void (*out_ready)(void*) = nullptr;
+  void* out_user = nullptr;
   // profiling
   bool profiling = false;
   struct Pending {

@@ -38,9 +38,12 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // 32/kBits per word, little-endian: 8/16 bits are plain byte / short arrays)
 template <int kBits>
 __device__ __forceinline__ uint32_t full_id(const uint32_t* __restrict__ full, uint64_t t) {
-  if (kBits == 32) return full[t];
-  constexpr uint32_t per = 32 / kBits;
-  return (full[t / per] >> ((uint32_t)(t % per) * kBits)) & ((1u << kBits) - 1u);
+  if constexpr (kBits == 32) {
+    return full[t];
+  } else {
+    constexpr uint32_t per = 32 / kBits;
+    return (full[t / per] >> ((uint32_t)(t % per) * kBits)) & ((1u << kBits) - 1u);
+  }
 }
 
 // Exact packed keys while (k+1) * bits(B-1) <= 63 (the early passes): no signature

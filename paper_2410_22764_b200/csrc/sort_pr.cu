@@ -55,9 +55,12 @@ struct SigParams {
 // B <= 2/16/256/65536 — 12.5 / 50 / 100 / 200 MB at 1e8 states) or the block array
 template <int kBits>
 __device__ __forceinline__ uint32_t succ_id(const SigParams& p, uint32_t t) {
-  if (kBits == 32) return p.block[t];
-  constexpr uint32_t per = 32 / kBits;
-  return (p.mirror[t / per] >> ((t % per) * kBits)) & ((1u << kBits) - 1u);
+  if constexpr (kBits == 32) {
+    return p.block[t];
+  } else {
+    constexpr uint32_t per = 32 / kBits;
+    return (p.mirror[t / per] >> ((t % per) * kBits)) & ((1u << kBits) - 1u);
+  }
 }
 
 template <int kBits>

@@ -44,3 +44,25 @@ def test_minimizes_like_the_oracle():
         out = run(*args, 2)
         ref = O.sort_pr(*pair)
         assert (out["blocks"], out["passes"]) == (ref.num_blocks, ref.iterations)
+
+
+def part_digest(block) -> str:
+    b = np.asarray(block, dtype=np.uint64)
+    i = np.arange(b.size, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return f"{int((b * (np.uint64(2654435761) * i + np.uint64(1))).sum(dtype=np.uint64)):016x}"
+
+
+@pytest.mark.gpu
+def test_large_partitions_through_the_output_hook():
+    """Partitions of >= 64 MB are prepared on a helper thread while the library works
+    and handed over through the out-ready hook (dfm_ctx_set_out_ready_hook): the C++
+    result equals the Python host-buffer result — an identity one (written by the
+    speculative iota thread) and a non-identity one (D2H)."""
+    eng = dfm.Engine(0)
+    for args, d in ((("random", 20_000_000, 2, 3), dfm.random_dfa(20_000_000, 2, 3, 0.5)),
+                    (("vlts", 1000, 20_000_000, 4), G.vlts_dfa(1000, 20_000_000, 4))):
+        out = run(*args, 1)
+        r = eng.sort_pr(d)
+        assert (out["blocks"], out["passes"]) == (r.partition.num_blocks, r.stats.iterations)
+        assert out["partition_digest"] == part_digest(r.partition.block), args

@@ -105,10 +105,14 @@ int main(int argc, char** argv) {
     best = std::min(best, ms);
     sum += ms;
   }
+  // partition digest: sum of block[i] * (2654435761 * i + 1) mod 2^64 (numpy-checkable)
+  uint64_t ph = 0;
+  for (size_t i = 0; i < r.partition.block.size(); ++i)
+    ph += (uint64_t)r.partition.block[i] * (2654435761ull * i + 1ull);
   std::printf("{\"input\": \"%s\", \"digest\": \"%016llx\", \"n\": %u, \"k\": %u, \"passes\": %llu, \"blocks\": %u, "
-              "\"ms_min\": %.3f, \"ms_mean\": %.3f, \"reps\": %d, \"status\": %d}\n",
+              "\"ms_min\": %.3f, \"ms_mean\": %.3f, \"reps\": %d, \"status\": %d, \"partition_digest\": \"%016llx\"}\n",
               what.c_str(), (unsigned long long)h, d.num_states, d.alphabet_size,
               (unsigned long long)r.stats.iterations, r.partition.num_blocks, best, sum / reps, reps,
-              (int)r.stats.status);
+              (int)r.stats.status, (unsigned long long)ph);
   return r.stats.status == dfamin::RunStatus::ok ? 0 : 1;
 }
