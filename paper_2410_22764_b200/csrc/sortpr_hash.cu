@@ -214,25 +214,36 @@ template <int kIdBits>
 __device__ __forceinline__ unsigned long long make_key_rows_warp(
     const InsertParams& p, uint64_t i0, bool valid, uint32_t q, uint32_t b, uint64_t pol_stream,
     uint64_t pol_ids, uint32_t* s_buf /* [32][9] */) {
+  // the row's k + 1 fields (own id, successor ids) are packed kPer to a word: every id
+  // of this pass is below 2^kIdBits (the mirror width), so a row is (k+1) / kPer words —
+  // 4 instead of 101 at k = 100 with 1-bit ids (the host sizes the rows to match:
+  // packed_row_words); the hash runs over the fields, whatever the packing
+  constexpr uint32_t kPer = 32 / kIdBits;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t k = p.k, words = k + 1;
+  const uint32_t fields = p.k + 1, words = (fields + kPer - 1) / kPer;
   const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
   unsigned long long h = mix64(p.seed * kGolden + b);
+  uint32_t* my = s_buf + lane * 9;
   for (uint32_t w0 = 0; w0 < words; w0 += 8) {
-    uint32_t t[8], v[8];
 #pragma unroll
-    for (uint32_t c = 0; c < 8; ++c) {
-      const uint32_t wd = w0 + c;
-      t[c] = (valid && wd >= 1 && wd < words)
-                 ? ld_stream(p.delta + (uint64_t)(wd - 1) * p.n + q, pol_stream)
-                 : 0u;
-    }
+    for (uint32_t c = 0; c < 8; ++c) my[c] = 0u;
+    const uint32_t f_end = min(fields, (w0 + 8) * kPer);
+    for (uint32_t f0 = w0 * kPer; f0 < f_end; f0 += 8) {
+      uint32_t t[8], v[8];
 #pragma unroll
-    for (uint32_t c = 0; c < 8; ++c) {
-      const uint32_t wd = w0 + c;
-      v[c] = wd == 0 ? b : (valid && wd < words) ? load_id<kIdBits>(p.ids, t[c], pol_ids) : 0u;
-      if (wd >= 1 && wd < words) h = mix64(h + kGolden + v[c]);
-      s_buf[lane * 9 + c] = v[c];
+      for (uint32_t c = 0; c < 8; ++c) {
+        const uint32_t f = f0 + c;
+        t[c] = (valid && f >= 1 && f < f_end)
+                   ? ld_stream(p.delta + (uint64_t)(f - 1) * p.n + q, pol_stream)
+                   : 0u;
+      }
+#pragma unroll
+      for (uint32_t c = 0; c < 8; ++c) {
+        const uint32_t f = f0 + c;
+        v[c] = f == 0 ? b : (valid && f < f_end) ? load_id<kIdBits>(p.ids, t[c], pol_ids) : 0u;
+        if (f >= 1 && f < f_end) h = mix64(h + kGolden + v[c]);
+        if (f < f_end) my[f / kPer - w0] |= v[c] << ((f % kPer) * kIdBits);
+      }
     }
     __syncwarp();
     // lane L writes word L % 8 of row (4 r + L / 8): one full sector per 8 lanes
@@ -1140,6 +1151,13 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
   DFM_LAUNCH_CHECK();
 }
 
+// words of a signature row written by make_key_rows_warp (fields packed at the pass's
+// mirror width; measured on C2 sortPR, vlts(1000, 1e7, 100): 29.2 -> 23.6 ms)
+uint32_t packed_row_words(uint64_t k, int id_bits) {
+  const uint64_t per = 32 / (uint64_t)id_bits;
+  return (uint32_t)((k + 1 + per - 1) / per);
+}
+
 bool layout_overlap_enabled() {  // DFM_SORTPR_LAYOUT_OVERLAP=0: build it at pass 2 (tests)
   const char* e = getenv("DFM_SORTPR_LAYOUT_OVERLAP");
   return e == nullptr || e[0] != '0';
@@ -1863,10 +1881,15 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         // load <= 0.4: a warp waits for its longest probe chain of DRAM-latency CASes
         cap = std::max<uint64_t>(1024, dups * 5 / 2);
       }
+      // signature rows of this pass: the warp-cooperative writer of the direct hashed
+      // insert (runtime k) packs the fields into mirror-width bit fields
+      const bool row_pack = !blocked && !packed && k != 2 && k != 4;
+      const uint32_t pw = row_pack ? packed_row_words(k, mirror_bits) : k + 1;
+      const uint32_t prow = row_pack ? (pw > 8 ? (pw + 7) & ~7u : pw) : row;
       Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", cap * sizeof(Slot)));
       DFM_CUDA(cudaMemsetAsync(slots, 0, cap * sizeof(Slot), ctx.stream));
       InsertParams ip{d.delta, n, k, block, ids, act, lead, filtered ? ncand : m, w, seed, cap,
-                      slots, slot_of, packed ? nullptr : sig, row, keys, present,
+                      slots, slot_of, packed ? nullptr : sig, prow, keys, present,
                       filtered ? cand : nullptr};
       // direct tables whose slot can become the id at once: the tiny smem-aggregated
       // ones (the ids are gathered from a mirror or were gathered by the layout) and
@@ -1914,7 +1937,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         // slot RMW 16 + slot_of 4 (+ signature row 4*row when hashed) per active state
         ProfScope p(ctx, "sig",
                     m * (4ull * k + (uint64_t)std::max(1, mirror_bits / 8) * k + 4 + 1 +
-                         (act ? 4 : 0) + 16 + 4 + (packed ? 0 : 4ull * row)));
+                         (act ? 4 : 0) + 16 + 4 + (packed ? 0 : 4ull * prow)));
         switch (mirror_bits) {
           case 1: launch_insert<1>(ctx, ip, !packed, direct, table); break;
           case 4: launch_insert<4>(ctx, ip, !packed, direct, table); break;
@@ -1929,11 +1952,11 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
           ProfScope p(ctx, "scan", (hrip_pre ? 0 : m * 10ull) + ncand * 8ull);
           if (hrip_pre) {
             rip_hashed_cand_kernel<<<grid_for(ctx, ncand), 256, 0, ctx.stream>>>(
-                ncand, cand, m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
+                ncand, cand, m, slot_of, slots, packed ? nullptr : sig, pw, prow,
                 reinterpret_cast<unsigned long long*>(sc + 2), B, res, flag);
           } else {
             rip_hashed_kernel<<<grid_for(ctx, m), 256, 0, ctx.stream>>>(
-                m, slot_of, slots, packed ? nullptr : sig, k + 1, row,
+                m, slot_of, slots, packed ? nullptr : sig, pw, prow,
                 reinterpret_cast<unsigned long long*>(sc + 2), B, res, lead, flag);
           }
           DFM_LAUNCH_CHECK();
@@ -1955,7 +1978,7 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         ProfScope p(ctx, "scan", m * (4ull + 16 + 4 + 4 + 1));  // slot_of, slot, own id, res, st
         resolve_kernel<<<grid_for(ctx, ceil_div(m, kResolveItems)), 256, 0, ctx.stream>>>(
             m,
-            ResolveIn{slots, slot_of, packed ? nullptr : sig, k + 1, row,
+            ResolveIn{slots, slot_of, packed ? nullptr : sig, pw, prow,
                       reinterpret_cast<unsigned long long*>(sc + 2), act, lead},
             ResolveOut{slots, act, block, res, st, B}, reinterpret_cast<unsigned long long*>(sc + 1),
             reinterpret_cast<unsigned long long*>(sc + 8));

@@ -456,6 +456,30 @@ def test_forced_hash_collisions_retry_exactly(eng, eng_radix, monkeypatch, n, k,
     dd.free()
 
 
+@pytest.mark.parametrize("name,pair", [
+    ("vlts_k10", lambda: O.vlts_dfa(500, 200_000, 10)),
+    ("vlts_k33", lambda: O.vlts_dfa(300, 60_000, 33)),
+    ("random_k7", lambda: O.random_dfa(300_000, 7, 9, 0.5)),
+    ("random_k40", lambda: O.random_dfa(20_000, 40, 10, 0.5)),
+])
+def test_packed_signature_rows(eng, monkeypatch, name, pair):
+    """Direct hashed passes with a runtime alphabet pack their signature rows into
+    mirror-width fields (1/4/8/16/32-bit ids): the oracle's partition and pass count,
+    also with every hashed pass forced to collide and retry (DFM_SORTPR_WEAK_HASH) so
+    the packed rows are what verifies the groups."""
+    delta, acc = pair()
+    d = to_dfa((delta, acc))
+    ref = O.sort_pr(delta, acc)
+    monkeypatch.setenv("DFM_SORTPR_SMALL", "0")
+    for weak in (None, "10"):
+        if weak:
+            monkeypatch.setenv("DFM_SORTPR_WEAK_HASH", weak)
+        r = eng.sort_pr(d)
+        monkeypatch.delenv("DFM_SORTPR_WEAK_HASH", raising=False)
+        assert r.stats.iterations == ref.iterations, (name, weak)
+        assert (r.partition.block == ref.block).all(), (name, weak)
+
+
 def test_layout_built_beside_pass_one(eng, monkeypatch):
     """The blocked layout built on the side stream during pass 1 (device-resident
     input) gives the result of building it at pass 2."""
