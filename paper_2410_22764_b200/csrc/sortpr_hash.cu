@@ -1152,7 +1152,9 @@ void launch_insert_keys(Ctx& ctx, const InsertParams& p, bool hashed, bool direc
 }
 
 // words of a signature row written by make_key_rows_warp (fields packed at the pass's
-// mirror width; measured on C2 sortPR, vlts(1000, 1e7, 100): 29.2 -> 23.6 ms)
+// mirror width; measured on C2 sortPR, vlts(1000, 1e7, 100): 29.2 -> 23.6 ms,
+// profiles/r04/r04l.  Bit-exact packing at bits(B - 1) — 32 instead of 51 words at
+// 10-bit ids — wrote less but cost more instructions per field: 31.4 ms, r04o)
 uint32_t packed_row_words(uint64_t k, int id_bits) {
   const uint64_t per = 32 / (uint64_t)id_bits;
   return (uint32_t)((k + 1 + per - 1) / per);
@@ -1882,8 +1884,9 @@ AlgoOut run_sort_pr_hash(Ctx& ctx, const DevDfa& d, const Deadline& dl, const df
         cap = std::max<uint64_t>(1024, dups * 5 / 2);
       }
       // signature rows of this pass: the warp-cooperative writer of the direct hashed
-      // insert (runtime k) packs the fields into mirror-width bit fields
-      const bool row_pack = !blocked && !packed && k != 2 && k != 4;
+      // insert (runtime k: launch_insert compiles k = 1..4) packs the fields at the
+      // mirror width
+      const bool row_pack = !blocked && !packed && k > 4;
       const uint32_t pw = row_pack ? packed_row_words(k, mirror_bits) : k + 1;
       const uint32_t prow = row_pack ? (pw > 8 ? (pw + 7) & ~7u : pw) : row;
       Slot* slots = static_cast<Slot*>(ctx.slot("sh.table", cap * sizeof(Slot)));

@@ -461,10 +461,13 @@ def test_forced_hash_collisions_retry_exactly(eng, eng_radix, monkeypatch, n, k,
     ("vlts_k33", lambda: O.vlts_dfa(300, 60_000, 33)),
     ("random_k7", lambda: O.random_dfa(300_000, 7, 9, 0.5)),
     ("random_k40", lambda: O.random_dfa(20_000, 40, 10, 0.5)),
+    ("random_k5", lambda: O.random_dfa(300_000, 5, 12, 0.5)),
+    ("random_k3", lambda: O.random_dfa(300_000, 3, 11, 0.5)),  # compile-time k: rows unpacked
 ])
 def test_packed_signature_rows(eng, monkeypatch, name, pair):
-    """Direct hashed passes with a runtime alphabet pack their signature rows into
-    mirror-width fields (1/4/8/16/32-bit ids): the oracle's partition and pass count,
+    """Direct hashed passes with a runtime alphabet (k > 4) pack their signature rows
+    at the pass's mirror width (1/4/8/16/32-bit fields); compile-time alphabets
+    (k <= 4) keep one word per field: the oracle's partition and pass count,
     also with every hashed pass forced to collide and retry (DFM_SORTPR_WEAK_HASH) so
     the packed rows are what verifies the groups."""
     delta, acc = pair()
