@@ -261,9 +261,17 @@ __device__ __forceinline__ unsigned long long make_key_rows_warp(
 // K1, hash or large direct table; warp-level aggregation of equal slots
 constexpr uint32_t kUnique = 0xFFFFFFFFu;  // slot_of mark: key seen once (filtered)
 
+// runtime-k hashed inserts are gather-latency bound: at 79 registers only 3 CTAs (24
+// warps) fit an SM; capped for DFM_INS_MINB CTAs per SM.  Measured on C2 sortPR
+// vlts(1000, 1e7, 100) (profiles/r04/r04r-s): 3 CTAs 23.6 ms, 4: 22.4, 5: 22.0,
+// 6: 20.9, 7: 23.3, 8: 23.4; vlts(1000, 1e7, 10): 4: 5.47, 6: 5.29, 8: 5.82
+#ifndef DFM_INS_MINB
+#define DFM_INS_MINB 6
+#endif
 template <int kIdBits, bool kHashed, bool kDirect, int kK, bool kFromKeys = false,
           bool kFilter = false>
-__global__ void __launch_bounds__(256) insert_kernel(InsertParams p) {
+__global__ void __launch_bounds__(256, (kHashed && kK == 0 && !kFromKeys && !kFilter) ? DFM_INS_MINB : 1)
+    insert_kernel(InsertParams p) {
   // large runtime alphabets with hashed keys: warp-cooperative coalesced row writes
   constexpr bool kRowsWarp = kHashed && kK == 0 && !kFromKeys && !kFilter;
   __shared__ uint32_t s_rows[kRowsWarp ? 8 * 32 * 9 : 1];
