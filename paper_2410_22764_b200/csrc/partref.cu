@@ -352,12 +352,8 @@ __device__ __forceinline__ uint32_t label_on_the_fly(uint32_t w, const unsigned 
 // kMask: the letter-mask variant (launched once the masks exist; the plain variants
 // keep their code: the extra paths doubled the latency-bound C1 kernel's SASS and
 // slowed it 43 %)
-#ifndef DFM_FUSED_MINB  // CTAs per SM of the grid-stride / dynamic-row instances
-#define DFM_FUSED_MINB 1
-#endif
 template <int kPolicy, bool kOne, bool kMask = false>
-__global__ void __launch_bounds__(kPersistThreads, kOne ? 1 : DFM_FUSED_MINB)
-    fused_pr_kernel(FusedArgs a) {
+__global__ void __launch_bounds__(kPersistThreads) fused_pr_kernel(FusedArgs a) {
   cg::grid_group g = cg::this_grid();
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
