@@ -102,3 +102,41 @@ def test_pinned_and_pageable_rows_give_the_same_result(eng):
         dd2 = eng.upload(d)
         assert _device_result(eng, dd2, n)[2].tolist()[:1000] == lab.tolist()[:1000]
         dd2.free()
+
+
+def test_concurrent_pageable_uploads_share_the_copy_pool(eng):
+    """Two contexts on two host threads minimizing pageable DFAs at the same time: their
+    staging copies take turns on the process's one host copy pool (capi.cu HostPool);
+    each result equals its device-resident run.  A vlts input (non-identity partition,
+    D2H) beside a random one (identity labels written by the speculative thread)."""
+    import threading
+    from paper_2410_22764_b200 import generators as G
+    n1, k1 = 17_000_001, 4
+    dd = eng.random_dfa_device(n1, k1, 41, 0.5)
+    want1 = _device_result(eng, dd, n1)
+    a = dd.download()
+    dd.free()
+    b = G.vlts_dfa(1000, 8_000_000, 6)
+    db = eng.upload(b)
+    want2 = _device_result(eng, db, b.num_states)
+    db.free()
+    engines = [eng, dfm.Engine(0)]
+    got = [None, None]
+    errs = []
+
+    def run(i, d):
+        try:
+            for _ in range(2):
+                got[i] = engines[i].sort_pr(d)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(0, a)), threading.Thread(target=run, args=(1, b))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for r, (nb, it, lab) in zip(got, (want1, want2)):
+        assert (r.partition.num_blocks, r.stats.iterations) == (nb, it)
+        assert (r.partition.block == lab).all()
